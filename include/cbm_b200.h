@@ -1,0 +1,190 @@
+/*
+ * cbm_b200.h — C ABI of the B200-native CBM multiply (drop-in for the hot path
+ * of arXiv 2409.02208's reference library, /root/reference/proj).
+ *
+ * Plain pointers and sizes only; no torch, no C++ types. Every entry point
+ * names the reference interface it replaces (file:line under
+ * /root/reference/proj). The reference-side C++ adapter that keeps the
+ * reference signatures (cbm::spmm_into(const CbmMatrix&, ...)) is
+ * include/cbm_b200_shim.hpp; INTEGRATION.md shows how a maintainer binds it.
+ *
+ * Error model (mirrors the reference's exceptions, kernels.cpp:11-14,107-109):
+ * every int-returning call returns CBM_B200_OK or a status below and sets a
+ * thread-local message readable with cbm_b200_last_error(). EINVAL carries the
+ * reference's exact std::invalid_argument text ("spmm: inner dimensions
+ * differ", "spmm: output has the wrong shape", ...).
+ */
+#ifndef CBM_B200_H_
+#define CBM_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  CBM_B200_OK = 0,
+  CBM_B200_EINVAL = 1,   /* std::invalid_argument in the reference */
+  CBM_B200_ECUDA = 2,    /* CUDA runtime / launch failure */
+  CBM_B200_ENOMEM = 3,   /* host or device allocation failure */
+  CBM_B200_ELOGIC = 4    /* std::logic_error in the reference (builder) */
+};
+
+#define CBM_B200_VIRTUAL_PARENT 0xFFFFFFFFu /* kVirtualParent, types.hpp:19 */
+
+/* Borrowed view of a pattern CSR matrix (CsrBinaryMatrix, csr.hpp:14-40):
+ * row_ptr has n_rows+1 entries, columns strictly increasing per row. */
+typedef struct cbm_b200_csr_view {
+  uint32_t n_rows;
+  uint32_t n_cols;
+  const uint64_t* row_ptr;
+  const uint32_t* col_idx;
+} cbm_b200_csr_view;
+
+/* Borrowed view of a built CBM (CbmMatrix, builder.hpp:66-74; f32 build,
+ * real_t = float). values are +-1 (plain) or +-row_scale[col] (normalized),
+ * exactly as build_cbm / build_cbm_normalized (builder.cpp:394-429) and
+ * load_cbm (io.cpp:369-380) guarantee. topo_order may be NULL. */
+typedef struct cbm_b200_cbm_view {
+  uint32_t n_rows;
+  uint32_t n_cols;
+  uint64_t nnz;          /* delta_matrix.nnz() */
+  uint64_t alpha;
+  int32_t is_normalized;
+  const uint32_t* parent;      /* chain.parent[n_rows] */
+  const uint32_t* topo_order;  /* chain.topo_order[n_rows] or NULL */
+  const uint64_t* row_ptr;     /* delta_matrix.row_ptr[n_rows+1] */
+  const uint32_t* col_idx;     /* delta_matrix.col_idx[nnz] */
+  const float* values;         /* delta_matrix.values[nnz] */
+  const float* row_scale;      /* row_scale[n_rows] (normalized) or NULL */
+} cbm_b200_cbm_view;
+
+/* ------------------------------------------------------------------------
+ * Host construction (stays on the host, timed separately).
+ * Replaces build_cbm (builder.hpp:99, builder.cpp:394-404) and
+ * build_cbm_normalized (builder.hpp:104-106, builder.cpp:406-429). The result
+ * is field-for-field identical to the reference builder's (same chain, same
+ * delta matrix, same row_scale bits); see DESIGN.md §Builder.
+ * degree_mode: 0 = DegreeMode::augmented, 1 = DegreeMode::original.
+ * --------------------------------------------------------------------- */
+typedef struct cbm_b200_host_cbm cbm_b200_host_cbm;
+
+int cbm_b200_build(const cbm_b200_csr_view* a, uint64_t alpha, int32_t normalized,
+                   int32_t degree_mode, int32_t threads, cbm_b200_host_cbm** out);
+/* Borrowed view of a built CBM; valid until cbm_b200_host_free. */
+int cbm_b200_host_view(const cbm_b200_host_cbm* c, cbm_b200_cbm_view* out);
+/* chain.branch_ptr (builder.hpp:38-40): n_branches+1 entries. */
+int cbm_b200_host_branches(const cbm_b200_host_cbm* c, const uint64_t** branch_ptr,
+                           uint64_t* n_branches);
+/* Build statistics: seconds per phase and the candidate-edge count. */
+typedef struct cbm_b200_build_stats {
+  double t_edges, t_arborescence, t_deltas, t_total;
+  uint64_t candidate_edges;
+  uint32_t rounds;
+} cbm_b200_build_stats;
+int cbm_b200_host_stats(const cbm_b200_host_cbm* c, cbm_b200_build_stats* out);
+void cbm_b200_host_free(cbm_b200_host_cbm* c);
+
+/* count_scalar_ops (kernels.hpp:22, kernels.cpp:66-68). */
+int cbm_b200_count_ops(const cbm_b200_cbm_view* c, uint64_t* multiply_adds,
+                       uint64_t* update_adds);
+
+/* ------------------------------------------------------------------------
+ * Device operator: the CBM uploaded once into the level-ordered device layout
+ * (DESIGN.md §Layout). Immutable after upload. Calls on one handle must be
+ * issued on one stream at a time (the handle owns its per-call workspace).
+ * --------------------------------------------------------------------- */
+typedef struct cbm_b200_matrix cbm_b200_matrix;
+
+typedef struct cbm_b200_options {
+  int32_t device;            /* CUDA device ordinal (-1 = current) */
+  int32_t order_faithful;    /* 1: every row summed in the reference's exact
+                                order (bit-identical for ANY X); 0: rows longer
+                                than split_threshold are split into chunks summed
+                                in a fixed tree order (bit-exact on integer X,
+                                ~1 ulp-level on Gaussian X) */
+  uint32_t split_threshold;  /* deltas per row before splitting (0 = default) */
+  uint32_t chunk;            /* deltas per chunk (0 = default) */
+  int32_t prescale;          /* normalized only: -1 auto, 0 off, 1 pre-scale X
+                                by row_scale once per call (bit-identical
+                                products, removes the per-delta FMUL) */
+} cbm_b200_options;
+
+void cbm_b200_default_options(cbm_b200_options* opt);
+
+/* Upload (the device counterpart of holding a CbmMatrix). Validates the
+ * structure like load_cbm does (io.cpp:346-380): parent range/acyclicity,
+ * row_ptr monotonicity, column range, value pattern. Host arrays are borrowed
+ * only for the duration of the call. */
+int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
+                    cbm_b200_matrix** out);
+void cbm_b200_free(cbm_b200_matrix* h);
+
+/* Y = A X on device memory (spmm_into, kernels.hpp:36-39, kernels.cpp:105-123).
+ * X is x_rows x x_cols row-major with leading dimension ldx (floats); Y is
+ * y_rows x y_cols with leading dimension ldy; Y is fully overwritten. A column
+ * slab of a wider matrix is passed as (base + c0, ldx = full width). Async on
+ * `stream` (a cudaStream_t; NULL = legacy default stream). */
+int cbm_b200_spmm(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_cols,
+                  int64_t ldx, float* y, int64_t y_rows, int64_t y_cols, int64_t ldy,
+                  void* stream);
+
+/* Same with HOST buffers (the drop-in for spmm_into on DenseMatrix data):
+ * H2D of X, the multiply, D2H of Y, then a stream synchronize. Pinned host
+ * memory gives full-bandwidth copies; pageable memory works too. */
+int cbm_b200_spmm_host(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_cols,
+                       float* y, int64_t y_rows, int64_t y_cols, void* stream);
+
+/* u = A v (spmv_into, kernels.hpp:41-44, kernels.cpp:70-97): v is n_cols x 1. */
+int cbm_b200_spmv(cbm_b200_matrix* h, const float* v, int64_t v_rows, int64_t v_cols,
+                  float* u, int64_t u_rows, int64_t u_cols, void* stream);
+
+/* Pre-size the per-call workspace for up to d_max columns so later calls
+ * never allocate (the device analogue of Property 3, kernels.hpp:36-39). */
+int cbm_b200_reserve(cbm_b200_matrix* h, int64_t d_max);
+
+typedef struct cbm_b200_info {
+  uint32_t n_rows, n_cols;
+  uint64_t nnz_delta;        /* delta entries (after layout) */
+  uint32_t n_levels;         /* depth of the compression forest */
+  uint32_t n_roots;
+  uint32_t n_interior;       /* rows with at least one child */
+  uint32_t n_items;          /* work items per column slab */
+  uint32_t n_chunk_items;    /* split-row chunks per column slab */
+  uint32_t max_row_deltas;
+  uint64_t device_bytes;     /* structure bytes resident on the device */
+  uint32_t launches_per_call;/* kernels launched by the last spmm call */
+  int32_t is_normalized;
+  int32_t order_faithful;
+} cbm_b200_info;
+int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* out);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* cbm_b200_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * Seeded workload generators (bench / test infrastructure). Streams follow the
+ * reference's UniformRng (prng.hpp:11-28: mt19937_64, unit() = 53-bit,
+ * below(n) = modulo) so CPU and GPU runs see identical inputs.
+ * --------------------------------------------------------------------- */
+typedef struct cbm_b200_csr cbm_b200_csr;
+/* kind: "community" (p = {n, communities, p_in, p_out}),
+ *       "pa_triangle" (p = {n, m, p_triangle}),
+ *       "clique_overlay" (p = {n, groups, k_min, k_max, zipf_s}),
+ *       "random_binary" (p = {rows, cols, density}) — oracles.hpp:167-175. */
+int cbm_b200_gen_graph(const char* kind, const double* params, int32_t n_params,
+                       uint64_t seed, cbm_b200_csr** out);
+int cbm_b200_csr_get(const cbm_b200_csr* a, cbm_b200_csr_view* out);
+void cbm_b200_csr_free(cbm_b200_csr* a);
+/* Dense fills: kind 0 = uniform [lo,hi) (random_dense, dense.cpp:56-62),
+ * 1 = integers below(hi-lo+1)+lo, 2 = N(0,1) Box-Muller (lo/hi unused),
+ * 3 = Glorot-uniform for a lo x hi (fan_in x fan_out) weight. */
+int cbm_b200_gen_dense(int32_t kind, uint64_t rows, uint64_t cols, double lo, double hi,
+                       uint64_t seed, float* out);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* CBM_B200_H_ */

@@ -1,0 +1,314 @@
+// extern "C" boundary (include/cbm_b200.h). Exceptions never cross it: each
+// entry point maps them onto a status code plus a thread-local message, the
+// way the reference raises std::invalid_argument / std::logic_error.
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/cbm_b200.h"
+#include "cbm_host.hpp"
+#include "device.hpp"
+
+struct cbm_b200_host_cbm {
+  cbmb::HostCbm c;
+};
+struct cbm_b200_matrix {
+  cbmb::DeviceMatrix* d;
+};
+struct cbm_b200_csr {
+  cbmb::Csr a;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    g_err.clear();
+    f();
+    return CBM_B200_OK;
+  } catch (const cbmb::invalid_argument& e) {
+    g_err = e.what();
+    return CBM_B200_EINVAL;
+  } catch (const cbmb::logic_error& e) {
+    g_err = e.what();
+    return CBM_B200_ELOGIC;
+  } catch (const cbmb::cuda_error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return CBM_B200_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CBM_B200_ELOGIC;
+  }
+}
+
+void need(bool ok, const char* msg) {
+  if (!ok) throw cbmb::invalid_argument(msg);
+}
+
+// Shape checks of kernels.cpp:11-14,107-109 (messages verbatim).
+void check_spmm_shapes(const cbmb::Layout& L, int64_t x_rows, int64_t x_cols, int64_t y_rows,
+                       int64_t y_cols, const char* who) {
+  if (x_rows != int64_t(L.n_cols))
+    throw cbmb::invalid_argument(std::string(who) + ": inner dimensions differ");
+  if (y_rows != int64_t(L.n_rows) || y_cols != x_cols)
+    throw cbmb::invalid_argument(std::string(who) + ": output has the wrong shape");
+  if (x_cols < 0 || x_cols > 0x7FFFFFFF)
+    throw cbmb::invalid_argument(std::string(who) + ": bad column count");
+}
+}  // namespace
+
+extern "C" {
+
+const char* cbm_b200_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ builder
+int cbm_b200_build(const cbm_b200_csr_view* a, uint64_t alpha, int32_t normalized,
+                   int32_t degree_mode, int32_t threads, cbm_b200_host_cbm** out) {
+  return guard([&] {
+    need(a && out, "build: null argument");
+    *out = nullptr;
+    need(a->row_ptr != nullptr, "build: null row_ptr");
+    cbmb::validate_csr(a->n_rows, a->n_cols, a->row_ptr, a->col_idx);
+    cbmb::Csr csr;
+    csr.n_rows = a->n_rows;
+    csr.n_cols = a->n_cols;
+    csr.row_ptr.assign(a->row_ptr, a->row_ptr + size_t(a->n_rows) + 1);
+    csr.col_idx.assign(a->col_idx, a->col_idx + csr.row_ptr.back());
+    const int t = threads > 0 ? threads : 1;
+    auto* h = new cbm_b200_host_cbm;
+    try {
+      h->c = normalized ? cbmb::build_cbm_normalized(csr, alpha, t, degree_mode == 1)
+                        : cbmb::build_cbm(csr, alpha, t);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int cbm_b200_host_view(const cbm_b200_host_cbm* h, cbm_b200_cbm_view* v) {
+  return guard([&] {
+    need(h && v, "host_view: null argument");
+    const auto& c = h->c;
+    v->n_rows = c.n_rows;
+    v->n_cols = c.n_cols;
+    v->nnz = c.row_ptr.back();
+    v->alpha = c.alpha;
+    v->is_normalized = c.normalized ? 1 : 0;
+    v->parent = c.parent.data();
+    v->topo_order = c.topo_order.data();
+    v->row_ptr = c.row_ptr.data();
+    v->col_idx = c.col_idx.data();
+    v->values = c.values.data();
+    v->row_scale = c.normalized ? c.row_scale.data() : nullptr;
+  });
+}
+
+int cbm_b200_host_branches(const cbm_b200_host_cbm* h, const uint64_t** bp, uint64_t* nb) {
+  return guard([&] {
+    need(h && bp && nb, "host_branches: null argument");
+    *bp = h->c.branch_ptr.data();
+    *nb = h->c.root_children.size();
+  });
+}
+
+int cbm_b200_host_stats(const cbm_b200_host_cbm* h, cbm_b200_build_stats* s) {
+  return guard([&] {
+    need(h && s, "host_stats: null argument");
+    s->t_edges = h->c.t_edges;
+    s->t_arborescence = h->c.t_arb;
+    s->t_deltas = h->c.t_deltas;
+    s->t_total = h->c.t_total;
+    s->candidate_edges = h->c.candidate_edges;
+    s->rounds = h->c.rounds;
+  });
+}
+
+void cbm_b200_host_free(cbm_b200_host_cbm* h) { delete h; }
+
+int cbm_b200_count_ops(const cbm_b200_cbm_view* c, uint64_t* mult, uint64_t* upd) {
+  return guard([&] {
+    need(c && mult && upd, "count_ops: null argument");
+    *mult = c->nnz;
+    uint64_t non_virtual = 0;
+    for (uint32_t x = 0; x < c->n_rows; ++x) non_virtual += c->parent[x] != cbmb::kVirtual;
+    *upd = non_virtual;
+  });
+}
+
+// ------------------------------------------------------------------ device
+void cbm_b200_default_options(cbm_b200_options* o) {
+  if (!o) return;
+  o->device = -1;
+  o->order_faithful = 0;
+  o->split_threshold = 0;
+  o->chunk = 0;
+  o->prescale = -1;
+}
+
+int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
+                    cbm_b200_matrix** out) {
+  return guard([&] {
+    need(c && out, "upload: null argument");
+    *out = nullptr;
+    cbm_b200_options o;
+    cbm_b200_default_options(&o);
+    if (opt) o = *opt;
+    auto* h = new cbm_b200_matrix{nullptr};
+    try {
+      h->d = cbmb::device_upload(*c, o);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void cbm_b200_free(cbm_b200_matrix* h) {
+  if (!h) return;
+  cbmb::device_free(h->d);
+  delete h;
+}
+
+int cbm_b200_reserve(cbm_b200_matrix* h, int64_t d_max) {
+  return guard([&] {
+    need(h && d_max >= 0, "reserve: bad argument");
+    std::lock_guard<std::mutex> lk(h->d->mu);
+    cbmb::device_reserve(h->d, uint64_t(d_max));
+  });
+}
+
+int cbm_b200_spmm(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_cols,
+                  int64_t ldx, float* y, int64_t y_rows, int64_t y_cols, int64_t ldy,
+                  void* stream) {
+  return guard([&] {
+    need(h != nullptr, "spmm: null handle");
+    check_spmm_shapes(h->d->info, x_rows, x_cols, y_rows, y_cols, "spmm");
+    need(ldx >= x_cols && ldy >= y_cols, "spmm: leading dimension smaller than the width");
+    need((x || x_rows * x_cols == 0) && (y || y_rows * y_cols == 0), "spmm: null data");
+    std::lock_guard<std::mutex> lk(h->d->mu);
+    cbmb::device_spmm(h->d, x, ldx, uint32_t(x_cols), y, ldy, stream);
+  });
+}
+
+int cbm_b200_spmm_host(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_cols,
+                       float* y, int64_t y_rows, int64_t y_cols, void* stream) {
+  return guard([&] {
+    need(h != nullptr, "spmm: null handle");
+    check_spmm_shapes(h->d->info, x_rows, x_cols, y_rows, y_cols, "spmm");
+    need((x || x_rows * x_cols == 0) && (y || y_rows * y_cols == 0), "spmm: null data");
+    std::lock_guard<std::mutex> lk(h->d->mu);
+    cbmb::device_spmm_host(h->d, x, uint32_t(x_cols), y, stream);
+  });
+}
+
+int cbm_b200_spmv(cbm_b200_matrix* h, const float* v, int64_t v_rows, int64_t v_cols, float* u,
+                  int64_t u_rows, int64_t u_cols, void* stream) {
+  return guard([&] {
+    need(h != nullptr, "spmv: null handle");
+    const auto& L = h->d->info;
+    // kernels.cpp:72-76
+    if (v_rows != int64_t(L.n_cols)) throw cbmb::invalid_argument("spmv: inner dimensions differ");
+    if (v_cols != 1) throw cbmb::invalid_argument("spmv: operand must be a single column");
+    if (u_rows != int64_t(L.n_rows) || u_cols != 1)
+      throw cbmb::invalid_argument("spmv: output must be n_rows x 1");
+    std::lock_guard<std::mutex> lk(h->d->mu);
+    cbmb::device_spmm(h->d, v, 1, 1, u, 1, stream);
+  });
+}
+
+int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* o) {
+  return guard([&] {
+    need(h && o, "info: null argument");
+    const auto& L = h->d->info;
+    o->n_rows = L.n_rows;
+    o->n_cols = L.n_cols;
+    o->nnz_delta = L.nnz;
+    o->n_levels = L.n_levels;
+    o->n_roots = L.n_roots;
+    o->n_interior = L.n_interior;
+    o->n_items = L.n_items;
+    o->n_chunk_items = L.n_chunk_items;
+    o->max_row_deltas = L.max_row_deltas;
+    o->device_bytes = h->d->device_bytes;
+    o->launches_per_call = h->d->last_launches;
+    o->is_normalized = L.normalized ? 1 : 0;
+    o->order_faithful = L.order_faithful ? 1 : 0;
+  });
+}
+
+// ------------------------------------------------------------------ workloads
+int cbm_b200_gen_graph(const char* kind, const double* params, int32_t n_params, uint64_t seed,
+                       cbm_b200_csr** out) {
+  return guard([&] {
+    need(kind && out && (params || n_params == 0), "gen_graph: null argument");
+    *out = nullptr;
+    std::vector<double> p(params, params + n_params);
+    auto* h = new cbm_b200_csr;
+    try {
+      h->a = cbmb::gen_graph(kind, p, seed);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int cbm_b200_csr_get(const cbm_b200_csr* a, cbm_b200_csr_view* v) {
+  return guard([&] {
+    need(a && v, "csr_get: null argument");
+    v->n_rows = a->a.n_rows;
+    v->n_cols = a->a.n_cols;
+    v->row_ptr = a->a.row_ptr.data();
+    v->col_idx = a->a.col_idx.data();
+  });
+}
+
+void cbm_b200_csr_free(cbm_b200_csr* a) { delete a; }
+
+int cbm_b200_gen_dense(int32_t kind, uint64_t rows, uint64_t cols, double lo, double hi,
+                       uint64_t seed, float* out) {
+  return guard([&] {
+    need(out || rows * cols == 0, "gen_dense: null output");
+    cbmb::Rng rng(seed);
+    const uint64_t n = rows * cols;
+    switch (kind) {
+      case 0:  // random_dense (dense.cpp:56-62)
+        for (uint64_t i = 0; i < n; ++i) out[i] = float(lo + (hi - lo) * rng.unit());
+        break;
+      case 1: {  // integers in [lo, hi]
+        const int64_t a = int64_t(lo), b = int64_t(hi);
+        need(b >= a, "gen_dense: empty integer range");
+        for (uint64_t i = 0; i < n; ++i) out[i] = float(int64_t(rng.below(uint64_t(b - a + 1))) + a);
+        break;
+      }
+      case 2:  // N(0,1), Box–Muller over two unit() draws, double then f32
+        for (uint64_t i = 0; i < n; i += 2) {
+          const double u1 = rng.unit(), u2 = rng.unit();
+          const double r = std::sqrt(-2.0 * std::log1p(-u1));
+          const double th = 6.283185307179586 * u2;
+          out[i] = float(r * std::cos(th));
+          if (i + 1 < n) out[i + 1] = float(r * std::sin(th));
+        }
+        break;
+      case 3: {  // Glorot-uniform for a rows x cols (fan_in x fan_out) weight
+        const double b = std::sqrt(6.0 / double(rows + cols));
+        for (uint64_t i = 0; i < n; ++i) out[i] = float(-b + 2.0 * b * rng.unit());
+        break;
+      }
+      default:
+        throw cbmb::invalid_argument("gen_dense: unknown kind");
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+// Device-resident CBM operator (host-side handle; implementation in
+// cbm_kernels.cu).
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "errors.hpp"
+#include "layout.hpp"
+
+namespace cbmb {
+
+struct DeviceMatrix {
+  int device = 0;
+  int num_sms = 148;
+  Layout info;  // sizes only after upload (host vectors released)
+  cbm_b200_options opt{};
+  // structure (immutable)
+  uint32_t* dptr = nullptr;
+  uint32_t* dcol = nullptr;
+  uint32_t* meta = nullptr;
+  uint32_t* oslot = nullptr;
+  float* scale = nullptr;
+  uint64_t device_bytes = 0;
+  // per-call workspace (grown on demand, or by cbm_b200_reserve)
+  uint32_t* counters = nullptr;  // [0] ticket, [1] exit count (self-resetting)
+  uint32_t* flags = nullptr;
+  uint64_t flags_cap = 0;        // entries
+  float* partial = nullptr;
+  uint64_t partial_cap = 0;      // floats
+  float* interior = nullptr;
+  uint64_t interior_cap = 0;
+  float* xs = nullptr;           // pre-scaled operand (normalized, prescale on)
+  uint64_t xs_cap = 0;
+  float* xstage = nullptr;       // host-API staging
+  uint64_t xstage_cap = 0;
+  float* ystage = nullptr;
+  uint64_t ystage_cap = 0;
+  uint32_t epoch = 0;
+  uint32_t last_launches = 0;
+  std::mutex mu;
+};
+
+DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& opt);
+void device_free(DeviceMatrix* h);
+void device_reserve(DeviceMatrix* h, uint64_t d);
+// Y = A X; x/y are device pointers; d = columns. Shapes already validated.
+void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
+                 int64_t ldy, void* stream);
+void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, void* stream);
+
+}  // namespace cbmb
