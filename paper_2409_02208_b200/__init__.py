@@ -128,9 +128,6 @@ def _check(rc: int):
     raise CbmError(rc, msg)
 
 
-def _ptr(a: np.ndarray) -> int | None:
-    return a.ctypes.data if a is not None and a.size else (a.ctypes.data if a is not None else None)
-
 
 # ---------------------------------------------------------------------------
 # Host containers
@@ -318,9 +315,9 @@ class DeviceCbm:
         self.is_normalized = c.is_normalized
         self.device = opt.device
 
-    def close(self):
+    def close(self, _free=_lib.cbm_b200_free):
         if getattr(self, "_h", None):
-            _lib.cbm_b200_free(self._h)
+            _free(self._h)
             self._h = None
 
     __del__ = close

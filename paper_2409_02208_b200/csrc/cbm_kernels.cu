@@ -125,6 +125,7 @@ struct Params {
   const uint32_t* __restrict__ dptr;
   const uint32_t* __restrict__ dcol;
   const uint4* __restrict__ meta;
+  const uint32_t* __restrict__ pcnt;
   const uint32_t* __restrict__ oslot;
   const float* __restrict__ scale;
   const float* __restrict__ x;
@@ -139,10 +140,18 @@ struct Params {
   uint32_t total_tickets, batch, total_warps, epoch;
 };
 
-// Stage 1 for one item: delta sum over dcol[beg, end) into acc.
-template <int V, int PF, bool SCALE>
+// Per lane: U vectors of V floats at columns col0 + u*32*V (each u is one
+// fully coalesced 32*V*4-byte segment of an X row).
+template <int V, int U>
+struct Acc {
+  typename Vec<V>::T v[U];
+};
+
+// Stage 1 for one item: delta sum over dcol[beg, end) into acc, deltas in
+// storage (ascending column) order, PF deltas x U segments in flight.
+template <int V, int U, int PF, bool SCALE>
 __device__ __forceinline__ void delta_sum(const Params& p, uint32_t beg, uint32_t end,
-                                          uint32_t col, bool active, typename Vec<V>::T& acc) {
+                                          uint32_t col0, Acc<V, U>& acc) {
   using W = Vec<V>;
   const int lane = threadIdx.x & 31;
   for (uint32_t k0 = beg; k0 < end; k0 += 32) {
@@ -152,74 +161,170 @@ __device__ __forceinline__ void delta_sum(const Params& p, uint32_t beg, uint32_
     if constexpr (SCALE) mys = lane < n ? __ldg(p.scale + (myc & 0x7FFFFFFFu)) : 0.0f;
 #pragma unroll 1
     for (uint32_t j = 0; j < n; j += PF) {
-      typename W::T xv[PF];
+      typename W::T xv[PF][U];
       uint32_t cq[PF];
 #pragma unroll
       for (int q = 0; q < PF; ++q) {
         cq[q] = __shfl_sync(kFull, myc, (j + q) & 31);
-        xv[q] = W::zero();
-        if (j + q < n && active)
-          xv[q] = W::ldg(p.x + (long long)(cq[q] & 0x7FFFFFFFu) * p.ldx + col);
+        const float* row = p.x + (long long)(cq[q] & 0x7FFFFFFFu) * p.ldx;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = col0 + uint32_t(u) * 32u * V;
+          xv[q][u] = (j + q < n && c < p.d) ? W::ldg(row + c) : W::zero();
+        }
       }
 #pragma unroll
       for (int q = 0; q < PF; ++q) {
-        typename W::T v = xv[q];
-        if constexpr (SCALE) v = W::mul(v, __shfl_sync(kFull, mys, (j + q) & 31));
-        if (j + q < n) acc = (cq[q] & 0x80000000u) ? W::sub(acc, v) : W::add(acc, v);
+        float s = 0.0f;
+        if constexpr (SCALE) s = __shfl_sync(kFull, mys, (j + q) & 31);
+        if (j + q < n) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            typename W::T v = xv[q][u];
+            if constexpr (SCALE) v = W::mul(v, s);
+            acc.v[u] = (cq[q] & 0x80000000u) ? W::sub(acc.v[u], v) : W::add(acc.v[u], v);
+          }
+        }
       }
     }
   }
 }
 
-template <int V, int PF, bool NORM, bool SCALE>
+template <int V, int U>
+__device__ __forceinline__ void add_row(Acc<V, U>& acc, const float* src, uint32_t col0,
+                                        uint32_t d) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t c = col0 + uint32_t(u) * 32u * V;
+    if (c < d) acc.v[u] = Vec<V>::add(acc.v[u], Vec<V>::ldcg(src + c));
+  }
+}
+
+template <int V, int U>
+__device__ __forceinline__ void store_row(const Acc<V, U>& acc, float* dst, uint32_t col0,
+                                          uint32_t d) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t c = col0 + uint32_t(u) * 32u * V;
+    if (c < d) Vec<V>::st(dst + c, acc.v[u]);
+  }
+}
+
+template <int V, int U>
+__device__ __forceinline__ void store_row_scaled(const Acc<V, U>& acc, float* dst, uint32_t col0,
+                                                 uint32_t d, float s) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t c = col0 + uint32_t(u) * 32u * V;
+    if (c < d) Vec<V>::st(dst + c, Vec<V>::mul(acc.v[u], s));
+  }
+}
+
+// acc += partial[first], partial[first+1], ... in order. The producers' ready
+// flags are checked 32 at a time (one lane each), then the partial rows are
+// streamed with PF x U loads in flight.
+template <int V, int U, int PF>
+__device__ __forceinline__ void add_partials(const Params& p, const uint32_t* flag_base,
+                                             uint32_t first, uint32_t cnt, uint32_t col0,
+                                             Acc<V, U>& acc) {
+  using W = Vec<V>;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b0 = 0; b0 < cnt; b0 += 32) {
+    const uint32_t nb = min(32u, cnt - b0);
+    if (uint32_t(lane) < nb) {
+      const uint32_t* f = flag_base + first + b0 + lane;
+      while (ld_acquire(f) != p.epoch) __nanosleep(32);
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (uint32_t j = 0; j < nb; j += PF) {
+      typename W::T xv[PF][U];
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const float* src = p.partial + (size_t)(first + b0 + j + q) * p.dpad;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = col0 + uint32_t(u) * 32u * V;
+          xv[q][u] = (j + q < nb && c < p.d) ? W::ldcg(src + c) : W::zero();
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < PF; ++q)
+        if (j + q < nb) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc.v[u] = W::add(acc.v[u], xv[q][u]);
+        }
+    }
+  }
+}
+
+// One ticket = one item over a column slab of 32*V*U columns. Tickets are
+// claimed in batches; the batch's dptr/meta are fetched with one
+// lane-parallel load and broadcast with shuffles.
+template <int V, int U, int PF, bool NORM, bool SCALE>
 __global__ void __launch_bounds__(kThreads) cbm_fused_kernel(const Params p) {
   using W = Vec<V>;
+  constexpr uint32_t kSlab = 32u * V * U;
   const int lane = threadIdx.x & 31;
   for (;;) {
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd(p.counters, p.batch);
     base = __shfl_sync(kFull, base, 0);
     if (base >= p.total_tickets) break;
-    const uint32_t lim = min(base + p.batch, p.total_tickets);
-    for (uint32_t T = base; T < lim; ++T) {
+    const uint32_t nb = min(p.batch, p.total_tickets - base);
+    uint32_t my_beg = 0, my_end = 0, my_slot = 0, my_cnt = 0;
+    uint4 my_meta = make_uint4(0u, 0xFFFFFFFFu, 0u, 0u);
+    if (uint32_t(lane) < nb) {
+      const uint32_t T = base + lane;
+      const uint32_t t = T - (T / p.n_items) * p.n_items;
+      my_beg = __ldg(p.dptr + t);
+      my_end = __ldg(p.dptr + t + 1);
+      my_meta = __ldg(p.meta + t);
+      my_cnt = __ldg(p.pcnt + t);
+      if constexpr (NORM) my_slot = __ldg(p.oslot + t);
+    }
+    for (uint32_t i = 0; i < nb; ++i) {
+      const uint32_t T = base + i;
       const uint32_t slab = T / p.n_items;
       const uint32_t t = T - slab * p.n_items;
-      const uint32_t col = slab * (32u * V) + uint32_t(lane) * V;
-      const bool active = col < p.d;
-      typename W::T acc = W::zero();
-      delta_sum<V, PF, SCALE>(p, p.dptr[t], p.dptr[t + 1], col, active, acc);
+      const uint32_t col0 = slab * kSlab + uint32_t(lane) * V;
+      const uint32_t beg = __shfl_sync(kFull, my_beg, i);
+      const uint32_t end = __shfl_sync(kFull, my_end, i);
+      const uint32_t first = __shfl_sync(kFull, my_meta.w, i);
+      const uint32_t cnt = __shfl_sync(kFull, my_cnt, i);
+      Acc<V, U> acc;
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc.v[u] = W::zero();
+      delta_sum<V, U, PF, SCALE>(p, beg, end, col0, acc);
       uint32_t* flag_base = p.flags + (size_t)slab * p.n_items;
-      if (t < p.n_chunk) {  // CHUNK item: publish the partial sum
-        if (active) W::st(p.partial + (size_t)t * p.dpad + col, acc);
+      if (cnt) add_partials<V, U, PF>(p, flag_base, first, cnt, col0, acc);
+      if (t < p.n_chunk) {  // CHUNK / MERGE item: publish the partial sum
+        store_row(acc, p.partial + (size_t)t * p.dpad, col0, p.d);
         publish(flag_base + t, p.epoch);
         continue;
       }
-      const uint4 mt = p.meta[t];
-      const uint32_t extra = mt.w >> 24;
-      if (extra) {  // remaining chunks of a split row, in order
-        const uint32_t first = mt.w & 0xFFFFFFu;
-        for (uint32_t i = 0; i < extra; ++i) {
-          await(flag_base + first + i, p.epoch);
-          if (active) acc = W::add(acc, W::ldcg(p.partial + (size_t)(first + i) * p.dpad + col));
+      const uint32_t mrow = __shfl_sync(kFull, my_meta.x, i);
+      const uint32_t ppos = __shfl_sync(kFull, my_meta.y, i);
+      const uint32_t psrc = __shfl_sync(kFull, my_meta.z, i);
+      if (ppos != 0xFFFFFFFFu) {  // stage 2: + unscaled parent row
+        await(flag_base + ppos, p.epoch);
+        const float* src = NORM ? p.interior + (size_t)psrc * p.dpad
+                                : p.y + (long long)psrc * p.ldy;
+        add_row(acc, src, col0, p.d);
+      }
+      const uint32_t row = mrow & 0x7FFFFFFFu;
+      const bool is_parent = (mrow >> 31) != 0;
+      if constexpr (NORM) {
+        if (is_parent) {  // children read the unscaled row from scratch
+          const uint32_t slot = __shfl_sync(kFull, my_slot, i);
+          store_row(acc, p.interior + (size_t)slot * p.dpad, col0, p.d);
+          publish(flag_base + t, p.epoch);
         }
+        store_row_scaled(acc, p.y + (long long)row * p.ldy, col0, p.d, __ldg(p.scale + row));
+      } else {
+        store_row(acc, p.y + (long long)row * p.ldy, col0, p.d);
+        if (is_parent) publish(flag_base + t, p.epoch);
       }
-      if (mt.y != 0xFFFFFFFFu) {  // stage 2: + unscaled parent row
-        await(flag_base + mt.y, p.epoch);
-        const float* src = NORM ? p.interior + (size_t)mt.z * p.dpad
-                                : p.y + (long long)mt.z * p.ldy;
-        if (active) acc = W::add(acc, W::ldcg(src + col));
-      }
-      const uint32_t row = mt.x & 0x7FFFFFFFu;
-      const bool is_parent = (mt.x >> 31) != 0;
-      if (active) {
-        if constexpr (NORM) {
-          if (is_parent) W::st(p.interior + (size_t)p.oslot[t] * p.dpad + col, acc);
-          W::st(p.y + (long long)row * p.ldy + col, W::mul(acc, __ldg(p.scale + row)));
-        } else {
-          W::st(p.y + (long long)row * p.ldy + col, acc);
-        }
-      }
-      if (is_parent) publish(flag_base + t, p.epoch);
     }
   }
   // self-resetting ticket counter: the last warp out rearms it
@@ -246,12 +351,12 @@ __global__ void prescale_kernel(const float* __restrict__ x, long long ldx,
   }
 }
 
-template <int V, int PF, bool NORM, bool SCALE>
+template <int V, int U, int PF, bool NORM, bool SCALE>
 int blocks_per_sm() {
   static int cached = -1;  // per template instance
   if (cached < 0) {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_fused_kernel<V, PF, NORM, SCALE>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_fused_kernel<V, U, PF, NORM, SCALE>,
                                                   kThreads, 0);
     cached = std::max(1, b);
   }
@@ -259,23 +364,32 @@ int blocks_per_sm() {
 }
 
 // Persistent grid: at most one full residency wave, never more warps than
-// tickets; ~6 ticket batches per warp keep the claim counter cool.
-template <int V, int PF, bool NORM, bool SCALE>
+// tickets; ~4 ticket batches per warp keep the claim counter cool.
+template <int V, int U, int PF, bool NORM, bool SCALE>
 void launch_one(Params& p, uint64_t tickets, int num_sms, cudaStream_t s) {
   constexpr uint64_t wpb = kThreads / 32;
-  const uint64_t cap = uint64_t(num_sms) * blocks_per_sm<V, PF, NORM, SCALE>() * wpb;
+  const uint64_t cap = uint64_t(num_sms) * blocks_per_sm<V, U, PF, NORM, SCALE>() * wpb;
   const uint64_t warps = std::max<uint64_t>(1, std::min(cap, tickets));
   const int grid = int((warps + wpb - 1) / wpb);
   p.total_warps = uint32_t(grid * wpb);
-  p.batch = uint32_t(std::clamp<uint64_t>(tickets / (uint64_t(p.total_warps) * 6), 1, 8));
-  cbm_fused_kernel<V, PF, NORM, SCALE><<<grid, kThreads, 0, s>>>(p);
+  p.batch = uint32_t(std::clamp<uint64_t>(tickets / (uint64_t(p.total_warps) * 2), 1, 16));
+  cbm_fused_kernel<V, U, PF, NORM, SCALE><<<grid, kThreads, 0, s>>>(p);
 }
 
-template <int V, int PF>
+template <int V, int U>
 void run_fused(Params& p, uint64_t tickets, bool norm, bool scl, int num_sms, cudaStream_t s) {
-  if (!norm) launch_one<V, PF, false, false>(p, tickets, num_sms, s);
-  else if (scl) launch_one<V, PF, true, true>(p, tickets, num_sms, s);
-  else launch_one<V, PF, true, false>(p, tickets, num_sms, s);
+  constexpr int PF = (32 / (V * U)) < 2 ? 2 : ((32 / (V * U)) > 16 ? 16 : (32 / (V * U)));
+  if (!norm) launch_one<V, U, PF, false, false>(p, tickets, num_sms, s);
+  else if (scl) launch_one<V, U, PF, true, true>(p, tickets, num_sms, s);
+  else launch_one<V, U, PF, true, false>(p, tickets, num_sms, s);
+}
+
+template <int V>
+void run_fused_u(uint32_t U, Params& p, uint64_t tickets, bool norm, bool scl, int num_sms,
+                 cudaStream_t s) {
+  if (U == 4) run_fused<V, 4>(p, tickets, norm, scl, num_sms, s);
+  else if (U == 2) run_fused<V, 2>(p, tickets, norm, scl, num_sms, s);
+  else run_fused<V, 1>(p, tickets, norm, scl, num_sms, s);
 }
 
 template <typename T>
@@ -312,6 +426,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
     put(h->dptr, L.dptr, "upload dptr");
     put(h->dcol, L.dcol, "upload dcol");
     put(h->meta, L.meta, "upload meta");
+    put(h->pcnt, L.pcnt, "upload pcnt");
     if (L.normalized) {
       put(h->oslot, L.oslot, "upload oslot");
       put(h->scale, L.scale, "upload scale");
@@ -322,6 +437,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
     L.dptr = {};
     L.dcol = {};
     L.meta = {};
+    L.pcnt = {};
     L.oslot = {};
     L.scale = {};
     h->info = std::move(L);
@@ -335,7 +451,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
 void device_free(DeviceMatrix* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  for (void* p : {(void*)h->dptr, (void*)h->dcol, (void*)h->meta, (void*)h->oslot,
+  for (void* p : {(void*)h->dptr, (void*)h->dcol, (void*)h->meta, (void*)h->pcnt, (void*)h->oslot,
                   (void*)h->scale, (void*)h->counters, (void*)h->flags, (void*)h->partial,
                   (void*)h->interior, (void*)h->xs, (void*)h->xstage, (void*)h->ystage})
     if (p) cudaFree(p);
@@ -395,8 +511,10 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     ldin = dpad;
   }
   const uint32_t V = pick_vec(d, xin, ldin, y, ldy);
-  const uint32_t slab_w = 32 * V;
-  const uint32_t n_slabs = (d + slab_w - 1) / slab_w;
+  // columns per ticket: up to 4 segments of 32*V columns (<= 512 floats)
+  const uint32_t segs = (d + 32 * V - 1) / (32 * V);
+  const uint32_t U = segs >= 3 ? 4 : segs;
+  const uint32_t n_slabs = (d + 32 * V * U - 1) / (32 * V * U);
   if (++h->epoch == 0) {  // wrapped: re-zero the flags
     ck(cudaMemsetAsync(h->flags, 0, h->flags_cap * sizeof(uint32_t), s), "flags memset");
     h->epoch = 1;
@@ -405,6 +523,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   p.dptr = h->dptr;
   p.dcol = h->dcol;
   p.meta = reinterpret_cast<const uint4*>(h->meta);
+  p.pcnt = h->pcnt;
   p.oslot = h->oslot;
   p.scale = h->scale;
   p.x = xin;
@@ -420,14 +539,14 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   p.d = d;
   p.dpad = dpad;
   const uint64_t tickets = uint64_t(L.n_items) * n_slabs;
-  if (tickets >= 0xFFFFFFFFull) throw invalid_argument("spmm: too many work tickets");
+  if (tickets >= 0x7FFFFFFFull) throw invalid_argument("spmm: too many work tickets");
   p.total_tickets = uint32_t(tickets);
   p.epoch = h->epoch;
 
   const bool norm = L.normalized, scl = L.normalized && !prescale;
-  if (V == 4) run_fused<4, 8>(p, tickets, norm, scl, h->num_sms, s);
-  else if (V == 2) run_fused<2, 16>(p, tickets, norm, scl, h->num_sms, s);
-  else run_fused<1, 16>(p, tickets, norm, scl, h->num_sms, s);
+  if (V == 4) run_fused_u<4>(U, p, tickets, norm, scl, h->num_sms, s);
+  else if (V == 2) run_fused_u<2>(U, p, tickets, norm, scl, h->num_sms, s);
+  else run_fused_u<1>(U, p, tickets, norm, scl, h->num_sms, s);
   ck(cudaGetLastError(), "cbm_fused launch");
   ++h->last_launches;
 }

@@ -21,6 +21,7 @@ struct DeviceMatrix {
   uint32_t* dptr = nullptr;
   uint32_t* dcol = nullptr;
   uint32_t* meta = nullptr;
+  uint32_t* pcnt = nullptr;
   uint32_t* oslot = nullptr;
   float* scale = nullptr;
   uint64_t device_bytes = 0;

@@ -99,31 +99,59 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
     for (uint32_t x = 0; x < m; ++x) rows[cur[depth[x]]++] = x;
   }
 
-  // split plan for long rows
-  if (split_threshold == 0) split_threshold = 1024;
-  if (chunk == 0) chunk = 512;
-  struct Split {
-    uint32_t pieces, piece;
-  };
-  std::vector<Split> sp(m, {1, 0});
-  uint64_t n_chunk = 0;
+  // split plan for long rows (default mode only)
+  if (split_threshold == 0) split_threshold = 96;
+  if (chunk == 0) chunk = 48;
+  if (chunk > split_threshold) chunk = split_threshold;
+  std::vector<uint32_t> pieces(m, 1);  // per ROW position i
+  uint64_t n_leaf = 0;
   if (!order_faithful) {
     for (uint32_t i = 0; i < m; ++i) {
       const uint32_t r = rows[i];
       const uint64_t len = v.row_ptr[r + 1] - v.row_ptr[r];
       if (len <= split_threshold) continue;
-      const uint64_t piece = std::max<uint64_t>(chunk, (len + 255) / 256);
-      const uint32_t pieces = uint32_t((len + piece - 1) / piece);
-      if (pieces < 2 || n_chunk + pieces - 1 >= (1u << 24)) continue;
-      sp[i] = {pieces, uint32_t(piece)};
-      n_chunk += pieces - 1;
+      pieces[i] = uint32_t((len + chunk - 1) / chunk);
+      n_leaf += pieces[i] - 1;
     }
   }
-  L.n_chunk_items = uint32_t(n_chunk);
-  L.n_items = uint32_t(n_chunk) + m;
+  // merge tree per split row: level 0 = the row's leaf chunks; a level with
+  // more than kFanIn nodes is grouped kFanIn at a time into MERGE nodes.
+  uint32_t max_lvls = 0;
+  std::vector<uint32_t> nl(m, 0);  // number of levels (incl. leaves) per split row
+  for (uint32_t i = 0; i < m; ++i) {
+    if (pieces[i] < 2) continue;
+    uint32_t n = pieces[i] - 1, k = 1;
+    while (n > kFanIn) {
+      n = (n + kFanIn - 1) / kFanIn;
+      ++k;
+    }
+    nl[i] = k;
+    max_lvls = std::max(max_lvls, k);
+  }
+  // first item index of each (row, level) block: leaves for all rows first,
+  // then merge level 1 for all rows, ...
+  std::vector<std::vector<uint32_t>> first_at(max_lvls);
+  std::vector<std::vector<uint32_t>> count_at(max_lvls);
+  uint64_t t_next = 0;
+  for (uint32_t lv = 0; lv < max_lvls; ++lv) {
+    first_at[lv].assign(m, kNoItem);
+    count_at[lv].assign(m, 0);
+    for (uint32_t i = 0; i < m; ++i) {
+      if (nl[i] <= lv) continue;
+      uint32_t n = pieces[i] - 1;
+      for (uint32_t q = 0; q < lv; ++q) n = (n + kFanIn - 1) / kFanIn;
+      first_at[lv][i] = uint32_t(t_next);
+      count_at[lv][i] = n;
+      t_next += n;
+    }
+  }
+  if (t_next + m >= 0x7FFFFFFFull) throw invalid_argument("upload: too many work items");
+  L.n_chunk_items = uint32_t(t_next);
+  L.n_merge_items = uint32_t(t_next - n_leaf);
+  L.n_items = uint32_t(t_next) + m;
 
   std::vector<uint32_t> item_of_row(m);
-  for (uint32_t i = 0; i < m; ++i) item_of_row[rows[i]] = uint32_t(n_chunk) + i;
+  for (uint32_t i = 0; i < m; ++i) item_of_row[rows[i]] = L.n_chunk_items + i;
   std::vector<uint8_t> interior(m, 0);
   for (uint32_t x = 0; x < m; ++x)
     if (v.parent[x] != kVirtual) interior[v.parent[x]] = 1;
@@ -134,42 +162,58 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   L.dptr.assign(size_t(L.n_items) + 1, 0);
   L.dcol.resize(nnz);
   L.meta.assign(size_t(L.n_items) * 4, 0);
+  L.pcnt.assign(L.n_items, 0);
   if (L.normalized) L.oslot.assign(L.n_items, kNoItem);
-  auto emit = [&](uint32_t row, uint64_t k0, uint64_t k1, uint64_t& o) {
-    for (uint64_t k = k0; k < k1; ++k)
-      L.dcol[o++] = v.col_idx[k] | (v.values[k] < 0.0f ? kSignBit : 0u);
-    (void)row;
-  };
-  uint64_t o = 0;
-  uint32_t t = 0;
-  std::vector<uint32_t> first_chunk(m, 0);
-  for (uint32_t i = 0; i < m; ++i) {  // CHUNK items: pieces 1.. of split rows
-    if (sp[i].pieces < 2) continue;
+  // delta ranges: items own [dptr[t], dptr[t+1]); fill in item order
+  std::vector<uint64_t> own_lo(L.n_items, 0), own_hi(L.n_items, 0);
+  for (uint32_t i = 0; i < m; ++i) {
     const uint32_t r = rows[i];
     const uint64_t lo = v.row_ptr[r], hi = v.row_ptr[r + 1];
-    first_chunk[i] = t;
-    for (uint32_t q = 1; q < sp[i].pieces; ++q) {
-      const uint64_t k0 = lo + uint64_t(q) * sp[i].piece;
-      const uint64_t k1 = std::min(hi, k0 + sp[i].piece);
+    const uint32_t t_row = L.n_chunk_items + i;
+    if (pieces[i] < 2) {
+      own_lo[t_row] = lo;
+      own_hi[t_row] = hi;
+      continue;
+    }
+    own_lo[t_row] = lo;  // piece 0 stays with the ROW item
+    own_hi[t_row] = lo + chunk;
+    for (uint32_t q = 1; q < pieces[i]; ++q) {
+      const uint32_t t = first_at[0][i] + q - 1;
+      own_lo[t] = lo + uint64_t(q) * chunk;
+      own_hi[t] = std::min<uint64_t>(hi, own_lo[t] + chunk);
       L.meta[size_t(t) * 4 + 0] = r;
       L.meta[size_t(t) * 4 + 1] = kNoItem;
-      emit(r, k0, k1, o);
-      L.dptr[++t] = uint32_t(o);
     }
+    // merge levels: node j at level lv sums nodes [j*F, min((j+1)*F, n_prev)) of lv-1
+    for (uint32_t lv = 1; lv < nl[i]; ++lv) {
+      const uint32_t n_prev = count_at[lv - 1][i];
+      for (uint32_t j = 0; j < count_at[lv][i]; ++j) {
+        const uint32_t t = first_at[lv][i] + j;
+        L.meta[size_t(t) * 4 + 0] = r;
+        L.meta[size_t(t) * 4 + 1] = kNoItem;
+        L.meta[size_t(t) * 4 + 3] = first_at[lv - 1][i] + j * kFanIn;
+        L.pcnt[t] = std::min(kFanIn, n_prev - j * kFanIn);
+      }
+    }
+    const uint32_t top = nl[i] - 1;
+    L.meta[size_t(t_row) * 4 + 3] = first_at[top][i];
+    L.pcnt[t_row] = count_at[top][i];
+  }
+  uint64_t o = 0;
+  for (uint32_t t = 0; t < L.n_items; ++t) {
+    for (uint64_t k = own_lo[t]; k < own_hi[t]; ++k)
+      L.dcol[o++] = v.col_idx[k] | (v.values[k] < 0.0f ? kSignBit : 0u);
+    L.dptr[t + 1] = uint32_t(o);
   }
   for (uint32_t i = 0; i < m; ++i) {  // ROW items
     const uint32_t r = rows[i];
-    const uint64_t lo = v.row_ptr[r], hi = v.row_ptr[r + 1];
-    const uint64_t k1 = sp[i].pieces > 1 ? lo + sp[i].piece : hi;
-    emit(r, lo, k1, o);
+    const uint32_t t = L.n_chunk_items + i;
     uint32_t* mt = &L.meta[size_t(t) * 4];
     const uint32_t p = v.parent[r];
     mt[0] = r | (interior[r] ? kInteriorBit : 0u);
     mt[1] = p == kVirtual ? kNoItem : item_of_row[p];
     mt[2] = p == kVirtual ? 0u : (L.normalized ? slot[p] : p);
-    mt[3] = sp[i].pieces > 1 ? ((sp[i].pieces - 1) << 24) | first_chunk[i] : 0u;
     if (L.normalized) L.oslot[t] = slot[r];
-    L.dptr[++t] = uint32_t(o);
   }
   return L;
 }

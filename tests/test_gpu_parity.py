@@ -209,3 +209,15 @@ def test_cfg1_full_size_gaussian(dev):
     assert_bitwise(got, want, "cfg1 faithful")
     got, _ = gpu_spmm(c, x, dev)
     assert normwise_err(got, want) <= TOL
+
+
+def test_deep_merge_trees(dev):
+    """Rows with thousands of deltas split into 2-delta chunks: three levels of
+    fan-in-32 MERGE items; integer X stays bit-exact."""
+    a = P.generate_graph("community", [3000, 3000, 0.9, 0.0], 41)
+    c = P.build_cbm(a, 0, threads=8)
+    x = P.generate_dense("int", 3000, 72, 42, -8, 8)
+    got, h = gpu_spmm(c, x, dev, split_threshold=4, chunk=2)
+    info = h.info()
+    assert info["n_chunk_items"] > 1000 and info["max_row_deltas"] > 2000
+    assert_bitwise(got, O.oracle_spmm(oracle_arrays(c), x), "deep merge")
