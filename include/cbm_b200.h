@@ -109,6 +109,8 @@ typedef struct cbm_b200_options {
   int32_t prescale;          /* normalized only: -1 auto, 0 off, 1 pre-scale X
                                 by row_scale once per call (bit-identical
                                 products, removes the per-delta FMUL) */
+  int32_t kernel;            /* 0 auto (LDG.128-wide lanes when rows allow),
+                                1 force scalar lanes (one float per lane) */
 } cbm_b200_options;
 
 void cbm_b200_default_options(cbm_b200_options* opt);

@@ -70,7 +70,8 @@ class _CbmView(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("order_faithful", C.c_int32),
-                ("split_threshold", C.c_uint32), ("chunk", C.c_uint32), ("prescale", C.c_int32)]
+                ("split_threshold", C.c_uint32), ("chunk", C.c_uint32), ("prescale", C.c_int32),
+                ("kernel", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -300,7 +301,8 @@ class DeviceCbm:
     """A CBM uploaded once into the device layout."""
 
     def __init__(self, c: CbmMatrix, device: int | None = None, order_faithful: bool = False,
-                 split_threshold: int = 0, chunk: int = 0, prescale: int = -1):
+                 split_threshold: int = 0, chunk: int = 0, prescale: int = -1,
+                 kernel: str = "auto"):
         opt = _Options()
         _lib.cbm_b200_default_options(C.byref(opt))
         opt.device = -1 if device is None else int(device)
@@ -308,6 +310,7 @@ class DeviceCbm:
         opt.split_threshold = split_threshold
         opt.chunk = chunk
         opt.prescale = prescale
+        opt.kernel = {"auto": 0, "scalar": 1}[kernel]
         self._h = _vp()
         view = c._view()
         _check(_lib.cbm_b200_upload(C.byref(view), C.byref(opt), C.byref(self._h)))

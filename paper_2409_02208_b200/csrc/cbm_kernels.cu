@@ -7,16 +7,27 @@
 //   stage 2  parent add       acc = acc (+) U[parent]                (unscaled parent)
 //   stage 3  row scale        Y   = acc (*) s_row                    (normalized)
 // with every (+)/(*) an explicitly rounded __fadd_rn/__fsub_rn/__fmul_rn (the
-// reference's object code has no FMA). Warps claim tickets (slab, item) from a
-// global counter in slab-major, level order; a ROW item whose parent (or whose
-// split chunks) are not finished yet spins on a per-item ready flag. Tickets
-// are only ever claimed by running warps and every wait targets an earlier
-// ticket, so the smallest unfinished ticket always makes progress: no
-// deadlock for any grid size or residency.
+// reference's object code has no FMA).
 //
-// Lanes cover a column slab of 32*V floats (V = 4: 128-bit loads of X rows);
-// a row's delta column indices are fetched 32 at a time with one coalesced load
-// and broadcast with shuffles; PF X-row slabs are in flight per warp.
+// Schedule. A ticket is (column slab, item), ordered slab-major then item
+// order (CHUNK, MERGE, then ROW items by tree depth). The grid is launched
+// cooperatively (every warp co-resident) and ticket T belongs to warp
+// T mod W: no claim counter, no atomics. A warp finishes its tickets in
+// increasing order and every wait (parent row, split-row partials) targets a
+// smaller ticket, so the smallest unfinished ticket is always being worked on
+// and its inputs are complete: no deadlock.
+//
+// Streaming. Each warp walks its ticket sequence with two cursors. The issue
+// cursor keeps D X-row segments in flight with cp.async (LDGSTS): every lane
+// copies its own V floats of the row into its own slice of a shared-memory
+// slot and later reads exactly those bytes back, so a lane-private
+// cp.async.wait_group is the only synchronisation. The consume cursor adds
+// slot after slot into the accumulator in delta order and runs each item's
+// epilogue (partials, parent, stores, flag) as it passes the item's end, while
+// the issue cursor is already fetching the next items' rows. Ticket records
+// and column-index windows are prefetched a group / a ticket ahead.
+// (Bulk async copies were measured and rejected for these row sizes: one
+// lane's copies serialise at ~350 ns each — profiles/r01_ubench_gather.txt.)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -122,111 +133,29 @@ __device__ __forceinline__ void await(const uint32_t* f, uint32_t epoch) {
 }
 
 struct Params {
-  const uint32_t* __restrict__ dptr;
+  const uint4* __restrict__ rec;      // 2 x uint4 per item (layout.hpp)
+  const float* __restrict__ srow;     // per item: its row's scale (normalized)
   const uint32_t* __restrict__ dcol;
-  const uint4* __restrict__ meta;
-  const uint32_t* __restrict__ pcnt;
-  const uint32_t* __restrict__ oslot;
-  const float* __restrict__ scale;
+  const float* __restrict__ scale;    // per column scale (normalized, per-delta products)
   const float* __restrict__ x;
   long long ldx;
   float* y;
   long long ldy;
-  float* partial;   // CHUNK partial sums, stride dpad
+  float* partial;   // CHUNK / MERGE partial sums, stride dpad
   float* interior;  // unscaled interior rows (normalized), stride dpad
   uint32_t* flags;
-  uint32_t* counters;
+  const uint32_t* __restrict__ wstart;  // per warp: first ticket of its range (total_warps + 1)
   uint32_t n_items, n_chunk, d, dpad;
-  uint32_t total_tickets, batch, total_warps, epoch;
+  uint32_t total_tickets, total_warps, epoch;
 };
-
-// Per lane: U vectors of V floats at columns col0 + u*32*V (each u is one
-// fully coalesced 32*V*4-byte segment of an X row).
-template <int V, int U>
-struct Acc {
-  typename Vec<V>::T v[U];
-};
-
-// Stage 1 for one item: delta sum over dcol[beg, end) into acc, deltas in
-// storage (ascending column) order, PF deltas x U segments in flight.
-template <int V, int U, int PF, bool SCALE>
-__device__ __forceinline__ void delta_sum(const Params& p, uint32_t beg, uint32_t end,
-                                          uint32_t col0, Acc<V, U>& acc) {
-  using W = Vec<V>;
-  const int lane = threadIdx.x & 31;
-  for (uint32_t k0 = beg; k0 < end; k0 += 32) {
-    const uint32_t n = min(32u, end - k0);
-    const uint32_t myc = lane < n ? __ldg(p.dcol + k0 + lane) : 0u;
-    float mys = 0.0f;
-    if constexpr (SCALE) mys = lane < n ? __ldg(p.scale + (myc & 0x7FFFFFFFu)) : 0.0f;
-#pragma unroll 1
-    for (uint32_t j = 0; j < n; j += PF) {
-      typename W::T xv[PF][U];
-      uint32_t cq[PF];
-#pragma unroll
-      for (int q = 0; q < PF; ++q) {
-        cq[q] = __shfl_sync(kFull, myc, (j + q) & 31);
-        const float* row = p.x + (long long)(cq[q] & 0x7FFFFFFFu) * p.ldx;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t c = col0 + uint32_t(u) * 32u * V;
-          xv[q][u] = (j + q < n && c < p.d) ? W::ldg(row + c) : W::zero();
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < PF; ++q) {
-        float s = 0.0f;
-        if constexpr (SCALE) s = __shfl_sync(kFull, mys, (j + q) & 31);
-        if (j + q < n) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            typename W::T v = xv[q][u];
-            if constexpr (SCALE) v = W::mul(v, s);
-            acc.v[u] = (cq[q] & 0x80000000u) ? W::sub(acc.v[u], v) : W::add(acc.v[u], v);
-          }
-        }
-      }
-    }
-  }
-}
-
-template <int V, int U>
-__device__ __forceinline__ void add_row(Acc<V, U>& acc, const float* src, uint32_t col0,
-                                        uint32_t d) {
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const uint32_t c = col0 + uint32_t(u) * 32u * V;
-    if (c < d) acc.v[u] = Vec<V>::add(acc.v[u], Vec<V>::ldcg(src + c));
-  }
-}
-
-template <int V, int U>
-__device__ __forceinline__ void store_row(const Acc<V, U>& acc, float* dst, uint32_t col0,
-                                          uint32_t d) {
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const uint32_t c = col0 + uint32_t(u) * 32u * V;
-    if (c < d) Vec<V>::st(dst + c, acc.v[u]);
-  }
-}
-
-template <int V, int U>
-__device__ __forceinline__ void store_row_scaled(const Acc<V, U>& acc, float* dst, uint32_t col0,
-                                                 uint32_t d, float s) {
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const uint32_t c = col0 + uint32_t(u) * 32u * V;
-    if (c < d) Vec<V>::st(dst + c, Vec<V>::mul(acc.v[u], s));
-  }
-}
 
 // acc += partial[first], partial[first+1], ... in order. The producers' ready
 // flags are checked 32 at a time (one lane each), then the partial rows are
-// streamed with PF x U loads in flight.
-template <int V, int U, int PF>
+// streamed with PF loads in flight.
+template <int V, int PF>
 __device__ __forceinline__ void add_partials(const Params& p, const uint32_t* flag_base,
-                                             uint32_t first, uint32_t cnt, uint32_t col0,
-                                             Acc<V, U>& acc) {
+                                             uint32_t first, uint32_t cnt, uint32_t col,
+                                             bool active, typename Vec<V>::T& acc) {
   using W = Vec<V>;
   const int lane = threadIdx.x & 31;
   for (uint32_t b0 = 0; b0 < cnt; b0 += 32) {
@@ -238,104 +167,237 @@ __device__ __forceinline__ void add_partials(const Params& p, const uint32_t* fl
     __syncwarp();
 #pragma unroll 1
     for (uint32_t j = 0; j < nb; j += PF) {
-      typename W::T xv[PF][U];
-#pragma unroll
-      for (int q = 0; q < PF; ++q) {
-        const float* src = p.partial + (size_t)(first + b0 + j + q) * p.dpad;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t c = col0 + uint32_t(u) * 32u * V;
-          xv[q][u] = (j + q < nb && c < p.d) ? W::ldcg(src + c) : W::zero();
-        }
-      }
+      typename W::T v[PF];
 #pragma unroll
       for (int q = 0; q < PF; ++q)
-        if (j + q < nb) {
+        v[q] = (j + q < nb && active)
+                   ? W::ldcg(p.partial + (size_t)(first + b0 + j + q) * p.dpad + col)
+                   : W::zero();
 #pragma unroll
-          for (int u = 0; u < U; ++u) acc.v[u] = W::add(acc.v[u], xv[q][u]);
-        }
+      for (int q = 0; q < PF; ++q)
+        if (j + q < nb) acc = W::add(acc, v[q]);
     }
   }
 }
 
-// One ticket = one item over a column slab of 32*V*U columns. Tickets are
-// claimed in batches; the batch's dptr/meta are fetched with one
-// lane-parallel load and broadcast with shuffles.
-template <int V, int U, int PF, bool NORM, bool SCALE>
-__global__ void __launch_bounds__(kThreads) cbm_fused_kernel(const Params p) {
-  using W = Vec<V>;
-  constexpr uint32_t kSlab = 32u * V * U;
+// cp.async (LDGSTS) helpers: each lane copies its own V floats of an X row
+// into its own slice of a shared-memory slot.
+template <int V>
+__device__ __forceinline__ void cp_async(float* dst, const float* src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  if constexpr (V == 4)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(V * 4)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_f(float* dst, const float* src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+template <int V>
+__device__ __forceinline__ typename Vec<V>::T lds(const float* p) {
+  if constexpr (V == 4) return *reinterpret_cast<const float4*>(p);
+  else if constexpr (V == 2) return *reinterpret_cast<const float2*>(p);
+  else return *p;
+}
+
+constexpr int kWarpsPerCta = 4;
+constexpr uint32_t kRecWin = 64;  // ticket records staged per warp (two groups of 32)
+
+// One ticket's record in shared memory (2 x 16 bytes).
+struct alignas(16) TRec {
+  uint32_t beg, end, rowk, ppos;
+  uint32_t psrc, first, cnt, slot;
+};
+
+template <int V, int D, bool NORM, bool SCALE>
+struct alignas(16) WarpSmem {
+  float ring[D][32 * V];          // slot s, lane l: [s][l*V, l*V+V)
+  TRec rec[kRecWin];              // warp-sequence tickets [g, g+64), slot i & 63
+  float srow[NORM ? kRecWin : 1];  // row scale per staged ticket
+  float sring[SCALE ? D : 1];     // the delta's column scale (lane 0 copies, all read)
+};
+
+// Stage the records of warp-sequence tickets [i0, i0+32) (ticket w + i*W).
+template <int V, int D, bool NORM, bool SCALE>
+__device__ __forceinline__ void stage_recs(const Params& p, WarpSmem<V, D, NORM, SCALE>& sm,
+                                           uint32_t w, uint32_t i0, uint32_t n_w) {
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(p.counters, p.batch);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= p.total_tickets) break;
-    const uint32_t nb = min(p.batch, p.total_tickets - base);
-    uint32_t my_beg = 0, my_end = 0, my_slot = 0, my_cnt = 0;
-    uint4 my_meta = make_uint4(0u, 0xFFFFFFFFu, 0u, 0u);
-    if (uint32_t(lane) < nb) {
-      const uint32_t T = base + lane;
-      const uint32_t t = T - (T / p.n_items) * p.n_items;
-      my_beg = __ldg(p.dptr + t);
-      my_end = __ldg(p.dptr + t + 1);
-      my_meta = __ldg(p.meta + t);
-      my_cnt = __ldg(p.pcnt + t);
-      if constexpr (NORM) my_slot = __ldg(p.oslot + t);
+  const uint32_t i = i0 + uint32_t(lane);
+  if (i < n_w) {
+    const uint32_t T = w + i * p.total_warps;
+    const uint32_t t = T - (T / p.n_items) * p.n_items;
+    TRec& r = sm.rec[i & (kRecWin - 1)];
+    *reinterpret_cast<uint4*>(&r.beg) = __ldg(p.rec + 2 * (size_t)t);
+    *reinterpret_cast<uint4*>(&r.psrc) = __ldg(p.rec + 2 * (size_t)t + 1);
+    if constexpr (NORM) sm.srow[i & (kRecWin - 1)] = __ldg(p.srow + t);
+  }
+}
+
+template <int V, int D, bool NORM, bool SCALE>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) {
+  using W = Vec<V>;
+  constexpr uint32_t kSlab = 32u * V;
+  constexpr int PFp = 8;
+  static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  WarpSmem<V, D, NORM, SCALE>& sm =
+      reinterpret_cast<WarpSmem<V, D, NORM, SCALE>*>(smem_raw)[threadIdx.x >> 5];
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= p.total_warps || w >= p.total_tickets) return;
+  const uint32_t WW = p.total_warps;
+  const uint32_t n_w = (p.total_tickets - w + WW - 1) / WW;  // tickets w, w+W, w+2W, ...
+  auto slab_of = [&](uint32_t i) { return (w + i * WW) / p.n_items; };
+  auto item_of = [&](uint32_t i) {
+    const uint32_t T = w + i * WW;
+    return T - (T / p.n_items) * p.n_items;
+  };
+
+  uint32_t g = 0;  // staged records cover warp-sequence tickets [g, g + 64)
+  stage_recs(p, sm, w, 0, n_w);
+  stage_recs(p, sm, w, 32, n_w);
+  __syncwarp();
+  auto R = [&](uint32_t i) -> const TRec& { return sm.rec[i & (kRecWin - 1)]; };
+  // first 32 column words of ticket i (0 past the end / outside the window)
+  auto window = [&](uint32_t i) -> uint32_t {
+    if (i >= n_w || i >= g + kRecWin) return 0u;
+    const TRec& r = R(i);
+    return r.beg + lane < r.end ? __ldg(p.dcol + r.beg + lane) : 0u;
+  };
+
+  // ---- issue cursor: ticket ii, offset iq inside it. win = window of ii,
+  // wn1 / wn2 = windows of ii+1 / ii+2 (fetched two tickets ahead)
+  uint32_t ii = 0, iq = 0, ibeg = 0, ilen = 0, icol = 0;
+  bool iact = false;
+  uint32_t win = window(0), wn1 = window(1), wn2 = window(2), wlong = 0;
+  uint32_t iseq = 0;   // deltas issued
+  uint32_t signs = 0;  // sign bit of the delta in each ring slot
+  bool iblocked = false;
+  auto load_ticket = [&]() {  // cursor fields of ticket ii (window already in win)
+    iq = 0;
+    const TRec& r = R(ii);
+    ibeg = r.beg;
+    ilen = r.end - r.beg;
+    icol = slab_of(ii) * kSlab + uint32_t(lane) * V;
+    iact = icol < p.d;
+    wlong = 32 + uint32_t(lane) < ilen ? __ldg(p.dcol + ibeg + 32 + lane) : 0u;
+  };
+  // step to the next ticket with deltas, shifting the window prefetch;
+  // block while the ticket two ahead is outside the staged records
+  auto next_ticket = [&]() {
+    for (;;) {
+      if (ii + 1 >= n_w) {
+        ii = n_w;
+        return;
+      }
+      if (ii + 3 >= g + kRecWin && ii + 3 < n_w) {
+        iblocked = true;  // resume after the record window slides
+        return;
+      }
+      ++ii;
+      win = wn1;
+      wn1 = wn2;
+      wn2 = window(ii + 2);
+      if (R(ii).end != R(ii).beg) {
+        load_ticket();
+        return;
+      }
     }
-    for (uint32_t i = 0; i < nb; ++i) {
-      const uint32_t T = base + i;
-      const uint32_t slab = T / p.n_items;
-      const uint32_t t = T - slab * p.n_items;
-      const uint32_t col0 = slab * kSlab + uint32_t(lane) * V;
-      const uint32_t beg = __shfl_sync(kFull, my_beg, i);
-      const uint32_t end = __shfl_sync(kFull, my_end, i);
-      const uint32_t first = __shfl_sync(kFull, my_meta.w, i);
-      const uint32_t cnt = __shfl_sync(kFull, my_cnt, i);
-      Acc<V, U> acc;
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc.v[u] = W::zero();
-      delta_sum<V, U, PF, SCALE>(p, beg, end, col0, acc);
-      uint32_t* flag_base = p.flags + (size_t)slab * p.n_items;
-      if (cnt) add_partials<V, U, PF>(p, flag_base, first, cnt, col0, acc);
-      if (t < p.n_chunk) {  // CHUNK / MERGE item: publish the partial sum
-        store_row(acc, p.partial + (size_t)t * p.dpad, col0, p.d);
+  };
+  auto issue_one = [&]() {
+    if (!iblocked && ii < n_w) {
+      const uint32_t cw = __shfl_sync(kFull, win, iq & 31);
+      const uint32_t c = cw & 0x7FFFFFFFu;
+      const uint32_t s = iseq & (D - 1);
+      if (iact) cp_async<V>(&sm.ring[s][lane * V], p.x + (long long)c * p.ldx + icol);
+      if constexpr (SCALE)
+        if (lane == 0) cp_async_f(&sm.sring[s], p.scale + c);
+      signs = (signs & ~(1u << s)) | ((cw >> 31) << s);
+      ++iseq;
+      ++iq;
+      if (iq == ilen) {
+        next_ticket();
+      } else if ((iq & 31) == 0) {  // next 32-delta block of a long ticket
+        win = wlong;
+        wlong = iq + 32 + lane < ilen ? __ldg(p.dcol + ibeg + iq + 32 + lane) : 0u;
+      }
+    }
+    cp_commit();
+  };
+
+  if (R(0).end != R(0).beg) load_ticket();
+  else next_ticket();
+#pragma unroll 1
+  for (int q = 0; q < D; ++q) issue_one();
+
+  uint32_t cseq = 0;  // deltas consumed
+#pragma unroll 1
+  for (uint32_t ci = 0; ci < n_w; ++ci) {
+    if (ci - g == 32) {  // slide the record window by one group
+      __syncwarp();
+      stage_recs(p, sm, w, g + kRecWin, n_w);
+      g += 32;
+      __syncwarp();
+      if (iblocked) {
+        iblocked = false;
+        next_ticket();
+      }
+    }
+    const TRec r = R(ci);
+    const uint32_t slab = slab_of(ci), t = item_of(ci);
+    const uint32_t col = slab * kSlab + uint32_t(lane) * V;
+    const bool active = col < p.d;
+    typename W::T acc = W::zero();
+#pragma unroll 1
+    for (uint32_t k = r.beg; k < r.end; ++k) {
+      cp_wait<D - 1>();  // this lane's copy of delta `cseq` has landed
+      const uint32_t s = cseq & (D - 1);
+      typename W::T v = active ? lds<V>(&sm.ring[s][lane * V]) : W::zero();
+      if constexpr (SCALE) {
+        __syncwarp();  // lane 0's scale copy (covered by its wait) is visible
+        v = W::mul(v, sm.sring[s]);
+      }
+      acc = ((signs >> s) & 1u) ? W::sub(acc, v) : W::add(acc, v);
+      ++cseq;
+      __syncwarp();  // slot s fully read before its refill
+      issue_one();
+    }
+    // ---- epilogue: partials, then CHUNK/MERGE publish or ROW stage 2 + 3
+    uint32_t* flag_base = p.flags + (size_t)slab * p.n_items;
+    if (r.cnt) add_partials<V, PFp>(p, flag_base, r.first, r.cnt, col, active, acc);
+    if (t < p.n_chunk) {
+      if (active) W::st(p.partial + (size_t)t * p.dpad + col, acc);
+      publish(flag_base + t, p.epoch);
+      continue;
+    }
+    if (r.ppos != 0xFFFFFFFFu) {  // + unscaled parent row
+      await(flag_base + r.ppos, p.epoch);
+      const float* src =
+          NORM ? p.interior + (size_t)r.psrc * p.dpad : p.y + (long long)r.psrc * p.ldy;
+      if (active) acc = W::add(acc, W::ldcg(src + col));
+    }
+    const uint32_t row = r.rowk & 0x7FFFFFFFu;
+    const bool is_parent = (r.rowk >> 31) != 0;
+    if constexpr (NORM) {
+      if (is_parent) {  // children read the unscaled row from scratch
+        if (active) W::st(p.interior + (size_t)r.slot * p.dpad + col, acc);
         publish(flag_base + t, p.epoch);
-        continue;
       }
-      const uint32_t mrow = __shfl_sync(kFull, my_meta.x, i);
-      const uint32_t ppos = __shfl_sync(kFull, my_meta.y, i);
-      const uint32_t psrc = __shfl_sync(kFull, my_meta.z, i);
-      if (ppos != 0xFFFFFFFFu) {  // stage 2: + unscaled parent row
-        await(flag_base + ppos, p.epoch);
-        const float* src = NORM ? p.interior + (size_t)psrc * p.dpad
-                                : p.y + (long long)psrc * p.ldy;
-        add_row(acc, src, col0, p.d);
-      }
-      const uint32_t row = mrow & 0x7FFFFFFFu;
-      const bool is_parent = (mrow >> 31) != 0;
-      if constexpr (NORM) {
-        if (is_parent) {  // children read the unscaled row from scratch
-          const uint32_t slot = __shfl_sync(kFull, my_slot, i);
-          store_row(acc, p.interior + (size_t)slot * p.dpad, col0, p.d);
-          publish(flag_base + t, p.epoch);
-        }
-        store_row_scaled(acc, p.y + (long long)row * p.ldy, col0, p.d, __ldg(p.scale + row));
-      } else {
-        store_row(acc, p.y + (long long)row * p.ldy, col0, p.d);
-        if (is_parent) publish(flag_base + t, p.epoch);
-      }
+      const float sr = sm.srow[ci & (kRecWin - 1)];
+      if (active) W::st(p.y + (long long)row * p.ldy + col, W::mul(acc, sr));
+    } else {
+      if (active) W::st(p.y + (long long)row * p.ldy + col, acc);
+      if (is_parent) publish(flag_base + t, p.epoch);
     }
   }
-  // self-resetting ticket counter: the last warp out rearms it
-  if (lane == 0) {
-    __threadfence();
-    if (atomicAdd(p.counters + 1, 1u) == p.total_warps - 1) {
-      p.counters[0] = 0;
-      p.counters[1] = 0;
-      __threadfence();
-    }
-  }
+  cp_wait<0>();  // no copy may target shared memory after exit
 }
 
 // xs[c, :] = row_scale[c] (*) x[c, :] — the bit-identical products of the
@@ -351,45 +413,73 @@ __global__ void prescale_kernel(const float* __restrict__ x, long long ldx,
   }
 }
 
-template <int V, int U, int PF, bool NORM, bool SCALE>
-int blocks_per_sm() {
-  static int cached = -1;  // per template instance
-  if (cached < 0) {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_fused_kernel<V, U, PF, NORM, SCALE>,
-                                                  kThreads, 0);
-    cached = std::max(1, b);
+// Cooperative launch: one full residency wave (all warps co-resident), no
+// more warps than tickets.
+// Contiguous ticket ranges per warp, balanced by cost = deltas + kItemCost per
+// item (the epilogue of an item costs about as much as a few deltas).
+constexpr uint64_t kItemCost = 4;
+const uint32_t* warp_ranges(DeviceMatrix* h, uint32_t warps, uint32_t slabs) {
+  for (const auto& pr : h->parts)
+    if (pr.warps == warps && pr.slabs == slabs) return pr.dev;
+  const Layout& L = h->info;
+  const uint64_t n = L.n_items, per_slab = uint64_t(L.item_beg[n]) + kItemCost * n;
+  const uint64_t tickets = n * slabs, total = per_slab * slabs;
+  auto cost = [&](uint64_t T) {  // cost of tickets [0, T)
+    const uint64_t sl = T / n, t = T - sl * n;
+    return sl * per_slab + L.item_beg[t] + kItemCost * t;
+  };
+  std::vector<uint32_t> ws(size_t(warps) + 1);
+  for (uint32_t w = 0; w <= warps; ++w) {
+    const uint64_t target = total * w / warps;
+    uint64_t lo = 0, hi = tickets;  // first T with cost(T) >= target
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      if (cost(mid) < target) lo = mid + 1;
+      else hi = mid;
+    }
+    ws[w] = uint32_t(lo);
   }
-  return cached;
+  ws[warps] = uint32_t(tickets);
+  uint32_t* dev = nullptr;
+  ck(cudaMalloc(&dev, ws.size() * sizeof(uint32_t)), "warp ranges");
+  ck(cudaMemcpy(dev, ws.data(), ws.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
+     "warp ranges");
+  h->parts.push_back({warps, slabs, dev});
+  return dev;
 }
 
-// Persistent grid: at most one full residency wave, never more warps than
-// tickets; ~4 ticket batches per warp keep the claim counter cool.
-template <int V, int U, int PF, bool NORM, bool SCALE>
-void launch_one(Params& p, uint64_t tickets, int num_sms, cudaStream_t s) {
-  constexpr uint64_t wpb = kThreads / 32;
-  const uint64_t cap = uint64_t(num_sms) * blocks_per_sm<V, U, PF, NORM, SCALE>() * wpb;
+template <int V, int D, bool NORM, bool SCALE>
+void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
+  const int num_sms = h->num_sms;
+  constexpr size_t smem = kWarpsPerCta * sizeof(WarpSmem<V, D, NORM, SCALE>);
+  static int bps = -1;  // per template instance
+  if (bps < 0) {
+    ck(cudaFuncSetAttribute(cbm_kernel<V, D, NORM, SCALE>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+       "smem attribute");
+    int b = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_kernel<V, D, NORM, SCALE>,
+                                                     kWarpsPerCta * 32, smem),
+       "occupancy");
+    bps = std::max(1, b);
+  }
+  constexpr uint64_t wpb = kWarpsPerCta;
+  const uint64_t cap = uint64_t(num_sms) * bps * wpb;
   const uint64_t warps = std::max<uint64_t>(1, std::min(cap, tickets));
   const int grid = int((warps + wpb - 1) / wpb);
   p.total_warps = uint32_t(grid * wpb);
-  p.batch = uint32_t(std::clamp<uint64_t>(tickets / (uint64_t(p.total_warps) * 2), 1, 16));
-  cbm_fused_kernel<V, U, PF, NORM, SCALE><<<grid, kThreads, 0, s>>>(p);
+  void* args[] = {&p};
+  ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&cbm_kernel<V, D, NORM, SCALE>),
+                                 dim3(grid), dim3(kWarpsPerCta * 32), args, smem, s),
+     "cbm_kernel cooperative launch");
 }
 
-template <int V, int U>
-void run_fused(Params& p, uint64_t tickets, bool norm, bool scl, int num_sms, cudaStream_t s) {
-  constexpr int PF = (32 / (V * U)) < 2 ? 2 : ((32 / (V * U)) > 16 ? 16 : (32 / (V * U)));
-  if (!norm) launch_one<V, U, PF, false, false>(p, tickets, num_sms, s);
-  else if (scl) launch_one<V, U, PF, true, true>(p, tickets, num_sms, s);
-  else launch_one<V, U, PF, true, false>(p, tickets, num_sms, s);
-}
-
-template <int V>
-void run_fused_u(uint32_t U, Params& p, uint64_t tickets, bool norm, bool scl, int num_sms,
-                 cudaStream_t s) {
-  if (U == 4) run_fused<V, 4>(p, tickets, norm, scl, num_sms, s);
-  else if (U == 2) run_fused<V, 2>(p, tickets, norm, scl, num_sms, s);
-  else run_fused<V, 1>(p, tickets, norm, scl, num_sms, s);
+template <int V, int D>
+void run_kernel(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl, DeviceMatrix* h,
+                cudaStream_t s) {
+  if (!norm) launch_one<V, D, false, false>(p, tickets, slabs, h, s);
+  else if (scl) launch_one<V, D, true, true>(p, tickets, slabs, h, s);
+  else launch_one<V, D, true, false>(p, tickets, slabs, h, s);
 }
 
 template <typename T>
@@ -423,22 +513,19 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
                                       cudaMemcpyHostToDevice), what);
       h->device_bytes += vec.size() * sizeof(E);
     };
-    put(h->dptr, L.dptr, "upload dptr");
     put(h->dcol, L.dcol, "upload dcol");
-    put(h->meta, L.meta, "upload meta");
-    put(h->pcnt, L.pcnt, "upload pcnt");
+    put(h->rec, L.rec, "upload rec");
     if (L.normalized) {
-      put(h->oslot, L.oslot, "upload oslot");
+      put(h->srow, L.srow, "upload srow");
       put(h->scale, L.scale, "upload scale");
     }
-    ck(cudaMalloc(&h->counters, 2 * sizeof(uint32_t)), "counters");
-    ck(cudaMemset(h->counters, 0, 2 * sizeof(uint32_t)), "counters");
+    int coop = 0;
+    ck(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev), "attr");
+    if (!coop) throw cuda_error("device lacks cooperative launch", CBM_B200_ECUDA);
     // keep only sizes on the host
-    L.dptr = {};
     L.dcol = {};
-    L.meta = {};
-    L.pcnt = {};
-    L.oslot = {};
+    L.rec = {};  // item_beg stays: it drives the per-warp work partition
+    L.srow = {};
     L.scale = {};
     h->info = std::move(L);
   } catch (...) {
@@ -451,8 +538,9 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
 void device_free(DeviceMatrix* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  for (void* p : {(void*)h->dptr, (void*)h->dcol, (void*)h->meta, (void*)h->pcnt, (void*)h->oslot,
-                  (void*)h->scale, (void*)h->counters, (void*)h->flags, (void*)h->partial,
+  for (auto& pr : h->parts) cudaFree(pr.dev);
+  for (void* p : {(void*)h->dcol, (void*)h->rec, (void*)h->srow, (void*)h->scale,
+                  (void*)h->flags, (void*)h->partial,
                   (void*)h->interior, (void*)h->xs, (void*)h->xstage, (void*)h->ystage})
     if (p) cudaFree(p);
   delete h;
@@ -461,8 +549,8 @@ void device_free(DeviceMatrix* h) {
 namespace {
 uint32_t pick_vec(uint32_t d, const float* x, int64_t ldx, const float* y, int64_t ldy) {
   auto al = [](const void* p, unsigned b) { return (reinterpret_cast<uintptr_t>(p) % b) == 0; };
-  if (d > 64 && d % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && al(x, 16) && al(y, 16)) return 4;
-  if (d > 32 && d % 2 == 0 && ldx % 2 == 0 && ldy % 2 == 0 && al(x, 8) && al(y, 8)) return 2;
+  if (d > 32 && d % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && al(x, 16) && al(y, 16)) return 4;
+  if (d > 16 && d % 2 == 0 && ldx % 2 == 0 && ldy % 2 == 0 && al(x, 8) && al(y, 8)) return 2;
   return 1;
 }
 }  // namespace
@@ -510,21 +598,18 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     xin = h->xs;
     ldin = dpad;
   }
-  const uint32_t V = pick_vec(d, xin, ldin, y, ldy);
-  // columns per ticket: up to 4 segments of 32*V columns (<= 512 floats)
-  const uint32_t segs = (d + 32 * V - 1) / (32 * V);
-  const uint32_t U = segs >= 3 ? 4 : segs;
-  const uint32_t n_slabs = (d + 32 * V * U - 1) / (32 * V * U);
+  // lanes x V floats per column slab: V = 4 (LDG.128) when rows are 16-byte
+  // aligned multiples, else 2 or 1; kernel option 1 forces scalar lanes
+  const uint32_t V = h->opt.kernel == 1 ? 1u : pick_vec(d, xin, ldin, y, ldy);
+  const uint32_t n_slabs = (d + 32 * V - 1) / (32 * V);
   if (++h->epoch == 0) {  // wrapped: re-zero the flags
     ck(cudaMemsetAsync(h->flags, 0, h->flags_cap * sizeof(uint32_t), s), "flags memset");
     h->epoch = 1;
   }
   Params p;
-  p.dptr = h->dptr;
+  p.rec = reinterpret_cast<const uint4*>(h->rec);
+  p.srow = h->srow;
   p.dcol = h->dcol;
-  p.meta = reinterpret_cast<const uint4*>(h->meta);
-  p.pcnt = h->pcnt;
-  p.oslot = h->oslot;
   p.scale = h->scale;
   p.x = xin;
   p.ldx = ldin;
@@ -533,7 +618,6 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   p.partial = h->partial;
   p.interior = h->interior;
   p.flags = h->flags;
-  p.counters = h->counters;
   p.n_items = L.n_items;
   p.n_chunk = L.n_chunk_items;
   p.d = d;
@@ -544,10 +628,10 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   p.epoch = h->epoch;
 
   const bool norm = L.normalized, scl = L.normalized && !prescale;
-  if (V == 4) run_fused_u<4>(U, p, tickets, norm, scl, h->num_sms, s);
-  else if (V == 2) run_fused_u<2>(U, p, tickets, norm, scl, h->num_sms, s);
-  else run_fused_u<1>(U, p, tickets, norm, scl, h->num_sms, s);
-  ck(cudaGetLastError(), "cbm_fused launch");
+  if (V == 4) run_kernel<4, 8>(p, tickets, n_slabs, norm, scl, h, s);
+  else if (V == 2) run_kernel<2, 16>(p, tickets, n_slabs, norm, scl, h, s);
+  else run_kernel<1, 16>(p, tickets, n_slabs, norm, scl, h, s);
+  ck(cudaGetLastError(), "cbm_kernel launch");
   ++h->last_launches;
 }
 

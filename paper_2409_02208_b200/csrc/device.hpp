@@ -6,6 +6,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "errors.hpp"
 #include "layout.hpp"
@@ -18,15 +19,12 @@ struct DeviceMatrix {
   Layout info;  // sizes only after upload (host vectors released)
   cbm_b200_options opt{};
   // structure (immutable)
-  uint32_t* dptr = nullptr;
   uint32_t* dcol = nullptr;
-  uint32_t* meta = nullptr;
-  uint32_t* pcnt = nullptr;
-  uint32_t* oslot = nullptr;
+  uint32_t* rec = nullptr;
+  float* srow = nullptr;
   float* scale = nullptr;
   uint64_t device_bytes = 0;
   // per-call workspace (grown on demand, or by cbm_b200_reserve)
-  uint32_t* counters = nullptr;  // [0] ticket, [1] exit count (self-resetting)
   uint32_t* flags = nullptr;
   uint64_t flags_cap = 0;        // entries
   float* partial = nullptr;
@@ -39,6 +37,11 @@ struct DeviceMatrix {
   uint64_t xstage_cap = 0;
   float* ystage = nullptr;
   uint64_t ystage_cap = 0;
+  struct Partition {  // per-warp ticket ranges for one launch shape
+    uint32_t warps, slabs;
+    uint32_t* dev;
+  };
+  std::vector<Partition> parts;
   uint32_t epoch = 0;
   uint32_t last_launches = 0;
   std::mutex mu;

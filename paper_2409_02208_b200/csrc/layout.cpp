@@ -100,8 +100,8 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   }
 
   // split plan for long rows (default mode only)
-  if (split_threshold == 0) split_threshold = 96;
-  if (chunk == 0) chunk = 48;
+  if (split_threshold == 0) split_threshold = 32;
+  if (chunk == 0) chunk = 32;
   if (chunk > split_threshold) chunk = split_threshold;
   std::vector<uint32_t> pieces(m, 1);  // per ROW position i
   uint64_t n_leaf = 0;
@@ -159,13 +159,16 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   for (uint32_t i = 0; i < m; ++i)
     if (interior[rows[i]]) slot[rows[i]] = L.n_interior++;
 
-  L.dptr.assign(size_t(L.n_items) + 1, 0);
   L.dcol.resize(nnz);
-  L.meta.assign(size_t(L.n_items) * 4, 0);
-  L.pcnt.assign(L.n_items, 0);
-  if (L.normalized) L.oslot.assign(L.n_items, kNoItem);
-  // delta ranges: items own [dptr[t], dptr[t+1]); fill in item order
+  L.rec.assign(size_t(L.n_items) * 8, 0);
+  if (L.normalized) L.srow.assign(L.n_items, 0.0f);
+  auto R = [&](uint32_t t) { return &L.rec[size_t(t) * 8]; };
+  // delta ranges: items own [beg, end) of dcol, laid out in item order
   std::vector<uint64_t> own_lo(L.n_items, 0), own_hi(L.n_items, 0);
+  for (uint32_t t = 0; t < L.n_items; ++t) {
+    R(t)[3] = kNoItem;
+    R(t)[7] = kNoItem;
+  }
   for (uint32_t i = 0; i < m; ++i) {
     const uint32_t r = rows[i];
     const uint64_t lo = v.row_ptr[r], hi = v.row_ptr[r + 1];
@@ -181,39 +184,43 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
       const uint32_t t = first_at[0][i] + q - 1;
       own_lo[t] = lo + uint64_t(q) * chunk;
       own_hi[t] = std::min<uint64_t>(hi, own_lo[t] + chunk);
-      L.meta[size_t(t) * 4 + 0] = r;
-      L.meta[size_t(t) * 4 + 1] = kNoItem;
+      R(t)[2] = r;
     }
     // merge levels: node j at level lv sums nodes [j*F, min((j+1)*F, n_prev)) of lv-1
     for (uint32_t lv = 1; lv < nl[i]; ++lv) {
       const uint32_t n_prev = count_at[lv - 1][i];
       for (uint32_t j = 0; j < count_at[lv][i]; ++j) {
         const uint32_t t = first_at[lv][i] + j;
-        L.meta[size_t(t) * 4 + 0] = r;
-        L.meta[size_t(t) * 4 + 1] = kNoItem;
-        L.meta[size_t(t) * 4 + 3] = first_at[lv - 1][i] + j * kFanIn;
-        L.pcnt[t] = std::min(kFanIn, n_prev - j * kFanIn);
+        R(t)[2] = r;
+        R(t)[5] = first_at[lv - 1][i] + j * kFanIn;
+        R(t)[6] = std::min(kFanIn, n_prev - j * kFanIn);
       }
     }
     const uint32_t top = nl[i] - 1;
-    L.meta[size_t(t_row) * 4 + 3] = first_at[top][i];
-    L.pcnt[t_row] = count_at[top][i];
+    R(t_row)[5] = first_at[top][i];
+    R(t_row)[6] = count_at[top][i];
   }
   uint64_t o = 0;
   for (uint32_t t = 0; t < L.n_items; ++t) {
+    R(t)[0] = uint32_t(o);
     for (uint64_t k = own_lo[t]; k < own_hi[t]; ++k)
       L.dcol[o++] = v.col_idx[k] | (v.values[k] < 0.0f ? kSignBit : 0u);
-    L.dptr[t + 1] = uint32_t(o);
+    R(t)[1] = uint32_t(o);
   }
+  L.item_beg.resize(size_t(L.n_items) + 1);
+  for (uint32_t t = 0; t < L.n_items; ++t) L.item_beg[t] = R(t)[0];
+  L.item_beg[L.n_items] = uint32_t(o);
   for (uint32_t i = 0; i < m; ++i) {  // ROW items
     const uint32_t r = rows[i];
     const uint32_t t = L.n_chunk_items + i;
-    uint32_t* mt = &L.meta[size_t(t) * 4];
     const uint32_t p = v.parent[r];
-    mt[0] = r | (interior[r] ? kInteriorBit : 0u);
-    mt[1] = p == kVirtual ? kNoItem : item_of_row[p];
-    mt[2] = p == kVirtual ? 0u : (L.normalized ? slot[p] : p);
-    if (L.normalized) L.oslot[t] = slot[r];
+    R(t)[2] = r | (interior[r] ? kInteriorBit : 0u);
+    R(t)[3] = p == kVirtual ? kNoItem : item_of_row[p];
+    R(t)[4] = p == kVirtual ? 0u : (L.normalized ? slot[p] : p);
+    if (L.normalized) {
+      R(t)[7] = slot[r];
+      L.srow[t] = L.scale[r];
+    }
   }
   return L;
 }

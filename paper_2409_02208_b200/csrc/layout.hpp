@@ -40,18 +40,20 @@ struct Layout {
   uint32_t n_interior = 0;     // rows with children (scratch slots, normalized)
   uint32_t n_levels = 0, n_roots = 0, max_row_deltas = 0;
   uint64_t nnz = 0;
-  std::vector<uint32_t> dptr;   // n_items + 1: item t owns dcol[dptr[t], dptr[t+1])
-  std::vector<uint32_t> dcol;   // column | sign << 31
-  // meta, 4 x u32 per item:
-  //   [0] row | kInteriorBit (row has children -> publishes a ready flag)
-  //   [1] ppos: item index of the parent's ROW item, or kNoItem
-  //   [2] psrc: where the parent's unscaled row lives: its row id (plain) or
-  //       its interior scratch slot (normalized)
-  //   [3] first partial item summed after the own deltas (see pcnt)
-  std::vector<uint32_t> meta;
-  std::vector<uint32_t> pcnt;   // per item: number of partials [meta[3], meta[3]+pcnt)
-  std::vector<uint32_t> oslot;  // per item: own scratch slot (normalized interior) or kNoItem
-  std::vector<float> scale;     // row_scale (normalized)
+  std::vector<uint32_t> dcol;   // column | sign << 31, in item order
+  // rec, 8 x u32 per item (two uint4 loads on the device):
+  //   [0] beg, [1] end   : the item owns dcol[beg, end)
+  //   [2] row | kInteriorBit (row has children -> publishes a ready flag)
+  //   [3] ppos  : item index of the parent's ROW item, or kNoItem
+  //   [4] psrc  : where the parent's unscaled row lives: its row id (plain) or
+  //               its interior scratch slot (normalized)
+  //   [5] first : first partial item summed after the own deltas
+  //   [6] cnt   : number of partials [first, first + cnt)
+  //   [7] slot  : own interior scratch slot (normalized parents) or kNoItem
+  std::vector<uint32_t> rec;
+  std::vector<float> srow;      // per item: row_scale[row] (normalized)
+  std::vector<float> scale;     // row_scale (normalized), indexed by column
+  std::vector<uint32_t> item_beg;  // n_items + 1: delta prefix by item (kept on the host)
   std::vector<uint32_t> level_ptr;  // ROW-item offsets of each level (relative to the ROW block)
 };
 

@@ -45,9 +45,16 @@ def test_golden_fixture_bitwise(name, faithful, dev):
         d = P.DeviceCbm(c, order_faithful=faithful)
         v = torch.from_numpy(g["x"]).to(dev)
         got = d.spmv(v).cpu().numpy()
+        split = d.info()["n_chunk_items"] > 0
     else:
-        got, _ = gpu_spmm(c, g["x"], dev, order_faithful=faithful)
-    assert_bitwise(got, g["y"], name)
+        got, d = gpu_spmm(c, g["x"], dev, order_faithful=faithful)
+        split = d.info()["n_chunk_items"] > 0
+    integer = np.array_equal(g["x"], np.round(g["x"]))
+    if split and not (integer and not c.is_normalized):
+        # chunked long rows change the summation order: tolerance, not bits
+        assert normwise_err(got, g["y"]) <= TOL, name
+    else:
+        assert_bitwise(got, g["y"], name)
 
 
 # ------------------------------------------------------------- known answers
@@ -103,13 +110,14 @@ def _suite(normalized, n_cases, seed0):
         yield k, c, x
 
 
+@pytest.mark.parametrize("kernel", ["auto", "scalar"])
 @pytest.mark.parametrize("normalized", [False, True])
-def test_random_suite_bitwise(normalized, dev):
-    """Reference suites (test_kernels.cpp:75-114 style, all d paths): rows are
-    short, nothing is split, so both modes are bit-identical to the oracle."""
+def test_random_suite_bitwise(normalized, kernel, dev):
+    """Reference suites (test_kernels.cpp:75-114 style, all d paths, both kernel
+    families): rows are short, nothing is split, so results are bit-identical."""
     for k, c, x in _suite(normalized, 60, 9000 + 100 * normalized):
         want = O.oracle_spmm(oracle_arrays(c), x)
-        got, _ = gpu_spmm(c, x, dev)
+        got, _ = gpu_spmm(c, x, dev, kernel=kernel)
         assert_bitwise(got, want, f"case {k} d={x.shape[1]}")
 
 
@@ -194,20 +202,22 @@ def test_cfg0_full_size_integer_bitexact(dev):
     x = P.generate_dense("int", 4096, 64, 0xC0F61000, -8, 8)
     want = O.oracle_spmm(oracle_arrays(c), x)
     for faithful in (True, False):
-        got, _ = gpu_spmm(c, x, dev, order_faithful=faithful)
-        assert_bitwise(got, want, f"cfg0 faithful={faithful}")
+        for kernel in ("auto", "scalar"):
+            got, _ = gpu_spmm(c, x, dev, order_faithful=faithful, kernel=kernel)
+            assert_bitwise(got, want, f"cfg0 faithful={faithful} kernel={kernel}")
 
 
-def test_cfg1_full_size_gaussian(dev):
+@pytest.mark.parametrize("kernel", ["auto", "scalar"])
+def test_cfg1_full_size_gaussian(kernel, dev):
     """cfg[1]: n=19,717 normalized, X N(0,1), d=512: order-faithful is
     bit-exact, the default split mode within 1e-5 normwise."""
     a = P.generate_graph("pa_triangle", [19717, 2, 0.3], 0xC0F60001)
     c = P.build_cbm_normalized(a, 0, threads=8)
     x = P.generate_dense("normal", 19717, 512, 0xC0F61001)
     want = O.oracle_spmm(oracle_arrays(c), x)
-    got, _ = gpu_spmm(c, x, dev, order_faithful=True)
+    got, _ = gpu_spmm(c, x, dev, order_faithful=True, kernel=kernel)
     assert_bitwise(got, want, "cfg1 faithful")
-    got, _ = gpu_spmm(c, x, dev)
+    got, _ = gpu_spmm(c, x, dev, kernel=kernel)
     assert normwise_err(got, want) <= TOL
 
 
