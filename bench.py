@@ -58,14 +58,6 @@ def dist_env():
     return rank, world, local
 
 
-def column_slab(d, world, rank, align=4):
-    """Contiguous column slab of rank (multiples of `align` where possible)."""
-    units = (d + align - 1) // align
-    lo = units * rank // world * align
-    hi = min(d, units * (rank + 1) // world * align)
-    return lo, max(lo, hi)
-
-
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -225,6 +217,7 @@ def run_ours(args, wl):
     t_upload = time.perf_counter() - t0
     info = op.info()
 
+    from paper_2409_02208_b200.sharding import column_slab
     lo, hi = column_slab(wl.d, world, rank)
     d_local = hi - lo
     x_full = wl.operand(a.n_cols)
