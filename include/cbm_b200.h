@@ -111,6 +111,8 @@ typedef struct cbm_b200_options {
                                 products, removes the per-delta FMUL) */
   int32_t kernel;            /* 0 auto (LDG.128-wide lanes when rows allow),
                                 1 force scalar lanes (one float per lane) */
+  int32_t max_segments;      /* column segments (32 lanes x V floats) per work
+                                ticket: 0 auto (up to 4), 1 or 2 to cap */
 } cbm_b200_options;
 
 void cbm_b200_default_options(cbm_b200_options* opt);

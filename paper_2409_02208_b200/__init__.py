@@ -71,7 +71,7 @@ class _CbmView(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("order_faithful", C.c_int32),
                 ("split_threshold", C.c_uint32), ("chunk", C.c_uint32), ("prescale", C.c_int32),
-                ("kernel", C.c_int32)]
+                ("kernel", C.c_int32), ("max_segments", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -302,7 +302,7 @@ class DeviceCbm:
 
     def __init__(self, c: CbmMatrix, device: int | None = None, order_faithful: bool = False,
                  split_threshold: int = 0, chunk: int = 0, prescale: int = -1,
-                 kernel: str = "auto"):
+                 kernel: str = "auto", max_segments: int = 0):
         opt = _Options()
         _lib.cbm_b200_default_options(C.byref(opt))
         opt.device = -1 if device is None else int(device)
@@ -311,6 +311,7 @@ class DeviceCbm:
         opt.chunk = chunk
         opt.prescale = prescale
         opt.kernel = {"auto": 0, "scalar": 1}[kernel]
+        opt.max_segments = max_segments
         self._h = _vp()
         view = c._view()
         _check(_lib.cbm_b200_upload(C.byref(view), C.byref(opt), C.byref(self._h)))

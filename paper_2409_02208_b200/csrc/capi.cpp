@@ -152,6 +152,7 @@ void cbm_b200_default_options(cbm_b200_options* o) {
   o->chunk = 0;
   o->prescale = -1;
   o->kernel = 0;
+  o->max_segments = 0;
 }
 
 int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,

@@ -126,7 +126,7 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* f) {
 
 __device__ __forceinline__ void await(const uint32_t* f, uint32_t epoch) {
   if ((threadIdx.x & 31) == 0) {
-    while (ld_acquire(f) != epoch) __nanosleep(32);
+    while (ld_acquire(f) != epoch) __nanosleep(128);
   }
   __syncwarp();
   (void)ld_acquire(f);  // every lane orders its own subsequent loads
@@ -151,31 +151,38 @@ struct Params {
 
 // acc += partial[first], partial[first+1], ... in order. The producers' ready
 // flags are checked 32 at a time (one lane each), then the partial rows are
-// streamed with PF loads in flight.
-template <int V, int PF>
+// streamed with PF loads in flight. U segments of 32*V floats per lane.
+template <int V, int U, int PF>
 __device__ __forceinline__ void add_partials(const Params& p, const uint32_t* flag_base,
                                              uint32_t first, uint32_t cnt, uint32_t col,
-                                             bool active, typename Vec<V>::T& acc) {
+                                             typename Vec<V>::T (&acc)[U]) {
   using W = Vec<V>;
   const int lane = threadIdx.x & 31;
   for (uint32_t b0 = 0; b0 < cnt; b0 += 32) {
     const uint32_t nb = min(32u, cnt - b0);
     if (uint32_t(lane) < nb) {
       const uint32_t* f = flag_base + first + b0 + lane;
-      while (ld_acquire(f) != p.epoch) __nanosleep(32);
+      while (ld_acquire(f) != p.epoch) __nanosleep(128);
     }
     __syncwarp();
 #pragma unroll 1
     for (uint32_t j = 0; j < nb; j += PF) {
-      typename W::T v[PF];
+      typename W::T v[PF][U];
 #pragma unroll
       for (int q = 0; q < PF; ++q)
-        v[q] = (j + q < nb && active)
-                   ? W::ldcg(p.partial + (size_t)(first + b0 + j + q) * p.dpad + col)
-                   : W::zero();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = col + uint32_t(u) * 32u * V;
+          v[q][u] = (j + q < nb && c < p.d)
+                        ? W::ldcg(p.partial + (size_t)(first + b0 + j + q) * p.dpad + c)
+                        : W::zero();
+        }
 #pragma unroll
       for (int q = 0; q < PF; ++q)
-        if (j + q < nb) acc = W::add(acc, v[q]);
+        if (j + q < nb) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc[u] = W::add(acc[u], v[q][u]);
+        }
     }
   }
 }
@@ -210,59 +217,62 @@ __device__ __forceinline__ typename Vec<V>::T lds(const float* p) {
 constexpr int kWarpsPerCta = 4;
 constexpr uint32_t kRecWin = 64;  // ticket records staged per warp (two groups of 32)
 
-// One ticket's record in shared memory (2 x 16 bytes).
+// One ticket's record in shared memory (2 x 16 bytes) + its item and slab.
 struct alignas(16) TRec {
   uint32_t beg, end, rowk, ppos;
   uint32_t psrc, first, cnt, slot;
 };
 
-template <int V, int D, bool NORM, bool SCALE>
+template <int V, int U, int D, bool NORM, bool SCALE>
 struct alignas(16) WarpSmem {
-  float ring[D][32 * V];          // slot s, lane l: [s][l*V, l*V+V)
-  TRec rec[kRecWin];              // warp-sequence tickets [g, g+64), slot i & 63
+  float ring[D][U][32 * V];        // slot s, segment u, lane l: [s][u][l*V, l*V+V)
+  TRec rec[kRecWin];               // warp-sequence tickets [g, g+64), slot i & 63
+  uint32_t item[kRecWin];          // item index of the staged ticket
+  uint32_t slab[kRecWin];          // column slab of the staged ticket
   float srow[NORM ? kRecWin : 1];  // row scale per staged ticket
-  float sring[SCALE ? D : 1];     // the delta's column scale (lane 0 copies, all read)
+  float sring[SCALE ? D : 1];      // the delta's column scale (lane 0 copies, all read)
 };
 
 // Stage the records of warp-sequence tickets [i0, i0+32) (ticket w + i*W).
-template <int V, int D, bool NORM, bool SCALE>
-__device__ __forceinline__ void stage_recs(const Params& p, WarpSmem<V, D, NORM, SCALE>& sm,
-                                           uint32_t w, uint32_t i0, uint32_t n_w) {
+template <class SM>
+__device__ __forceinline__ void stage_recs(const Params& p, SM& sm, uint32_t w, uint32_t i0,
+                                           uint32_t n_w, bool norm) {
   const int lane = threadIdx.x & 31;
   const uint32_t i = i0 + uint32_t(lane);
   if (i < n_w) {
     const uint32_t T = w + i * p.total_warps;
-    const uint32_t t = T - (T / p.n_items) * p.n_items;
-    TRec& r = sm.rec[i & (kRecWin - 1)];
+    const uint32_t sl = T / p.n_items;
+    const uint32_t t = T - sl * p.n_items;
+    const uint32_t k = i & (kRecWin - 1);
+    TRec& r = sm.rec[k];
     *reinterpret_cast<uint4*>(&r.beg) = __ldg(p.rec + 2 * (size_t)t);
     *reinterpret_cast<uint4*>(&r.psrc) = __ldg(p.rec + 2 * (size_t)t + 1);
-    if constexpr (NORM) sm.srow[i & (kRecWin - 1)] = __ldg(p.srow + t);
+    sm.item[k] = t;
+    sm.slab[k] = sl;
+    if (norm) sm.srow[k] = __ldg(p.srow + t);
   }
 }
 
-template <int V, int D, bool NORM, bool SCALE>
+template <int V, int U, int D, bool NORM, bool SCALE>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) {
   using W = Vec<V>;
-  constexpr uint32_t kSlab = 32u * V;
-  constexpr int PFp = 8;
+  using T4 = typename W::T;
+  constexpr uint32_t kSeg = 32u * V;      // floats of one segment (one LDGSTS per lane)
+  constexpr uint32_t kSlab = kSeg * U;    // floats per ticket
+  constexpr int PFp = U >= 4 ? 2 : (U == 2 ? 4 : 8);
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  WarpSmem<V, D, NORM, SCALE>& sm =
-      reinterpret_cast<WarpSmem<V, D, NORM, SCALE>*>(smem_raw)[threadIdx.x >> 5];
+  using SM = WarpSmem<V, U, D, NORM, SCALE>;
+  SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= p.total_warps || w >= p.total_tickets) return;
   const uint32_t WW = p.total_warps;
   const uint32_t n_w = (p.total_tickets - w + WW - 1) / WW;  // tickets w, w+W, w+2W, ...
-  auto slab_of = [&](uint32_t i) { return (w + i * WW) / p.n_items; };
-  auto item_of = [&](uint32_t i) {
-    const uint32_t T = w + i * WW;
-    return T - (T / p.n_items) * p.n_items;
-  };
 
   uint32_t g = 0;  // staged records cover warp-sequence tickets [g, g + 64)
-  stage_recs(p, sm, w, 0, n_w);
-  stage_recs(p, sm, w, 32, n_w);
+  stage_recs(p, sm, w, 0, n_w, NORM);
+  stage_recs(p, sm, w, 32, n_w, NORM);
   __syncwarp();
   auto R = [&](uint32_t i) -> const TRec& { return sm.rec[i & (kRecWin - 1)]; };
   // first 32 column words of ticket i (0 past the end / outside the window)
@@ -275,7 +285,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   // ---- issue cursor: ticket ii, offset iq inside it. win = window of ii,
   // wn1 / wn2 = windows of ii+1 / ii+2 (fetched two tickets ahead)
   uint32_t ii = 0, iq = 0, ibeg = 0, ilen = 0, icol = 0;
-  bool iact = false;
   uint32_t win = window(0), wn1 = window(1), wn2 = window(2), wlong = 0;
   uint32_t iseq = 0;   // deltas issued
   uint32_t signs = 0;  // sign bit of the delta in each ring slot
@@ -285,8 +294,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     const TRec& r = R(ii);
     ibeg = r.beg;
     ilen = r.end - r.beg;
-    icol = slab_of(ii) * kSlab + uint32_t(lane) * V;
-    iact = icol < p.d;
+    icol = sm.slab[ii & (kRecWin - 1)] * kSlab + uint32_t(lane) * V;
     wlong = 32 + uint32_t(lane) < ilen ? __ldg(p.dcol + ibeg + 32 + lane) : 0u;
   };
   // step to the next ticket with deltas, shifting the window prefetch;
@@ -316,7 +324,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       const uint32_t cw = __shfl_sync(kFull, win, iq & 31);
       const uint32_t c = cw & 0x7FFFFFFFu;
       const uint32_t s = iseq & (D - 1);
-      if (iact) cp_async<V>(&sm.ring[s][lane * V], p.x + (long long)c * p.ldx + icol);
+      const float* src = p.x + (long long)c * p.ldx + icol;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (icol + uint32_t(u) * kSeg < p.d) cp_async<V>(&sm.ring[s][u][lane * V], src + u * kSeg);
       if constexpr (SCALE)
         if (lane == 0) cp_async_f(&sm.sring[s], p.scale + c);
       signs = (signs & ~(1u << s)) | ((cw >> 31) << s);
@@ -342,7 +353,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   for (uint32_t ci = 0; ci < n_w; ++ci) {
     if (ci - g == 32) {  // slide the record window by one group
       __syncwarp();
-      stage_recs(p, sm, w, g + kRecWin, n_w);
+      stage_recs(p, sm, w, g + kRecWin, n_w, NORM);
       g += 32;
       __syncwarp();
       if (iblocked) {
@@ -350,30 +361,43 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
         next_ticket();
       }
     }
-    const TRec r = R(ci);
-    const uint32_t slab = slab_of(ci), t = item_of(ci);
+    const uint32_t k_ci = ci & (kRecWin - 1);
+    const TRec r = sm.rec[k_ci];
+    const uint32_t slab = sm.slab[k_ci], t = sm.item[k_ci];
     const uint32_t col = slab * kSlab + uint32_t(lane) * V;
-    const bool active = col < p.d;
-    typename W::T acc = W::zero();
+    T4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = W::zero();
 #pragma unroll 1
     for (uint32_t k = r.beg; k < r.end; ++k) {
-      cp_wait<D - 1>();  // this lane's copy of delta `cseq` has landed
+      cp_wait<D - 1>();  // this lane's copies of delta `cseq` have landed
       const uint32_t s = cseq & (D - 1);
-      typename W::T v = active ? lds<V>(&sm.ring[s][lane * V]) : W::zero();
+      float sc = 1.0f;
       if constexpr (SCALE) {
         __syncwarp();  // lane 0's scale copy (covered by its wait) is visible
-        v = W::mul(v, sm.sring[s]);
+        sc = sm.sring[s];
       }
-      acc = ((signs >> s) & 1u) ? W::sub(acc, v) : W::add(acc, v);
+      const bool neg = (signs >> s) & 1u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (col + uint32_t(u) * kSeg < p.d) {
+          T4 v = lds<V>(&sm.ring[s][u][lane * V]);
+          if constexpr (SCALE) v = W::mul(v, sc);
+          acc[u] = neg ? W::sub(acc[u], v) : W::add(acc[u], v);
+        }
+      }
       ++cseq;
       __syncwarp();  // slot s fully read before its refill
       issue_one();
     }
     // ---- epilogue: partials, then CHUNK/MERGE publish or ROW stage 2 + 3
     uint32_t* flag_base = p.flags + (size_t)slab * p.n_items;
-    if (r.cnt) add_partials<V, PFp>(p, flag_base, r.first, r.cnt, col, active, acc);
+    if (r.cnt) add_partials<V, U, PFp>(p, flag_base, r.first, r.cnt, col, acc);
     if (t < p.n_chunk) {
-      if (active) W::st(p.partial + (size_t)t * p.dpad + col, acc);
+      float* dst = p.partial + (size_t)t * p.dpad;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (col + uint32_t(u) * kSeg < p.d) W::st(dst + col + u * kSeg, acc[u]);
       publish(flag_base + t, p.epoch);
       continue;
     }
@@ -381,19 +405,32 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       await(flag_base + r.ppos, p.epoch);
       const float* src =
           NORM ? p.interior + (size_t)r.psrc * p.dpad : p.y + (long long)r.psrc * p.ldy;
-      if (active) acc = W::add(acc, W::ldcg(src + col));
+      T4 pv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        pv[u] = col + uint32_t(u) * kSeg < p.d ? W::ldcg(src + col + u * kSeg) : W::zero();
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u] = W::add(acc[u], pv[u]);
     }
     const uint32_t row = r.rowk & 0x7FFFFFFFu;
     const bool is_parent = (r.rowk >> 31) != 0;
+    float* yrow = p.y + (long long)row * p.ldy;
     if constexpr (NORM) {
       if (is_parent) {  // children read the unscaled row from scratch
-        if (active) W::st(p.interior + (size_t)r.slot * p.dpad + col, acc);
+        float* dst = p.interior + (size_t)r.slot * p.dpad;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (col + uint32_t(u) * kSeg < p.d) W::st(dst + col + u * kSeg, acc[u]);
         publish(flag_base + t, p.epoch);
       }
-      const float sr = sm.srow[ci & (kRecWin - 1)];
-      if (active) W::st(p.y + (long long)row * p.ldy + col, W::mul(acc, sr));
+      const float sr = sm.srow[k_ci];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (col + uint32_t(u) * kSeg < p.d) W::st(yrow + col + u * kSeg, W::mul(acc[u], sr));
     } else {
-      if (active) W::st(p.y + (long long)row * p.ldy + col, acc);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (col + uint32_t(u) * kSeg < p.d) W::st(yrow + col + u * kSeg, acc[u]);
       if (is_parent) publish(flag_base + t, p.epoch);
     }
   }
@@ -415,71 +452,39 @@ __global__ void prescale_kernel(const float* __restrict__ x, long long ldx,
 
 // Cooperative launch: one full residency wave (all warps co-resident), no
 // more warps than tickets.
-// Contiguous ticket ranges per warp, balanced by cost = deltas + kItemCost per
-// item (the epilogue of an item costs about as much as a few deltas).
-constexpr uint64_t kItemCost = 4;
-const uint32_t* warp_ranges(DeviceMatrix* h, uint32_t warps, uint32_t slabs) {
-  for (const auto& pr : h->parts)
-    if (pr.warps == warps && pr.slabs == slabs) return pr.dev;
-  const Layout& L = h->info;
-  const uint64_t n = L.n_items, per_slab = uint64_t(L.item_beg[n]) + kItemCost * n;
-  const uint64_t tickets = n * slabs, total = per_slab * slabs;
-  auto cost = [&](uint64_t T) {  // cost of tickets [0, T)
-    const uint64_t sl = T / n, t = T - sl * n;
-    return sl * per_slab + L.item_beg[t] + kItemCost * t;
-  };
-  std::vector<uint32_t> ws(size_t(warps) + 1);
-  for (uint32_t w = 0; w <= warps; ++w) {
-    const uint64_t target = total * w / warps;
-    uint64_t lo = 0, hi = tickets;  // first T with cost(T) >= target
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) / 2;
-      if (cost(mid) < target) lo = mid + 1;
-      else hi = mid;
-    }
-    ws[w] = uint32_t(lo);
-  }
-  ws[warps] = uint32_t(tickets);
-  uint32_t* dev = nullptr;
-  ck(cudaMalloc(&dev, ws.size() * sizeof(uint32_t)), "warp ranges");
-  ck(cudaMemcpy(dev, ws.data(), ws.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
-     "warp ranges");
-  h->parts.push_back({warps, slabs, dev});
-  return dev;
-}
-
-template <int V, int D, bool NORM, bool SCALE>
-void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
-  const int num_sms = h->num_sms;
-  constexpr size_t smem = kWarpsPerCta * sizeof(WarpSmem<V, D, NORM, SCALE>);
+template <int V, int U, int D, bool NORM, bool SCALE>
+void launch_one(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
+  constexpr size_t smem = kWarpsPerCta * sizeof(WarpSmem<V, U, D, NORM, SCALE>);
   static int bps = -1;  // per template instance
   if (bps < 0) {
-    ck(cudaFuncSetAttribute(cbm_kernel<V, D, NORM, SCALE>,
+    ck(cudaFuncSetAttribute(cbm_kernel<V, U, D, NORM, SCALE>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
        "smem attribute");
     int b = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_kernel<V, D, NORM, SCALE>,
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_kernel<V, U, D, NORM, SCALE>,
                                                      kWarpsPerCta * 32, smem),
        "occupancy");
     bps = std::max(1, b);
   }
+  // cooperative launch: one full residency wave, never more warps than tickets
   constexpr uint64_t wpb = kWarpsPerCta;
-  const uint64_t cap = uint64_t(num_sms) * bps * wpb;
+  const uint64_t cap = uint64_t(h->num_sms) * bps * wpb;
   const uint64_t warps = std::max<uint64_t>(1, std::min(cap, tickets));
   const int grid = int((warps + wpb - 1) / wpb);
   p.total_warps = uint32_t(grid * wpb);
   void* args[] = {&p};
-  ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&cbm_kernel<V, D, NORM, SCALE>),
-                                 dim3(grid), dim3(kWarpsPerCta * 32), args, smem, s),
+  ck(cudaLaunchCooperativeKernel(
+         reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SCALE>), dim3(grid),
+         dim3(kWarpsPerCta * 32), args, smem, s),
      "cbm_kernel cooperative launch");
 }
 
-template <int V, int D>
-void run_kernel(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl, DeviceMatrix* h,
+template <int V, int U, int D>
+void run_kernel(Params& p, uint64_t tickets, bool norm, bool scl, DeviceMatrix* h,
                 cudaStream_t s) {
-  if (!norm) launch_one<V, D, false, false>(p, tickets, slabs, h, s);
-  else if (scl) launch_one<V, D, true, true>(p, tickets, slabs, h, s);
-  else launch_one<V, D, true, false>(p, tickets, slabs, h, s);
+  if (!norm) launch_one<V, U, D, false, false>(p, tickets, h, s);
+  else if (scl) launch_one<V, U, D, true, true>(p, tickets, h, s);
+  else launch_one<V, U, D, true, false>(p, tickets, h, s);
 }
 
 template <typename T>
@@ -601,7 +606,13 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   // lanes x V floats per column slab: V = 4 (LDG.128) when rows are 16-byte
   // aligned multiples, else 2 or 1; kernel option 1 forces scalar lanes
   const uint32_t V = h->opt.kernel == 1 ? 1u : pick_vec(d, xin, ldin, y, ldy);
-  const uint32_t n_slabs = (d + 32 * V - 1) / (32 * V);
+  // segments of 32*V columns per ticket: wide X shares one ticket's record,
+  // indices and epilogue across up to 4 segments
+  const uint32_t segs = (d + 32 * V - 1) / (32 * V);
+  uint32_t U = segs >= 4 ? 4 : (segs >= 2 ? 2 : 1);
+  if (h->opt.max_segments == 1 || h->opt.max_segments == 2)
+    U = std::min<uint32_t>(U, uint32_t(h->opt.max_segments));
+  const uint32_t n_slabs = (d + 32 * V * U - 1) / (32 * V * U);
   if (++h->epoch == 0) {  // wrapped: re-zero the flags
     ck(cudaMemsetAsync(h->flags, 0, h->flags_cap * sizeof(uint32_t), s), "flags memset");
     h->epoch = 1;
@@ -628,9 +639,19 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   p.epoch = h->epoch;
 
   const bool norm = L.normalized, scl = L.normalized && !prescale;
-  if (V == 4) run_kernel<4, 8>(p, tickets, n_slabs, norm, scl, h, s);
-  else if (V == 2) run_kernel<2, 16>(p, tickets, n_slabs, norm, scl, h, s);
-  else run_kernel<1, 16>(p, tickets, n_slabs, norm, scl, h, s);
+  if (V == 4) {
+    if (U == 4) run_kernel<4, 4, 4>(p, tickets, norm, scl, h, s);
+    else if (U == 2) run_kernel<4, 2, 8>(p, tickets, norm, scl, h, s);
+    else run_kernel<4, 1, 8>(p, tickets, norm, scl, h, s);
+  } else if (V == 2) {
+    if (U == 4) run_kernel<2, 4, 8>(p, tickets, norm, scl, h, s);
+    else if (U == 2) run_kernel<2, 2, 8>(p, tickets, norm, scl, h, s);
+    else run_kernel<2, 1, 16>(p, tickets, norm, scl, h, s);
+  } else {
+    if (U == 4) run_kernel<1, 4, 16>(p, tickets, norm, scl, h, s);
+    else if (U == 2) run_kernel<1, 2, 16>(p, tickets, norm, scl, h, s);
+    else run_kernel<1, 1, 16>(p, tickets, norm, scl, h, s);
+  }
   ck(cudaGetLastError(), "cbm_kernel launch");
   ++h->last_launches;
 }
