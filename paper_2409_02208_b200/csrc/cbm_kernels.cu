@@ -543,7 +543,11 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
 void device_free(DeviceMatrix* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  for (auto& pr : h->parts) cudaFree(pr.dev);
+  if (h->s_in) {
+    cudaStreamDestroy(h->s_in);
+    cudaStreamDestroy(h->s_out);
+    for (auto e : h->ev) cudaEventDestroy(e);
+  }
   for (void* p : {(void*)h->dcol, (void*)h->rec, (void*)h->srow, (void*)h->scale,
                   (void*)h->flags, (void*)h->partial,
                   (void*)h->interior, (void*)h->xs, (void*)h->xstage, (void*)h->ystage})
@@ -656,6 +660,10 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   ++h->last_launches;
 }
 
+// Host-buffer entry point. Columns are independent (kernels.cpp:27-62), so X
+// and Y move in column chunks on three streams: H2D of chunk k+1 and D2H of
+// chunk k-1 run while chunk k multiplies, and the two copy directions overlap
+// on the full-duplex PCIe link. One chunk when the operand is small.
 void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, void* stream) {
   const Layout& L = h->info;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -663,21 +671,40 @@ void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, voi
   const uint32_t dpad = (d + 3) & ~3u;
   grow(h->xstage, h->xstage_cap, uint64_t(L.n_cols) * dpad, "staging X");
   grow(h->ystage, h->ystage_cap, uint64_t(L.n_rows) * dpad, "staging Y");
-  const size_t xb = size_t(L.n_cols) * d * sizeof(float);
-  const size_t yb = size_t(L.n_rows) * d * sizeof(float);
-  if (d == dpad) {
-    if (xb) ck(cudaMemcpyAsync(h->xstage, x, xb, cudaMemcpyHostToDevice, s), "H2D X");
-  } else if (xb) {
-    ck(cudaMemcpy2DAsync(h->xstage, dpad * sizeof(float), x, d * sizeof(float),
-                         d * sizeof(float), L.n_cols, cudaMemcpyHostToDevice, s), "H2D X");
+  if (!h->s_in) {
+    ck(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking), "stream");
+    for (auto& e : h->ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   }
-  device_spmm(h, h->xstage, dpad, d, h->ystage, dpad, stream);
-  if (d == dpad) {
-    if (yb) ck(cudaMemcpyAsync(y, h->ystage, yb, cudaMemcpyDeviceToHost, s), "D2H Y");
-  } else if (yb) {
-    ck(cudaMemcpy2DAsync(y, d * sizeof(float), h->ystage, dpad * sizeof(float),
-                         d * sizeof(float), L.n_rows, cudaMemcpyDeviceToHost, s), "D2H Y");
+  const uint64_t bytes = (uint64_t(L.n_cols) + L.n_rows) * d * sizeof(float);
+  uint32_t chunks = 1;
+  if (bytes >= (8u << 20) && d >= 256) chunks = std::min<uint32_t>(4, d / 128);
+  const uint32_t cw = ((d + chunks - 1) / chunks + 3) & ~3u;  // chunk width, 16-byte aligned
+  // ev[0]: caller's prior work on s; ev[1+k]: X chunk k landed; ev[5+k]: Y chunk k ready
+  ck(cudaEventRecord(h->ev[0], s), "event");
+  ck(cudaStreamWaitEvent(h->s_in, h->ev[0], 0), "wait");
+  ck(cudaStreamWaitEvent(h->s_out, h->ev[0], 0), "wait");
+  for (uint32_t k = 0, c0 = 0; c0 < d; ++k, c0 += cw) {
+    const uint32_t w = std::min(cw, d - c0);
+    ck(cudaMemcpy2DAsync(h->xstage + c0, dpad * sizeof(float), x + c0, d * sizeof(float),
+                         w * sizeof(float), L.n_cols, cudaMemcpyHostToDevice, h->s_in),
+       "H2D X");
+    ck(cudaEventRecord(h->ev[1 + k], h->s_in), "event");
   }
+  uint32_t launches = 0;
+  for (uint32_t k = 0, c0 = 0; c0 < d; ++k, c0 += cw) {
+    const uint32_t w = std::min(cw, d - c0);
+    ck(cudaStreamWaitEvent(s, h->ev[1 + k], 0), "wait");
+    device_spmm(h, h->xstage + c0, dpad, w, h->ystage + c0, dpad, stream);
+    launches += h->last_launches;
+    ck(cudaEventRecord(h->ev[5 + k], s), "event");
+    ck(cudaStreamWaitEvent(h->s_out, h->ev[5 + k], 0), "wait");
+    ck(cudaMemcpy2DAsync(y + c0, d * sizeof(float), h->ystage + c0, dpad * sizeof(float),
+                         w * sizeof(float), L.n_rows, cudaMemcpyDeviceToHost, h->s_out),
+       "D2H Y");
+  }
+  h->last_launches = launches;  // kernels launched by this call (one per chunk)
+  ck(cudaStreamSynchronize(h->s_out), "spmm_host synchronize");
   ck(cudaStreamSynchronize(s), "spmm_host synchronize");
 }
 

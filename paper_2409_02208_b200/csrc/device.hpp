@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "errors.hpp"
 #include "layout.hpp"
 
@@ -37,11 +39,9 @@ struct DeviceMatrix {
   uint64_t xstage_cap = 0;
   float* ystage = nullptr;
   uint64_t ystage_cap = 0;
-  struct Partition {  // per-warp ticket ranges for one launch shape
-    uint32_t warps, slabs;
-    uint32_t* dev;
-  };
-  std::vector<Partition> parts;
+  // host-API pipeline: copy-in / copy-out streams and chunk events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev[9] = {};
   uint32_t epoch = 0;
   uint32_t last_launches = 0;
   std::mutex mu;
