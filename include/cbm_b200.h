@@ -72,6 +72,12 @@ typedef struct cbm_b200_host_cbm cbm_b200_host_cbm;
 
 int cbm_b200_build(const cbm_b200_csr_view* a, uint64_t alpha, int32_t normalized,
                    int32_t degree_mode, int32_t threads, cbm_b200_host_cbm** out);
+/* Same, choosing the arborescence algorithm: 0 = mergeable-heap Edmonds
+ * (default, O(E log E)), 1 = the reference's round-synchronous contraction
+ * restated (O(E * rounds)). Both return the reference's chain. */
+int cbm_b200_build_ex(const cbm_b200_csr_view* a, uint64_t alpha, int32_t normalized,
+                      int32_t degree_mode, int32_t threads, int32_t algo,
+                      cbm_b200_host_cbm** out);
 /* Borrowed view of a built CBM; valid until cbm_b200_host_free. */
 int cbm_b200_host_view(const cbm_b200_host_cbm* c, cbm_b200_cbm_view* out);
 /* chain.branch_ptr (builder.hpp:38-40): n_branches+1 entries. */

@@ -93,6 +93,8 @@ _vp, _i64, _u64, _i32 = C.c_void_p, C.c_int64, C.c_uint64, C.c_int32
 _sig = {
     "cbm_b200_last_error": (C.c_char_p, []),
     "cbm_b200_build": (C.c_int, [C.POINTER(_CsrView), _u64, _i32, _i32, _i32, C.POINTER(_vp)]),
+    "cbm_b200_build_ex": (C.c_int, [C.POINTER(_CsrView), _u64, _i32, _i32, _i32, _i32,
+                                    C.POINTER(_vp)]),
     "cbm_b200_host_view": (C.c_int, [_vp, C.POINTER(_CbmView)]),
     "cbm_b200_host_branches": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_u64)]),
     "cbm_b200_host_stats": (C.c_int, [_vp, C.POINTER(_Stats)]),
@@ -214,11 +216,11 @@ def _copy(ptr, n, dtype):
     return np.frombuffer(buf, dtype=dtype, count=n).copy()
 
 
-def _build(a: CsrBinaryMatrix, alpha, normalized, degree_mode, threads) -> CbmMatrix:
+def _build(a: CsrBinaryMatrix, alpha, normalized, degree_mode, threads, algo=0) -> CbmMatrix:
     h = _vp()
     view = a._view()
-    _check(_lib.cbm_b200_build(C.byref(view), alpha, int(normalized), degree_mode,
-                               threads, C.byref(h)))
+    _check(_lib.cbm_b200_build_ex(C.byref(view), alpha, int(normalized), degree_mode,
+                                  threads, algo, C.byref(h)))
     try:
         v = _CbmView()
         _check(_lib.cbm_b200_host_view(h, C.byref(v)))
@@ -241,16 +243,20 @@ def _build(a: CsrBinaryMatrix, alpha, normalized, degree_mode, threads) -> CbmMa
         _lib.cbm_b200_host_free(h)
 
 
-def build_cbm(a: CsrBinaryMatrix, alpha: int = 0, threads: int = 1) -> CbmMatrix:
+_ALGO = {"heap": 0, "rounds": 1}
+
+
+def build_cbm(a: CsrBinaryMatrix, alpha: int = 0, threads: int = 1,
+              arborescence: str = "heap") -> CbmMatrix:
     """build_cbm (builder.hpp:99): same chain and delta matrix as the reference."""
-    return _build(a, alpha, False, 0, threads)
+    return _build(a, alpha, False, 0, threads, _ALGO[arborescence])
 
 
 def build_cbm_normalized(a: CsrBinaryMatrix, alpha: int = 0, threads: int = 1,
-                         degree_mode: str = "augmented") -> CbmMatrix:
+                         degree_mode: str = "augmented", arborescence: str = "heap") -> CbmMatrix:
     """build_cbm_normalized (builder.hpp:104-106): represents D^-1/2 (A+I) D^-1/2."""
     mode = {"augmented": 0, "original": 1}[degree_mode]
-    return _build(a, alpha, True, mode, threads)
+    return _build(a, alpha, True, mode, threads, _ALGO[arborescence])
 
 
 def count_scalar_ops(c: CbmMatrix) -> tuple[int, int]:

@@ -506,7 +506,7 @@ Csr with_diagonal(const Csr& a) {
 
 }  // namespace
 
-HostCbm build_cbm(const Csr& a, uint64_t alpha, int threads) {
+HostCbm build_cbm(const Csr& a, uint64_t alpha, int threads, int algo) {
   const auto t0 = Clock::now();
   HostCbm c;
   c.n_rows = a.n_rows;
@@ -516,7 +516,8 @@ HostCbm build_cbm(const Csr& a, uint64_t alpha, int threads) {
   c.t_edges = secs(t0);
   c.candidate_edges = e.src.size();
   const auto t1 = Clock::now();
-  c.parent = min_arborescence(e, a.n_rows, threads, &c.rounds);
+  c.parent = algo == 1 ? min_arborescence(e, a.n_rows, threads, &c.rounds)
+                       : min_arborescence_heap(e, a.n_rows, &c.rounds);
   EdgeLists().ptr.swap(e.ptr);
   std::vector<uint32_t>().swap(e.src);
   std::vector<uint32_t>().swap(e.w);
@@ -530,7 +531,7 @@ HostCbm build_cbm(const Csr& a, uint64_t alpha, int threads) {
 }
 
 HostCbm build_cbm_normalized(const Csr& a, uint64_t alpha, int threads,
-                             bool degrees_from_original) {
+                             bool degrees_from_original, int algo) {
   if (a.n_rows != a.n_cols)
     throw invalid_argument("build_cbm_normalized: matrix must be square");
   const auto t0 = Clock::now();
@@ -544,7 +545,7 @@ HostCbm build_cbm_normalized(const Csr& a, uint64_t alpha, int threads,
     // builder.cpp:420: real_t(1) / static_cast<real_t>(std::sqrt(double(d)))
     scale[x] = 1.0f / static_cast<float>(std::sqrt(static_cast<double>(d)));
   }
-  HostCbm c = build_cbm(aug, alpha, threads);
+  HostCbm c = build_cbm(aug, alpha, threads, algo);
   for (uint64_t k = 0; k < c.values.size(); ++k) c.values[k] *= scale[c.col_idx[k]];
   c.row_scale = std::move(scale);
   c.normalized = true;

@@ -70,6 +70,12 @@ const char* cbm_b200_last_error(void) { return g_err.c_str(); }
 // ------------------------------------------------------------------ builder
 int cbm_b200_build(const cbm_b200_csr_view* a, uint64_t alpha, int32_t normalized,
                    int32_t degree_mode, int32_t threads, cbm_b200_host_cbm** out) {
+  return cbm_b200_build_ex(a, alpha, normalized, degree_mode, threads, 0, out);
+}
+
+int cbm_b200_build_ex(const cbm_b200_csr_view* a, uint64_t alpha, int32_t normalized,
+                      int32_t degree_mode, int32_t threads, int32_t algo,
+                      cbm_b200_host_cbm** out) {
   return guard([&] {
     need(a && out, "build: null argument");
     *out = nullptr;
@@ -83,8 +89,8 @@ int cbm_b200_build(const cbm_b200_csr_view* a, uint64_t alpha, int32_t normalize
     const int t = threads > 0 ? threads : 1;
     auto* h = new cbm_b200_host_cbm;
     try {
-      h->c = normalized ? cbmb::build_cbm_normalized(csr, alpha, t, degree_mode == 1)
-                        : cbmb::build_cbm(csr, alpha, t);
+      h->c = normalized ? cbmb::build_cbm_normalized(csr, alpha, t, degree_mode == 1, algo)
+                        : cbmb::build_cbm(csr, alpha, t, algo);
     } catch (...) {
       delete h;
       throw;

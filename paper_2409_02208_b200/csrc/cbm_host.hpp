@@ -60,9 +60,10 @@ struct HostCbm {
 void chain_from_parents(HostCbm& c);
 
 // Full construction (build_cbm / build_cbm_normalized, builder.cpp:394-429).
-HostCbm build_cbm(const Csr& a, uint64_t alpha, int threads);
+// algo 0: heap-based Edmonds (default), 1: round-synchronous restatement.
+HostCbm build_cbm(const Csr& a, uint64_t alpha, int threads, int algo = 0);
 HostCbm build_cbm_normalized(const Csr& a, uint64_t alpha, int threads,
-                             bool degrees_from_original);
+                             bool degrees_from_original, int algo = 0);
 
 // ---- internals exposed for tests ------------------------------------------
 
@@ -80,6 +81,8 @@ EdgeLists candidate_edges(const Csr& a, uint64_t alpha, int threads);
 // parent[m] (kVirtual for roots). `rounds` receives the contraction count.
 std::vector<uint32_t> min_arborescence(const EdgeLists& e, uint32_t m, int threads,
                                        uint32_t* rounds);
+// Same arborescence with mergeable heaps, O(E log E) (arborescence.cpp).
+std::vector<uint32_t> min_arborescence_heap(const EdgeLists& e, uint32_t m, uint32_t* rounds);
 
 // ---- parallel helper (the reference's parallel_chunks, parallel.hpp:13-32)
 template <typename Fn>

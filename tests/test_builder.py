@@ -107,3 +107,29 @@ def test_builder_errors_mirror_reference():
     oob = P.CsrBinaryMatrix(1, 2, np.array([0, 1], np.uint64), np.array([5], np.uint32))
     with pytest.raises(ValueError, match="out of range"):
         P.build_cbm(oob, 0)
+
+
+@pytest.mark.parametrize("kind,params,normalized", [
+    ("community", [3000, 500, 0.8, 1e-3], True),        # cascading contractions (cfg[3] shape)
+    ("community", [4096, 64, 0.5, 0.001], False),       # cfg[0] shape
+    ("pa_triangle", [5000, 2, 0.3], True),              # cfg[1] shape
+    ("clique_overlay", [4000, 15000, 2, 10, 1.1], False),  # cfg[2] shape, scaled
+])
+def test_heap_edmonds_equals_round_synchronous(kind, params, normalized):
+    """The mergeable-heap Edmonds (default) selects exactly the reference's
+    round-synchronous contraction result (restated in min_arborescence)."""
+    a = P.generate_graph(kind, params, 11)
+    build = P.build_cbm_normalized if normalized else P.build_cbm
+    for alpha in (0, 4):
+        h = build(a, alpha, threads=8, arborescence="heap")
+        r = build(a, alpha, threads=8, arborescence="rounds")
+        assert same_cbm(h, r)
+        assert h.build_stats["rounds"] == r.build_stats["rounds"]
+
+
+def test_heap_edmonds_matches_reference_on_community_cascade():
+    if not O.ref_available():
+        pytest.skip("compiled reference absent")
+    a = P.generate_graph("community", [1500, 500, 0.8, 1e-3], 3)
+    ra = O.RefCsr.from_arrays(a.n_rows, a.n_cols, a.row_ptr, a.col_idx)
+    assert _ref_vs_ours(ra, 0, True, threads=8)
