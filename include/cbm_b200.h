@@ -28,7 +28,8 @@ enum {
   CBM_B200_EINVAL = 1,   /* std::invalid_argument in the reference */
   CBM_B200_ECUDA = 2,    /* CUDA runtime / launch failure */
   CBM_B200_ENOMEM = 3,   /* host or device allocation failure */
-  CBM_B200_ELOGIC = 4    /* std::logic_error in the reference (builder) */
+  CBM_B200_ELOGIC = 4,   /* std::logic_error in the reference (builder) */
+  CBM_B200_EFORMAT = 5   /* cbm::format_error (bad or truncated CBM1 container) */
 };
 
 #define CBM_B200_VIRTUAL_PARENT 0xFFFFFFFFu /* kVirtualParent, types.hpp:19 */
@@ -91,6 +92,12 @@ typedef struct cbm_b200_build_stats {
 } cbm_b200_build_stats;
 int cbm_b200_host_stats(const cbm_b200_host_cbm* c, cbm_b200_build_stats* out);
 void cbm_b200_host_free(cbm_b200_host_cbm* c);
+
+/* CBM1 container (io.hpp:44-57): load_cbm (io.cpp:293-382, same validation and
+ * messages; f64 values narrowed to f32 like the f32 build) and save_cbm
+ * (io.cpp:261-291). Files interoperate with the reference in both directions. */
+int cbm_b200_load_cbm1(const char* path, cbm_b200_host_cbm** out);
+int cbm_b200_save_cbm1(const cbm_b200_cbm_view* c, const char* path);
 
 /* count_scalar_ops (kernels.hpp:22, kernels.cpp:66-68). */
 int cbm_b200_count_ops(const cbm_b200_cbm_view* c, uint64_t* multiply_adds,

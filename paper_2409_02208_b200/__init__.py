@@ -30,7 +30,8 @@ import numpy as np
 
 __all__ = [
     "CsrBinaryMatrix", "CbmMatrix", "DeviceCbm", "build_cbm", "build_cbm_normalized",
-    "count_scalar_ops", "generate_graph", "generate_dense", "CbmError", "VIRTUAL_PARENT",
+    "count_scalar_ops", "generate_graph", "generate_dense", "CbmError", "FormatError",
+    "load_cbm", "save_cbm", "VIRTUAL_PARENT",
     "library_path",
 ]
 
@@ -45,7 +46,7 @@ if not os.path.exists(library_path):
 
 _lib = C.CDLL(library_path)
 
-OK, EINVAL, ECUDA, ENOMEM, ELOGIC = 0, 1, 2, 3, 4
+OK, EINVAL, ECUDA, ENOMEM, ELOGIC, EFORMAT = 0, 1, 2, 3, 4, 5
 
 
 class CbmError(RuntimeError):
@@ -99,6 +100,8 @@ _sig = {
     "cbm_b200_host_branches": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_u64)]),
     "cbm_b200_host_stats": (C.c_int, [_vp, C.POINTER(_Stats)]),
     "cbm_b200_host_free": (None, [_vp]),
+    "cbm_b200_load_cbm1": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "cbm_b200_save_cbm1": (C.c_int, [C.POINTER(_CbmView), C.c_char_p]),
     "cbm_b200_count_ops": (C.c_int, [C.POINTER(_CbmView), C.POINTER(_u64), C.POINTER(_u64)]),
     "cbm_b200_default_options": (None, [C.POINTER(_Options)]),
     "cbm_b200_upload": (C.c_int, [C.POINTER(_CbmView), C.POINTER(_Options), C.POINTER(_vp)]),
@@ -122,12 +125,18 @@ for _name, (_res, _args) in _sig.items():
 EXPORTED_SYMBOLS = tuple(_sig)
 
 
+class FormatError(CbmError):
+    """cbm::format_error (io.hpp:19-22): bad or truncated CBM1 container."""
+
+
 def _check(rc: int):
     if rc == OK:
         return
     msg = _lib.cbm_b200_last_error().decode()
     if rc == EINVAL:
         raise ValueError(msg)
+    if rc == EFORMAT:
+        raise FormatError(rc, msg)
     raise CbmError(rc, msg)
 
 
@@ -216,11 +225,7 @@ def _copy(ptr, n, dtype):
     return np.frombuffer(buf, dtype=dtype, count=n).copy()
 
 
-def _build(a: CsrBinaryMatrix, alpha, normalized, degree_mode, threads, algo=0) -> CbmMatrix:
-    h = _vp()
-    view = a._view()
-    _check(_lib.cbm_b200_build_ex(C.byref(view), alpha, int(normalized), degree_mode,
-                                  threads, algo, C.byref(h)))
+def _from_host_handle(h) -> CbmMatrix:
     try:
         v = _CbmView()
         _check(_lib.cbm_b200_host_view(h, C.byref(v)))
@@ -241,6 +246,27 @@ def _build(a: CsrBinaryMatrix, alpha, normalized, degree_mode, threads, algo=0) 
                          "candidate_edges": st.candidate_edges, "rounds": st.rounds})
     finally:
         _lib.cbm_b200_host_free(h)
+
+
+def _build(a: CsrBinaryMatrix, alpha, normalized, degree_mode, threads, algo=0) -> CbmMatrix:
+    h = _vp()
+    view = a._view()
+    _check(_lib.cbm_b200_build_ex(C.byref(view), alpha, int(normalized), degree_mode,
+                                  threads, algo, C.byref(h)))
+    return _from_host_handle(h)
+
+
+def load_cbm(path) -> CbmMatrix:
+    """load_cbm (io.hpp:57): read and fully validate a CBM1 container."""
+    h = _vp()
+    _check(_lib.cbm_b200_load_cbm1(str(path).encode(), C.byref(h)))
+    return _from_host_handle(h)
+
+
+def save_cbm(c: CbmMatrix, path) -> None:
+    """save_cbm (io.hpp:52): write a CBM1 container the reference can load."""
+    v = c._view()
+    _check(_lib.cbm_b200_save_cbm1(C.byref(v), str(path).encode()))
 
 
 _ALGO = {"heap": 0, "rounds": 1}

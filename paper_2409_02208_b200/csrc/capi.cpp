@@ -35,6 +35,9 @@ int guard(F&& f) {
   } catch (const cbmb::logic_error& e) {
     g_err = e.what();
     return CBM_B200_ELOGIC;
+  } catch (const cbmb::format_error& e) {
+    g_err = e.what();
+    return CBM_B200_EFORMAT;
   } catch (const cbmb::cuda_error& e) {
     g_err = e.what();
     return e.code;
@@ -138,6 +141,39 @@ int cbm_b200_host_stats(const cbm_b200_host_cbm* h, cbm_b200_build_stats* s) {
 }
 
 void cbm_b200_host_free(cbm_b200_host_cbm* h) { delete h; }
+
+int cbm_b200_load_cbm1(const char* path, cbm_b200_host_cbm** out) {
+  return guard([&] {
+    need(path && out, "load_cbm1: null argument");
+    *out = nullptr;
+    auto* h = new cbm_b200_host_cbm;
+    try {
+      h->c = cbmb::load_cbm1(path);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int cbm_b200_save_cbm1(const cbm_b200_cbm_view* v, const char* path) {
+  return guard([&] {
+    need(v && path, "save_cbm1: null argument");
+    cbmb::HostCbm c;
+    c.n_rows = v->n_rows;
+    c.n_cols = v->n_cols;
+    c.alpha = v->alpha;
+    c.normalized = v->is_normalized != 0;
+    c.parent.assign(v->parent, v->parent + v->n_rows);
+    cbmb::chain_from_parents(c);  // topo order as the reference stores it
+    c.row_ptr.assign(v->row_ptr, v->row_ptr + size_t(v->n_rows) + 1);
+    c.col_idx.assign(v->col_idx, v->col_idx + v->nnz);
+    c.values.assign(v->values, v->values + v->nnz);
+    if (c.normalized) c.row_scale.assign(v->row_scale, v->row_scale + v->n_rows);
+    cbmb::save_cbm1(c, path);
+  });
+}
 
 int cbm_b200_count_ops(const cbm_b200_cbm_view* c, uint64_t* mult, uint64_t* upd) {
   return guard([&] {

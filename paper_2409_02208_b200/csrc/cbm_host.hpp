@@ -65,6 +65,10 @@ HostCbm build_cbm(const Csr& a, uint64_t alpha, int threads, int algo = 0);
 HostCbm build_cbm_normalized(const Csr& a, uint64_t alpha, int threads,
                              bool degrees_from_original, int algo = 0);
 
+// CBM1 container (io.hpp:44-57, io.cpp:198-382); throws format_error.
+void save_cbm1(const HostCbm& c, const std::string& path);
+HostCbm load_cbm1(const std::string& path);
+
 // ---- internals exposed for tests ------------------------------------------
 
 // Candidate edges in dst-major CSR: for destination row x, entries

@@ -13,6 +13,9 @@ struct invalid_argument : std::invalid_argument {  // std::invalid_argument in t
 struct logic_error : std::logic_error {  // std::logic_error in the reference builder
   using std::logic_error::logic_error;
 };
+struct format_error : std::runtime_error {  // cbm::format_error (io.hpp:19-22)
+  using std::runtime_error::runtime_error;
+};
 struct cuda_error : std::runtime_error {  // CUDA failure, carries a CBM_B200_* code
   int code;
   cuda_error(const std::string& s, int c) : std::runtime_error(s), code(c) {}
