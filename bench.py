@@ -47,6 +47,7 @@ def parse():
                     help="bounded CPU-baseline sample (seconds of reference work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order-faithful", action="store_true")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "register", "scalar"])
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     return ap.parse_args()
 
@@ -212,7 +213,7 @@ def run_ours(args, wl):
     c = wl.build(a, args.threads)
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
-    op = P.DeviceCbm(c, device=local, order_faithful=args.order_faithful)
+    op = P.DeviceCbm(c, device=local, order_faithful=args.order_faithful, kernel=args.kernel)
     torch.cuda.synchronize()
     t_upload = time.perf_counter() - t0
     info = op.info()
@@ -312,7 +313,7 @@ def run_ours(args, wl):
                       "nnz_delta": info["nnz_delta"], "d": wl.d, "d_per_rank": d_local,
                       "alpha": wl.alpha, "normalized": wl.normalized,
                       "parallelism": f"column-shard x{world}",
-                      "order_faithful": bool(args.order_faithful),
+                      "order_faithful": bool(args.order_faithful), "kernel": args.kernel,
                       "l2": "flushed (256 MiB write) before every timed step",
                       "levels": info["n_levels"], "chunk_items": info["n_chunk_items"],
                       "build_s": t_build, "upload_s": t_upload},

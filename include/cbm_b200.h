@@ -157,6 +157,22 @@ int cbm_b200_spmm_host(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64
 int cbm_b200_spmv(cbm_b200_matrix* h, const float* v, int64_t v_rows, int64_t v_cols,
                   float* u, int64_t u_rows, int64_t u_cols, void* stream);
 
+/* C = A B on device memory with the reference's arithmetic (dense_matmul,
+ * dense.hpp:48-50, dense.cpp:31-49): per output entry, ascending inner index,
+ * zero lhs entries skipped, every product rounded before the add (no FMA) —
+ * bit-identical to the reference. A is m x k, B k x n, C m x n, all packed
+ * row-major. */
+int cbm_b200_dense_matmul(const float* a, int64_t m, int64_t k, const float* b, int64_t n,
+                          float* c, void* stream);
+
+/* Two-layer GCN inference out = A_hat relu(A_hat (X W0)) W1 (gcn_forward,
+ * gcn.hpp:27-29, gcn.cpp:22-33) with a normalized uploaded adjacency: the two
+ * GEMMs above, the ReLU fused into the first CBM product's epilogue. X is
+ * n x f, W0 f x hid, W1 hid x classes, out n x classes (device, packed). */
+int cbm_b200_gcn_forward(cbm_b200_matrix* h, const float* x, int64_t n, int64_t f,
+                         const float* w0, int64_t hid, const float* w1, int64_t classes,
+                         float* out, void* stream);
+
 /* Pre-size the per-call workspace for up to d_max columns so later calls
  * never allocate (the device analogue of Property 3, kernels.hpp:36-39). */
 int cbm_b200_reserve(cbm_b200_matrix* h, int64_t d_max);

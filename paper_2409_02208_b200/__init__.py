@@ -31,7 +31,7 @@ import numpy as np
 __all__ = [
     "CsrBinaryMatrix", "CbmMatrix", "DeviceCbm", "build_cbm", "build_cbm_normalized",
     "count_scalar_ops", "generate_graph", "generate_dense", "CbmError", "FormatError",
-    "load_cbm", "save_cbm", "VIRTUAL_PARENT",
+    "load_cbm", "save_cbm", "dense_matmul", "VIRTUAL_PARENT",
     "library_path",
 ]
 
@@ -111,6 +111,8 @@ _sig = {
     "cbm_b200_spmm_host": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp]),
     "cbm_b200_spmv": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp]),
     "cbm_b200_get_info": (C.c_int, [_vp, C.POINTER(_Info)]),
+    "cbm_b200_dense_matmul": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp]),
+    "cbm_b200_gcn_forward": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "cbm_b200_gen_graph": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), _i32, _u64,
                                      C.POINTER(_vp)]),
     "cbm_b200_csr_get": (C.c_int, [_vp, C.POINTER(_CsrView)]),
@@ -321,6 +323,19 @@ def generate_dense(kind: str, rows: int, cols: int, seed: int, lo: float = -1.0,
     return out
 
 
+def dense_matmul(a, b, stream=None):
+    """dense_matmul (dense.hpp:48-50) on CUDA float32 tensors, reference-exact."""
+    torch = _torch()
+    a, b = a.contiguous(), b.contiguous()
+    if a.shape[1] != b.shape[0]:
+        raise ValueError("dense_matmul: inner dimensions differ")
+    c = torch.empty((a.shape[0], b.shape[1]), dtype=torch.float32, device=a.device)
+    s = DeviceCbm._stream(stream)
+    _check(_lib.cbm_b200_dense_matmul(a.data_ptr(), a.shape[0], a.shape[1], b.data_ptr(),
+                                      b.shape[1], c.data_ptr(), s))
+    return c
+
+
 # ---------------------------------------------------------------------------
 # Device operator
 # ---------------------------------------------------------------------------
@@ -342,7 +357,7 @@ class DeviceCbm:
         opt.split_threshold = split_threshold
         opt.chunk = chunk
         opt.prescale = prescale
-        opt.kernel = {"auto": 0, "scalar": 1}[kernel]
+        opt.kernel = {"auto": 0, "scalar": 1, "register": 2}[kernel]
         opt.max_segments = max_segments
         self._h = _vp()
         view = c._view()
@@ -408,6 +423,18 @@ class DeviceCbm:
         _check(_lib.cbm_b200_spmm_host(self._h, x.ctypes.data, x.shape[0], x.shape[1],
                                        y.ctypes.data, y.shape[0], y.shape[1], s))
         return y
+
+    def gcn_forward(self, x, w0, w1, stream=None):
+        """gcn_forward (gcn.cpp:22-33) on CUDA float32 tensors (packed row-major)."""
+        torch = _torch()
+        x, w0, w1 = (t.contiguous() for t in (x, w0, w1))
+        if w0.shape[0] != x.shape[1] or w1.shape[0] != w0.shape[1]:
+            raise ValueError("dense_matmul: inner dimensions differ")
+        out = torch.empty((x.shape[0], w1.shape[1]), dtype=torch.float32, device=x.device)
+        _check(_lib.cbm_b200_gcn_forward(self._h, x.data_ptr(), x.shape[0], x.shape[1],
+                                         w0.data_ptr(), w0.shape[1], w1.data_ptr(), w1.shape[1],
+                                         out.data_ptr(), self._stream(stream)))
+        return out
 
     def spmm_host_ptr(self, x_ptr, x_rows, x_cols, y_ptr, y_rows, y_cols, stream=None):
         _check(_lib.cbm_b200_spmm_host(self._h, x_ptr, x_rows, x_cols, y_ptr, y_rows, y_cols,

@@ -269,6 +269,34 @@ int cbm_b200_spmv(cbm_b200_matrix* h, const float* v, int64_t v_rows, int64_t v_
   });
 }
 
+int cbm_b200_dense_matmul(const float* a, int64_t m, int64_t k, const float* b, int64_t n,
+                          float* c, void* stream) {
+  return guard([&] {
+    need(m >= 0 && k >= 0 && n >= 0 && m < (1ll << 32) && k < (1ll << 32) && n < (1ll << 32),
+         "dense_matmul: bad shape");
+    need((a || m * k == 0) && (b || k * n == 0) && (c || m * n == 0), "dense_matmul: null data");
+    cbmb::device_dense_matmul(a, uint32_t(m), uint32_t(k), b, uint32_t(n), c, stream);
+  });
+}
+
+int cbm_b200_gcn_forward(cbm_b200_matrix* h, const float* x, int64_t n, int64_t f,
+                         const float* w0, int64_t hid, const float* w1, int64_t classes,
+                         float* out, void* stream) {
+  return guard([&] {
+    need(h != nullptr, "gcn_forward: null handle");
+    const auto& L = h->d->info;
+    // gcn.cpp:24-27
+    if (!L.normalized) throw cbmb::invalid_argument("gcn_forward: adjacency must be normalized");
+    if (n != int64_t(L.n_cols))
+      throw cbmb::invalid_argument("gcn_forward: feature rows must match nodes");
+    need(f > 0 && hid > 0 && classes > 0, "gcn_forward: empty weight shape");
+    need(x && w0 && w1 && out, "gcn_forward: null data");
+    std::lock_guard<std::mutex> lk(h->d->mu);
+    cbmb::device_gcn_forward(h->d, x, uint32_t(n), uint32_t(f), w0, uint32_t(hid), w1,
+                             uint32_t(classes), out, stream);
+  });
+}
+
 int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* o) {
   return guard([&] {
     need(h && o, "info: null argument");

@@ -147,6 +147,8 @@ struct Params {
   const uint32_t* __restrict__ wstart;  // per warp: first ticket of its range (total_warps + 1)
   uint32_t n_items, n_chunk, d, dpad;
   uint32_t total_tickets, total_warps, epoch;
+  uint32_t cta_stride;  // CTAs per residency round (grid / CTAs per SM)
+  uint32_t relu;        // fused ReLU on Y (relu_inplace, dense.cpp:51-54) for the GCN
 };
 
 // acc += partial[first], partial[first+1], ... in order. The producers' ready
@@ -192,11 +194,9 @@ __device__ __forceinline__ void add_partials(const Params& p, const uint32_t* fl
 template <int V>
 __device__ __forceinline__ void cp_async(float* dst, const float* src) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-  if constexpr (V == 4)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(V * 4)
-                 : "memory");
+  // .ca: allocate in L1 — adjacent rows of one SM gather the same X rows
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(V * 4)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_f(float* dst, const float* src) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -206,6 +206,14 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// relu_inplace (dense.cpp:51-54): v < 0 -> +0, everything else (-0.0 too) kept
+__device__ __forceinline__ float relu1(float v) { return v < 0.0f ? 0.0f : v; }
+template <int V>
+__device__ __forceinline__ typename Vec<V>::T relu_v(typename Vec<V>::T v) {
+  if constexpr (V == 4) return make_float4(relu1(v.x), relu1(v.y), relu1(v.z), relu1(v.w));
+  else if constexpr (V == 2) return make_float2(relu1(v.x), relu1(v.y));
+  else return relu1(v);
 }
 template <int V>
 __device__ __forceinline__ typename Vec<V>::T lds(const float* p) {
@@ -265,7 +273,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   const int lane = threadIdx.x & 31;
   using SM = WarpSmem<V, U, D, NORM, SCALE>;
   SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
-  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // warp -> position in the round-robin: CTAs b, b+G, b+2G, ... (G = p.cta_stride,
+  // one per SM) share an SM, so consecutive tickets (adjacent rows, similar
+  // delta columns) land on one SM and reuse its L1
+  const uint32_t cta = blockIdx.x, wi = threadIdx.x >> 5;
+  const uint32_t w = (cta % p.cta_stride) * (p.total_warps / p.cta_stride) +
+                     (cta / p.cta_stride) * kWarpsPerCta + wi;
   if (w >= p.total_warps || w >= p.total_tickets) return;
   const uint32_t WW = p.total_warps;
   const uint32_t n_w = (p.total_tickets - w + WW - 1) / WW;  // tickets w, w+W, w+2W, ...
@@ -426,15 +439,257 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       const float sr = sm.srow[k_ci];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (col + uint32_t(u) * kSeg < p.d) W::st(yrow + col + u * kSeg, W::mul(acc[u], sr));
+        if (col + uint32_t(u) * kSeg < p.d) {
+          T4 yv = W::mul(acc[u], sr);
+          if (p.relu) yv = relu_v<V>(yv);
+          W::st(yrow + col + u * kSeg, yv);
+        }
     } else {
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (col + uint32_t(u) * kSeg < p.d) W::st(yrow + col + u * kSeg, acc[u]);
+        if (col + uint32_t(u) * kSeg < p.d) W::st(yrow + col + u * kSeg, p.relu ? relu_v<V>(acc[u]) : acc[u]);
       if (is_parent) publish(flag_base + t, p.epoch);
     }
   }
   cp_wait<0>();  // no copy may target shared memory after exit
+}
+
+// ------------------------------------------------------------ register kernel
+// Same schedule, records and epilogues as cbm_kernel; the X rows are staged in
+// registers instead: deltas are taken in groups of G, the group after the
+// current one (possibly the first group of the warp's next ticket) is loaded
+// while the current one is summed (two register buffers), the delta's sign is
+// applied with one XOR per float (fl(a + (-x)) == fl(a - x)), and column bounds
+// are resolved once per ticket. ~20 instructions per delta and segment.
+template <int V, int U, bool NORM, bool SCALE>
+struct alignas(16) RegSmem {
+  TRec rec[kRecWin];
+  uint32_t item[kRecWin];
+  uint32_t slab[kRecWin];
+  float srow[NORM ? kRecWin : 1];
+};
+
+template <int V>
+__device__ __forceinline__ typename Vec<V>::T xor_sign(typename Vec<V>::T v, uint32_t m) {
+  if constexpr (V == 4) {
+    return make_float4(__int_as_float(__float_as_int(v.x) ^ m), __int_as_float(__float_as_int(v.y) ^ m),
+                       __int_as_float(__float_as_int(v.z) ^ m), __int_as_float(__float_as_int(v.w) ^ m));
+  } else if constexpr (V == 2) {
+    return make_float2(__int_as_float(__float_as_int(v.x) ^ m), __int_as_float(__float_as_int(v.y) ^ m));
+  } else {
+    return __int_as_float(__float_as_int(v) ^ m);
+  }
+}
+
+template <int V, int U, int G, bool NORM, bool SCALE>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_rkernel(const Params p) {
+  using W = Vec<V>;
+  using T4 = typename W::T;
+  constexpr uint32_t kSeg = 32u * V;
+  constexpr uint32_t kSlab = kSeg * U;
+  constexpr int PFp = U >= 4 ? 2 : (U == 2 ? 4 : 8);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  using SM = RegSmem<V, U, NORM, SCALE>;
+  SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
+  const uint32_t cta = blockIdx.x, wi = threadIdx.x >> 5;
+  const uint32_t w = (cta % p.cta_stride) * (p.total_warps / p.cta_stride) +
+                     (cta / p.cta_stride) * kWarpsPerCta + wi;
+  if (w >= p.total_warps || w >= p.total_tickets) return;
+  const uint32_t n_w = (p.total_tickets - w + p.total_warps - 1) / p.total_warps;
+
+  uint32_t g = 0;
+  stage_recs(p, sm, w, 0, n_w, NORM);
+  stage_recs(p, sm, w, 32, n_w, NORM);
+  __syncwarp();
+  auto window = [&](uint32_t i) -> uint32_t {
+    if (i >= n_w || i >= g + kRecWin) return 0u;
+    const TRec& r = sm.rec[i & (kRecWin - 1)];
+    return r.beg + lane < r.end ? __ldg(p.dcol + r.beg + lane) : 0u;
+  };
+  // a ticket as the loader sees it
+  struct Tk {
+    uint32_t beg, len, win;
+    const float* xcol;  // this lane's column base for segment 0
+    uint32_t umask;     // bit u: segment u inside the matrix
+  };
+  auto ticket = [&](uint32_t i, uint32_t win) {
+    Tk t;
+    const TRec& r = sm.rec[i & (kRecWin - 1)];
+    t.beg = r.beg;
+    t.len = i < n_w ? r.end - r.beg : 0u;
+    t.win = win;
+    const uint32_t col = sm.slab[i & (kRecWin - 1)] * kSlab + uint32_t(lane) * V;
+    t.xcol = p.x + col;
+    t.umask = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (col + uint32_t(u) * kSeg < p.d) t.umask |= 1u << u;
+    return t;
+  };
+  // load group q of ticket t into (buf, cw, sc)
+  auto load = [&](T4 (&buf)[G][U], uint32_t (&cw)[G], float (&sc)[G], const Tk& t, uint32_t q) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const uint32_t k = q * G + j;
+      const uint32_t fromw = __shfl_sync(kFull, t.win, k & 31);
+      uint32_t c = 0;
+      if (k < t.len) c = k < 32 ? fromw : __ldg(p.dcol + t.beg + k);
+      cw[j] = c;
+      const float* row = t.xcol + (long long)(c & 0x7FFFFFFFu) * p.ldx;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        buf[j][u] = (k < t.len && (t.umask >> u) & 1u) ? W::ldg(row + u * kSeg) : W::zero();
+      if constexpr (SCALE) sc[j] = k < t.len ? __ldg(p.scale + (c & 0x7FFFFFFFu)) : 0.0f;
+    }
+  };
+  auto consume = [&](const T4 (&buf)[G][U], const uint32_t (&cw)[G], const float (&sc)[G],
+                     uint32_t len, uint32_t q, T4 (&acc)[U]) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if (q * G + j < len) {
+        const uint32_t m = cw[j] & 0x80000000u;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          T4 v = buf[j][u];
+          if constexpr (SCALE) v = W::mul(v, sc[j]);
+          acc[u] = W::add(acc[u], xor_sign<V>(v, m));
+        }
+      }
+    }
+  };
+
+  T4 bufA[G][U], bufB[G][U];
+  uint32_t cwA[G], cwB[G];
+  float scA[G], scB[G];
+  uint32_t wn1 = window(1), wn2 = window(2);
+  Tk cur = ticket(0, window(0));
+  Tk nxt = ticket(1, wn1);
+  load(bufA, cwA, scA, cur, 0);
+  bool in_a = true;  // the group about to be consumed sits in bufA
+#pragma unroll 1
+  for (uint32_t ci = 0; ci < n_w; ++ci) {
+    const uint32_t k_ci = ci & (kRecWin - 1);
+    const TRec r = sm.rec[k_ci];
+    const uint32_t slab = sm.slab[k_ci], t = sm.item[k_ci];
+    const uint32_t col = slab * kSlab + uint32_t(lane) * V;
+    const uint32_t ng = cur.len ? (cur.len + G - 1) / G : 1u;
+    T4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = W::zero();
+#pragma unroll 1
+    for (uint32_t q = 0; q < ng; ++q) {
+      const bool last = q + 1 == ng;
+      if (in_a) {
+        if (!last) load(bufB, cwB, scB, cur, q + 1);
+        else load(bufB, cwB, scB, nxt, 0);
+        consume(bufA, cwA, scA, cur.len, q, acc);
+      } else {
+        if (!last) load(bufA, cwA, scA, cur, q + 1);
+        else load(bufA, cwA, scA, nxt, 0);
+        consume(bufB, cwB, scB, cur.len, q, acc);
+      }
+      in_a = !in_a;
+    }
+    // ---- epilogue (stages 2 + 3) while the next ticket's first group is in flight
+    uint32_t* flag_base = p.flags + (size_t)slab * p.n_items;
+    if (r.cnt) add_partials<V, U, PFp>(p, flag_base, r.first, r.cnt, col, acc);
+    if (t < p.n_chunk) {
+      float* dst = p.partial + (size_t)t * p.dpad;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if ((cur.umask >> u) & 1u) W::st(dst + col + u * kSeg, acc[u]);
+      publish(flag_base + t, p.epoch);
+    } else {
+      if (r.ppos != 0xFFFFFFFFu) {  // + unscaled parent row
+        await(flag_base + r.ppos, p.epoch);
+        const float* src =
+            NORM ? p.interior + (size_t)r.psrc * p.dpad : p.y + (long long)r.psrc * p.ldy;
+        T4 pv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          pv[u] = ((cur.umask >> u) & 1u) ? W::ldcg(src + col + u * kSeg) : W::zero();
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = W::add(acc[u], pv[u]);
+      }
+      const uint32_t row = r.rowk & 0x7FFFFFFFu;
+      const bool is_parent = (r.rowk >> 31) != 0;
+      float* yrow = p.y + (long long)row * p.ldy;
+      if constexpr (NORM) {
+        if (is_parent) {
+          float* dst = p.interior + (size_t)r.slot * p.dpad;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if ((cur.umask >> u) & 1u) W::st(dst + col + u * kSeg, acc[u]);
+          publish(flag_base + t, p.epoch);
+        }
+        const float sr = sm.srow[k_ci];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if ((cur.umask >> u) & 1u) {
+            T4 yv = W::mul(acc[u], sr);
+            if (p.relu) yv = relu_v<V>(yv);
+            W::st(yrow + col + u * kSeg, yv);
+          }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if ((cur.umask >> u) & 1u) W::st(yrow + col + u * kSeg, p.relu ? relu_v<V>(acc[u]) : acc[u]);
+        if (is_parent) publish(flag_base + t, p.epoch);
+      }
+    }
+    // ---- advance: record window, index windows
+    if (ci + 1 - g == 32 && ci + 1 < n_w) {
+      __syncwarp();
+      stage_recs(p, sm, w, g + kRecWin, n_w, NORM);
+      g += 32;
+      __syncwarp();
+    }
+    cur = nxt;
+    wn1 = wn2;
+    wn2 = window(ci + 3);
+    nxt = ticket(ci + 2, wn1);
+  }
+}
+
+template <int V, int U, int G, bool NORM, bool SCALE>
+void launch_reg(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
+  constexpr size_t smem = kWarpsPerCta * sizeof(RegSmem<V, U, NORM, SCALE>);
+  static int bps = -1;
+  if (bps < 0) {
+    ck(cudaFuncSetAttribute(cbm_rkernel<V, U, G, NORM, SCALE>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+       "smem attribute");
+    int b = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_rkernel<V, U, G, NORM, SCALE>,
+                                                     kWarpsPerCta * 32, smem),
+       "occupancy");
+    bps = std::max(1, b);
+  }
+  constexpr uint64_t wpb = kWarpsPerCta;
+  const uint64_t cap = uint64_t(h->num_sms) * bps * wpb;
+  const uint64_t warps = std::max<uint64_t>(1, std::min(cap, tickets));
+  int grid = int((warps + wpb - 1) / wpb);
+  const int per_sm = std::max(1, (grid + h->num_sms - 1) / h->num_sms);
+  p.cta_stride = uint32_t((grid + per_sm - 1) / per_sm);
+  grid = int(p.cta_stride) * per_sm;
+  if (uint64_t(grid) > uint64_t(h->num_sms) * bps) {
+    p.cta_stride = uint32_t(grid / per_sm);
+    grid = int(p.cta_stride) * per_sm;
+  }
+  p.total_warps = uint32_t(grid * wpb);
+  void* args[] = {&p};
+  ck(cudaLaunchCooperativeKernel(
+         reinterpret_cast<const void*>(&cbm_rkernel<V, U, G, NORM, SCALE>), dim3(grid),
+         dim3(kWarpsPerCta * 32), args, smem, s),
+     "cbm_rkernel cooperative launch");
+}
+
+template <int V, int U, int G>
+void run_reg(Params& p, uint64_t tickets, bool norm, bool scl, DeviceMatrix* h, cudaStream_t s) {
+  if (!norm) launch_reg<V, U, G, false, false>(p, tickets, h, s);
+  else if (scl) launch_reg<V, U, G, true, true>(p, tickets, h, s);
+  else launch_reg<V, U, G, true, false>(p, tickets, h, s);
 }
 
 // xs[c, :] = row_scale[c] (*) x[c, :] — the bit-identical products of the
@@ -470,7 +725,15 @@ void launch_one(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
   constexpr uint64_t wpb = kWarpsPerCta;
   const uint64_t cap = uint64_t(h->num_sms) * bps * wpb;
   const uint64_t warps = std::max<uint64_t>(1, std::min(cap, tickets));
-  const int grid = int((warps + wpb - 1) / wpb);
+  int grid = int((warps + wpb - 1) / wpb);
+  // SM-local mapping needs grid = cta_stride * CTAs-per-SM exactly
+  const int per_sm = std::max(1, (grid + h->num_sms - 1) / h->num_sms);
+  p.cta_stride = uint32_t((grid + per_sm - 1) / per_sm);
+  grid = int(p.cta_stride) * per_sm;
+  if (uint64_t(grid) > uint64_t(h->num_sms) * bps) {  // rounding overflowed a wave
+    p.cta_stride = uint32_t(grid / per_sm);
+    grid = int(p.cta_stride) * per_sm;
+  }
   p.total_warps = uint32_t(grid * wpb);
   void* args[] = {&p};
   ck(cudaLaunchCooperativeKernel(
@@ -499,6 +762,94 @@ void grow(T*& ptr, uint64_t& cap, uint64_t need, const char* what) {
 
 }  // namespace
 
+namespace {
+// dense_matmul (dense.cpp:31-49) with the reference's exact arithmetic:
+// c[i,q] = sum over ascending j with a[i,j] != 0 of fl(a[i,j] * b[j,q]),
+// each product rounded before the add, starting from +0. A CTA computes a
+// 32-row x 128-column tile; b is staged through shared memory 32 rows of j at
+// a time; the zero test is warp-uniform (a warp shares its row).
+constexpr int kGemmRows = 32, kGemmCols = 128, kGemmK = 32;
+__global__ void __launch_bounds__(256) ordered_gemm_kernel(const float* __restrict__ a,
+                                                           const float* __restrict__ b,
+                                                           float* __restrict__ c, uint32_t m,
+                                                           uint32_t k, uint32_t n) {
+  __shared__ float bs[kGemmK][kGemmCols];
+  __shared__ float as[kGemmRows][kGemmK + 1];
+  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 lanes x 8 warps
+  const uint32_t row0 = blockIdx.y * kGemmRows, col0 = blockIdx.x * kGemmCols;
+  float acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[r][q] = 0.0f;
+  for (uint32_t j0 = 0; j0 < k; j0 += kGemmK) {
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < kGemmK * kGemmCols; e += 256) {
+      const uint32_t jj = e / kGemmCols, cc = e % kGemmCols;
+      bs[jj][cc] = (j0 + jj < k && col0 + cc < n) ? b[(size_t)(j0 + jj) * n + col0 + cc] : 0.0f;
+    }
+    for (uint32_t e = threadIdx.x; e < kGemmRows * kGemmK; e += 256) {
+      const uint32_t rr = e / kGemmK, jj = e % kGemmK;
+      as[rr][jj] = (row0 + rr < m && j0 + jj < k) ? a[(size_t)(row0 + rr) * k + j0 + jj] : 0.0f;
+    }
+    __syncthreads();
+    const uint32_t jn = min(uint32_t(kGemmK), k - j0);
+    for (uint32_t jj = 0; jj < jn; ++jj) {
+      float bv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bv[q] = bs[jj][tx + 32 * q];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float av = as[ty + 8 * r][jj];
+        if (av != 0.0f) {  // dense.cpp:42 skips zero lhs entries
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[r][q] = __fadd_rn(acc[r][q], __fmul_rn(av, bv[q]));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t i = row0 + ty + 8 * r;
+    if (i >= m) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t cc = col0 + tx + 32 * q;
+      if (cc < n) c[(size_t)i * n + cc] = acc[r][q];
+    }
+  }
+}
+}  // namespace
+
+void device_dense_matmul(const float* a, uint32_t m, uint32_t k, const float* b, uint32_t n,
+                         float* c, void* stream) {
+  if (m == 0 || n == 0) return;
+  const dim3 grid((n + kGemmCols - 1) / kGemmCols, (m + kGemmRows - 1) / kGemmRows);
+  ordered_gemm_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, b, c, m, k, n);
+  ck(cudaGetLastError(), "ordered_gemm launch");
+}
+
+// gcn_forward (gcn.cpp:22-33): X W0 -> A_hat . -> relu -> A_hat . -> . W1, the
+// ReLU fused into the first product's epilogue. Device pointers throughout.
+void device_gcn_forward(DeviceMatrix* h, const float* x, uint32_t n, uint32_t f,
+                        const float* w0, uint32_t hid, const float* w1, uint32_t classes,
+                        float* out, void* stream) {
+  ck(cudaSetDevice(h->device), "cudaSetDevice");
+  const uint32_t hp = (hid + 3) & ~3u;
+  grow(h->gcn_h, h->gcn_h_cap, uint64_t(n) * hp * 2, "gcn workspace");
+  float* h0 = h->gcn_h;
+  float* h1 = h->gcn_h + uint64_t(n) * hp;
+  uint32_t launches = 0;
+  device_dense_matmul(x, n, f, w0, hid, h0, stream);  // packed n x hid
+  ++launches;
+  device_spmm(h, h0, hid, hid, h1, hid, stream, /*relu=*/true);
+  launches += h->last_launches;
+  device_spmm(h, h1, hid, hid, h0, hid, stream, /*relu=*/false);
+  launches += h->last_launches;
+  device_dense_matmul(h0, n, hid, w1, classes, out, stream);
+  h->last_launches = launches + 1;
+}
+
 DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& opt) {
   // validate + plan on the host first: malformed input is EINVAL, never a CUDA error
   Layout L = plan_layout(v, opt.order_faithful != 0, opt.split_threshold, opt.chunk);
@@ -510,6 +861,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
     h->device = dev;
     h->opt = opt;
     ck(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    ck(cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, dev), "attr");
     auto put = [&](auto*& dst, const auto& vec, const char* what) {
       using E = typename std::remove_reference_t<decltype(vec)>::value_type;
       const size_t bytes = std::max<size_t>(vec.size(), 1) * sizeof(E);
@@ -548,6 +900,7 @@ void device_free(DeviceMatrix* h) {
     cudaStreamDestroy(h->s_out);
     for (auto e : h->ev) cudaEventDestroy(e);
   }
+  if (h->gcn_h) cudaFree(h->gcn_h);
   for (void* p : {(void*)h->dcol, (void*)h->rec, (void*)h->srow, (void*)h->scale,
                   (void*)h->flags, (void*)h->partial,
                   (void*)h->interior, (void*)h->xs, (void*)h->xstage, (void*)h->ystage})
@@ -580,7 +933,7 @@ void device_reserve(DeviceMatrix* h, uint64_t d) {
 }
 
 void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
-                 int64_t ldy, void* stream) {
+                 int64_t ldy, void* stream, bool relu) {
   const Layout& L = h->info;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   h->last_launches = 0;
@@ -609,13 +962,15 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   }
   // lanes x V floats per column slab: V = 4 (LDG.128) when rows are 16-byte
   // aligned multiples, else 2 or 1; kernel option 1 forces scalar lanes
-  const uint32_t V = h->opt.kernel == 1 ? 1u : pick_vec(d, xin, ldin, y, ldy);
+  const uint32_t V = h->opt.kernel == 1 ? 1u : pick_vec(d, xin, ldin, y, ldy);  // 2: register kernel
   // segments of 32*V columns per ticket: wide X shares one ticket's record,
-  // indices and epilogue across up to 4 segments
+  // indices and epilogue across up to 4 segments ...
   const uint32_t segs = (d + 32 * V - 1) / (32 * V);
   uint32_t U = segs >= 4 ? 4 : (segs >= 2 ? 2 : 1);
   if (h->opt.max_segments == 1 || h->opt.max_segments == 2)
     U = std::min<uint32_t>(U, uint32_t(h->opt.max_segments));
+  // (narrower slabs that fit X in L2 were measured slower on cfg[2]/cfg[3]:
+  // the extra per-ticket work outweighs the L2 misses they remove)
   const uint32_t n_slabs = (d + 32 * V * U - 1) / (32 * V * U);
   if (++h->epoch == 0) {  // wrapped: re-zero the flags
     ck(cudaMemsetAsync(h->flags, 0, h->flags_cap * sizeof(uint32_t), s), "flags memset");
@@ -641,9 +996,24 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   if (tickets >= 0x7FFFFFFFull) throw invalid_argument("spmm: too many work tickets");
   p.total_tickets = uint32_t(tickets);
   p.epoch = h->epoch;
+  p.relu = relu ? 1u : 0u;
 
   const bool norm = L.normalized, scl = L.normalized && !prescale;
-  if (V == 4) {
+  if (h->opt.kernel == 2) {  // register-staged group pipeline
+    if (V == 4) {
+      if (U == 4) run_reg<4, 4, 2>(p, tickets, norm, scl, h, s);
+      else if (U == 2) run_reg<4, 2, 4>(p, tickets, norm, scl, h, s);
+      else run_reg<4, 1, 8>(p, tickets, norm, scl, h, s);
+    } else if (V == 2) {
+      if (U == 4) run_reg<2, 4, 4>(p, tickets, norm, scl, h, s);
+      else if (U == 2) run_reg<2, 2, 8>(p, tickets, norm, scl, h, s);
+      else run_reg<2, 1, 8>(p, tickets, norm, scl, h, s);
+    } else {
+      if (U == 4) run_reg<1, 4, 8>(p, tickets, norm, scl, h, s);
+      else if (U == 2) run_reg<1, 2, 8>(p, tickets, norm, scl, h, s);
+      else run_reg<1, 1, 8>(p, tickets, norm, scl, h, s);
+    }
+  } else if (V == 4) {
     if (U == 4) run_kernel<4, 4, 4>(p, tickets, norm, scl, h, s);
     else if (U == 2) run_kernel<4, 2, 8>(p, tickets, norm, scl, h, s);
     else run_kernel<4, 1, 8>(p, tickets, norm, scl, h, s);
@@ -695,7 +1065,7 @@ void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, voi
   for (uint32_t k = 0, c0 = 0; c0 < d; ++k, c0 += cw) {
     const uint32_t w = std::min(cw, d - c0);
     ck(cudaStreamWaitEvent(s, h->ev[1 + k], 0), "wait");
-    device_spmm(h, h->xstage + c0, dpad, w, h->ystage + c0, dpad, stream);
+    device_spmm(h, h->xstage + c0, dpad, w, h->ystage + c0, dpad, stream, false);
     launches += h->last_launches;
     ck(cudaEventRecord(h->ev[5 + k], s), "event");
     ck(cudaStreamWaitEvent(h->s_out, h->ev[5 + k], 0), "wait");

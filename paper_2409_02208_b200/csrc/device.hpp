@@ -18,6 +18,7 @@ namespace cbmb {
 struct DeviceMatrix {
   int device = 0;
   int num_sms = 148;
+  int l2_bytes = 126 << 20;
   Layout info;  // sizes only after upload (host vectors released)
   cbm_b200_options opt{};
   // structure (immutable)
@@ -37,6 +38,8 @@ struct DeviceMatrix {
   uint64_t xs_cap = 0;
   float* xstage = nullptr;       // host-API staging
   uint64_t xstage_cap = 0;
+  float* gcn_h = nullptr;        // GCN hidden activations (2 x n x hid)
+  uint64_t gcn_h_cap = 0;
   float* ystage = nullptr;
   uint64_t ystage_cap = 0;
   // host-API pipeline: copy-in / copy-out streams and chunk events
@@ -52,7 +55,12 @@ void device_free(DeviceMatrix* h);
 void device_reserve(DeviceMatrix* h, uint64_t d);
 // Y = A X; x/y are device pointers; d = columns. Shapes already validated.
 void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
-                 int64_t ldy, void* stream);
+                 int64_t ldy, void* stream, bool relu = false);
+void device_dense_matmul(const float* a, uint32_t m, uint32_t k, const float* b, uint32_t n,
+                         float* c, void* stream);
+void device_gcn_forward(DeviceMatrix* h, const float* x, uint32_t n, uint32_t f,
+                        const float* w0, uint32_t hid, const float* w1, uint32_t classes,
+                        float* out, void* stream);
 void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, void* stream);
 
 }  // namespace cbmb

@@ -1,0 +1,65 @@
+"""GCN end to end on the GPU (gcn.cpp:22-33): bit-exact against the
+reference's gcn_forward (f32 build) — ordered GEMM kernel, ReLU fused into the
+first CBM product, both A_hat products through the CBM kernel."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2409_02208_b200 as P
+from helpers import assert_bitwise, golden_cbm, load_golden, oracle_arrays
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+
+
+def test_dense_matmul_matches_reference_arithmetic():
+    rng = np.random.default_rng(3)
+    for m, k, n in ((1, 1, 1), (37, 53, 130), (300, 128, 256), (64, 256, 112)):
+        a = rng.standard_normal((m, k)).astype(np.float32)
+        a[rng.random((m, k)) < 0.2] = 0.0          # zero lhs entries are skipped
+        b = rng.standard_normal((k, n)).astype(np.float32)
+        assert_bitwise(P.dense_matmul(_t(a), _t(b)).cpu().numpy(), O.oracle_dense_matmul(a, b),
+                       f"gemm {m}x{k}x{n}")
+
+
+def test_gcn_golden_fixture_bitwise():
+    g = load_golden("gcn_small")             # reference gcn_forward output
+    c = golden_cbm(g)
+    op = P.DeviceCbm(c, order_faithful=True)
+    out = op.gcn_forward(_t(g["x"]), _t(g["w0"]), _t(g["w1"])).cpu().numpy()
+    assert_bitwise(out, g["y"], "gcn_small")
+
+
+@pytest.mark.parametrize("faithful", [True, False])
+def test_gcn_cfg3_shape_scaled(faithful):
+    """cfg[3] shape (communities of 500, 0.8 / 1e-4), scaled to 6000 nodes,
+    f=128, hidden=256, classes=112, Glorot weights."""
+    a = P.generate_graph("community", [6000, 500, 0.8, 1e-4], 0xC0F60003)
+    c = P.build_cbm_normalized(a, 0, threads=8)
+    x = P.generate_dense("normal", 6000, 128, 0xC0F61003)
+    w0 = P.generate_dense("glorot", 128, 256, 0xC0F62003)
+    w1 = P.generate_dense("glorot", 256, 112, 0xC0F62004)
+    want = O.oracle_gcn_forward(oracle_arrays(c), x, w0, w1)
+    got = P.DeviceCbm(c, order_faithful=faithful).gcn_forward(_t(x), _t(w0), _t(w1)).cpu().numpy()
+    if faithful:
+        assert_bitwise(got, want, "gcn cfg3-shape")
+    else:
+        err = np.abs(got - want).max() / np.abs(want).max()
+        assert err <= 1e-5
+
+
+def test_gcn_errors_mirror_reference():
+    a = P.CsrBinaryMatrix.from_rows(3, [[1], [0, 2], [1]])
+    plain = P.DeviceCbm(P.build_cbm(a, 0))
+    x = torch.zeros((3, 4), device="cuda")
+    w0 = torch.zeros((4, 2), device="cuda")
+    w1 = torch.zeros((2, 2), device="cuda")
+    with pytest.raises(ValueError, match="adjacency must be normalized"):
+        plain.gcn_forward(x, w0, w1)
+    norm = P.DeviceCbm(P.build_cbm_normalized(a, 0))
+    with pytest.raises(ValueError, match="feature rows must match nodes"):
+        norm.gcn_forward(torch.zeros((4, 4), device="cuda"), w0, w1)

@@ -110,7 +110,7 @@ def _suite(normalized, n_cases, seed0):
         yield k, c, x
 
 
-@pytest.mark.parametrize("kernel", ["auto", "scalar"])
+@pytest.mark.parametrize("kernel", ["auto", "scalar", "register"])
 @pytest.mark.parametrize("normalized", [False, True])
 def test_random_suite_bitwise(normalized, kernel, dev):
     """Reference suites (test_kernels.cpp:75-114 style, all d paths, both kernel
@@ -121,8 +121,9 @@ def test_random_suite_bitwise(normalized, kernel, dev):
         assert_bitwise(got, want, f"case {k} d={x.shape[1]}")
 
 
+@pytest.mark.parametrize("kernel", ["auto", "register"])
 @pytest.mark.parametrize("normalized", [False, True])
-def test_split_rows_integer_bitexact_and_gaussian_tolerance(normalized, dev):
+def test_split_rows_integer_bitexact_and_gaussian_tolerance(normalized, kernel, dev):
     """Force every long row through the CHUNK path (split_threshold=4, chunk=2)."""
     rng = np.random.default_rng(77)
     for k in range(12):
@@ -131,7 +132,7 @@ def test_split_rows_integer_bitexact_and_gaussian_tolerance(normalized, dev):
         c = (P.build_cbm_normalized if normalized else P.build_cbm)(a, 0)
         d = int(rng.choice([3, 8, 64, 128, 160]))
         xi = P.generate_dense("int", n, d, 50 + k, -8, 8)
-        got, h = gpu_spmm(c, xi, dev, split_threshold=4, chunk=2)
+        got, h = gpu_spmm(c, xi, dev, split_threshold=4, chunk=2, kernel=kernel)
         if c.nnz:
             assert h.info()["n_chunk_items"] > 0 or np.diff(c.row_ptr).max() <= 4
         want = O.oracle_spmm(oracle_arrays(c), xi)
@@ -140,7 +141,7 @@ def test_split_rows_integer_bitexact_and_gaussian_tolerance(normalized, dev):
         else:
             assert_bitwise(got, want, f"split int case {k}")
         xg = P.generate_dense("normal", n, d, 70 + k)
-        got, _ = gpu_spmm(c, xg, dev, split_threshold=4, chunk=2)
+        got, _ = gpu_spmm(c, xg, dev, split_threshold=4, chunk=2, kernel=kernel)
         assert normwise_err(got, O.oracle_spmm(oracle_arrays(c), xg)) <= TOL
 
 
@@ -202,12 +203,12 @@ def test_cfg0_full_size_integer_bitexact(dev):
     x = P.generate_dense("int", 4096, 64, 0xC0F61000, -8, 8)
     want = O.oracle_spmm(oracle_arrays(c), x)
     for faithful in (True, False):
-        for kernel in ("auto", "scalar"):
+        for kernel in ("auto", "scalar", "register"):
             got, _ = gpu_spmm(c, x, dev, order_faithful=faithful, kernel=kernel)
             assert_bitwise(got, want, f"cfg0 faithful={faithful} kernel={kernel}")
 
 
-@pytest.mark.parametrize("kernel", ["auto", "scalar"])
+@pytest.mark.parametrize("kernel", ["auto", "scalar", "register"])
 def test_cfg1_full_size_gaussian(kernel, dev):
     """cfg[1]: n=19,717 normalized, X N(0,1), d=512: order-faithful is
     bit-exact, the default split mode within 1e-5 normwise."""
