@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order-faithful", action="store_true")
     ap.add_argument("--kernel", default="auto", choices=["auto", "register", "scalar"])
+    ap.add_argument("--no-csr-comparator", action="store_true",
+                    help="skip timing the uncompressed (CSR) matrix with the same kernel")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     return ap.parse_args()
 
@@ -301,6 +303,33 @@ def run_ours(args, wl):
                 "b_alg_bytes": b_alg_local, "kernel": "cbm_fused_kernel",
                 "peak_source": peak_src}
 
+    gpu_csr = None
+    if not args.no_csr_comparator:
+        # same kernel on the uncompressed matrix: the paper's runtime reduction
+        # (t_csr - t_cbm) / t_csr, both on this B200
+        csr_op = P.DeviceCbm(P.csr_operator(a, wl.normalized), device=local)
+        csr_op.reserve(max(1, d_local))
+        if d_local:
+            for _ in range(3):
+                csr_op.spmm_into(x, y, stream)
+        torch.cuda.synchronize()
+        t_csr = []
+        for i in range(min(args.steps, 50)):
+            flush.fill_(float(i))
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if d_local:
+                csr_op.spmm_into(x, y, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t_csr.append(e0.elapsed_time(e1))
+        csr_ms = float(statistics.mean(t_csr))
+        gpu_csr = {"ms_per_step": csr_ms, "value": flops / (csr_ms * 1e-3) / 1e9,
+                   "runtime_reduction_pct": (csr_ms - ms) / csr_ms * 100.0,
+                   "note": "uncompressed matrix through the same kernel (every parent virtual)"}
+        del csr_op
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, wl, c, nnz)
@@ -319,6 +348,7 @@ def run_ours(args, wl):
                       "build_s": t_build, "upload_s": t_upload},
            "roofline": roofline,
            "cpu_baseline": cpu,
+           "gpu_csr_comparator": gpu_csr,
            "e2e": {"value": e2e_value, "unit": UNIT,
                    "h2d_bytes_per_step": int(a.n_cols * d_local * 4),
                    "d2h_bytes_per_step": int(a.n_rows * d_local * 4),

@@ -126,6 +126,11 @@ typedef struct cbm_b200_options {
                                 1 force scalar lanes (one float per lane) */
   int32_t max_segments;      /* column segments (32 lanes x V floats) per work
                                 ticket: 0 auto (up to 4), 1 or 2 to cap */
+  int32_t flatten_gain;      /* default mode only: a row whose CBM delta row
+                                saves fewer than this many entries over its full
+                                row is summed directly (no wait on its parent;
+                                same value, CSR summation order). -1 = auto (16),
+                                0 = keep every chain link */
 } cbm_b200_options;
 
 void cbm_b200_default_options(cbm_b200_options* opt);
@@ -179,7 +184,9 @@ int cbm_b200_reserve(cbm_b200_matrix* h, int64_t d_max);
 
 typedef struct cbm_b200_info {
   uint32_t n_rows, n_cols;
-  uint64_t nnz_delta;        /* delta entries (after layout) */
+  uint64_t nnz_delta;        /* delta entries of the uploaded CBM */
+  uint64_t nnz_effective;    /* entries the kernel sums (after flattening) */
+  uint32_t n_flattened;      /* rows summed directly instead of via their parent */
   uint32_t n_levels;         /* depth of the compression forest */
   uint32_t n_roots;
   uint32_t n_interior;       /* rows with at least one child */

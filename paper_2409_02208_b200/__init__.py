@@ -31,7 +31,7 @@ import numpy as np
 __all__ = [
     "CsrBinaryMatrix", "CbmMatrix", "DeviceCbm", "build_cbm", "build_cbm_normalized",
     "count_scalar_ops", "generate_graph", "generate_dense", "CbmError", "FormatError",
-    "load_cbm", "save_cbm", "dense_matmul", "VIRTUAL_PARENT",
+    "load_cbm", "save_cbm", "dense_matmul", "csr_operator", "VIRTUAL_PARENT",
     "library_path",
 ]
 
@@ -72,11 +72,13 @@ class _CbmView(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("order_faithful", C.c_int32),
                 ("split_threshold", C.c_uint32), ("chunk", C.c_uint32), ("prescale", C.c_int32),
-                ("kernel", C.c_int32), ("max_segments", C.c_int32)]
+                ("kernel", C.c_int32), ("max_segments", C.c_int32),
+                ("flatten_gain", C.c_int32)]
 
 
 class _Info(C.Structure):
     _fields_ = [("n_rows", C.c_uint32), ("n_cols", C.c_uint32), ("nnz_delta", C.c_uint64),
+                ("nnz_effective", C.c_uint64), ("n_flattened", C.c_uint32),
                 ("n_levels", C.c_uint32), ("n_roots", C.c_uint32), ("n_interior", C.c_uint32),
                 ("n_items", C.c_uint32), ("n_chunk_items", C.c_uint32),
                 ("max_row_deltas", C.c_uint32), ("device_bytes", C.c_uint64),
@@ -287,6 +289,34 @@ def build_cbm_normalized(a: CsrBinaryMatrix, alpha: int = 0, threads: int = 1,
     return _build(a, alpha, True, mode, threads, _ALGO[arborescence])
 
 
+def csr_operator(a: CsrBinaryMatrix, normalized: bool = False) -> CbmMatrix:
+    """The UNCOMPRESSED matrix in CBM form (every parent virtual, one +1 delta
+    per nonzero; normalized: the pattern of A + I with column and row scales),
+    for timing the GPU CSR SpMM comparator with the same kernel (the paper's
+    runtime-reduction metric; csr_spmm_into, kernels.cpp:152)."""
+    rp, ci = a.row_ptr, a.col_idx
+    scale = None
+    if normalized:
+        if a.n_rows != a.n_cols:
+            raise ValueError("normalized_adjacency_csr: matrix must be square")
+        rows = []
+        for x in range(a.n_rows):
+            r = ci[rp[x]:rp[x + 1]]
+            if not np.any(r == x):
+                r = np.sort(np.append(r, np.uint32(x)))
+            rows.append(r)
+        lens = np.array([len(r) for r in rows], np.uint64)
+        rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+        ci = np.concatenate(rows).astype(np.uint32) if rows else np.zeros(0, np.uint32)
+        deg = np.diff(rp).astype(np.float64)
+        scale = (np.float32(1.0) / np.sqrt(deg).astype(np.float32)).astype(np.float32)
+        vals = scale[ci]
+    else:
+        vals = np.ones(ci.size, np.float32)
+    return CbmMatrix(a.n_rows, a.n_cols, 0, normalized,
+                     np.full(a.n_rows, VIRTUAL_PARENT, np.uint32), rp, ci, vals, scale)
+
+
 def count_scalar_ops(c: CbmMatrix) -> tuple[int, int]:
     """count_scalar_ops (kernels.cpp:66-68): (multiply_adds, update_adds)."""
     a, b = _u64(), _u64()
@@ -349,7 +379,7 @@ class DeviceCbm:
 
     def __init__(self, c: CbmMatrix, device: int | None = None, order_faithful: bool = False,
                  split_threshold: int = 0, chunk: int = 0, prescale: int = -1,
-                 kernel: str = "auto", max_segments: int = 0):
+                 kernel: str = "auto", max_segments: int = 0, flatten_gain: int = -1):
         opt = _Options()
         _lib.cbm_b200_default_options(C.byref(opt))
         opt.device = -1 if device is None else int(device)
@@ -359,6 +389,7 @@ class DeviceCbm:
         opt.prescale = prescale
         opt.kernel = {"auto": 0, "scalar": 1, "register": 2}[kernel]
         opt.max_segments = max_segments
+        opt.flatten_gain = flatten_gain
         self._h = _vp()
         view = c._view()
         _check(_lib.cbm_b200_upload(C.byref(view), C.byref(opt), C.byref(self._h)))

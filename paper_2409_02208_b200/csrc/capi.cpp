@@ -195,6 +195,7 @@ void cbm_b200_default_options(cbm_b200_options* o) {
   o->prescale = -1;
   o->kernel = 0;
   o->max_segments = 0;
+  o->flatten_gain = -1;
 }
 
 int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
@@ -304,6 +305,8 @@ int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* o) {
     o->n_rows = L.n_rows;
     o->n_cols = L.n_cols;
     o->nnz_delta = L.nnz;
+    o->nnz_effective = L.nnz_effective;
+    o->n_flattened = L.n_flattened;
     o->n_levels = L.n_levels;
     o->n_roots = L.n_roots;
     o->n_interior = L.n_interior;

@@ -852,7 +852,8 @@ void device_gcn_forward(DeviceMatrix* h, const float* x, uint32_t n, uint32_t f,
 
 DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& opt) {
   // validate + plan on the host first: malformed input is EINVAL, never a CUDA error
-  Layout L = plan_layout(v, opt.order_faithful != 0, opt.split_threshold, opt.chunk);
+  const uint32_t gain = opt.flatten_gain < 0 ? 16u : uint32_t(opt.flatten_gain);
+  Layout L = plan_layout(v, opt.order_faithful != 0, opt.split_threshold, opt.chunk, gain);
   auto* h = new DeviceMatrix;
   try {
     int dev = opt.device;
@@ -946,7 +947,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     if (h->opt.prescale > 0) prescale = true;
     // auto: the per-delta FMUL costs nnz*d ALU ops; pre-scaling costs an
     // extra 8*n*d bytes of HBM traffic (prescale).
-    else if (h->opt.prescale < 0) prescale = L.nnz > 48ull * L.n_cols;
+    else if (h->opt.prescale < 0) prescale = L.nnz_effective > 48ull * L.n_cols;
   }
   const float* xin = x;
   int64_t ldin = ldx;

@@ -10,7 +10,7 @@
 namespace cbmb {
 
 Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t split_threshold,
-                   uint32_t chunk) {
+                   uint32_t chunk, uint32_t flatten_gain) {
   const uint32_t m = v.n_rows;
   Layout L;
   L.n_rows = m;
@@ -86,6 +86,121 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   }
   if (bfs.size() != m) throw invalid_argument("chain: parent links contain a cycle");
 
+  // ---- effective structure: optionally flatten rows whose parent saves little
+  // A row x with full row a_x and delta row D_x costs |D_x| gathers plus a wait
+  // on its parent and a parent-row read under the CBM; summed directly it costs
+  // |a_x| gathers and no wait. Rows with |a_x| - |D_x| < flatten_gain are
+  // summed directly (default mode only: the row VALUE is unchanged, children
+  // still read it, only its summation order changes). order_faithful keeps
+  // the reference's chain exactly.
+  std::vector<uint32_t> eparent(v.parent, v.parent + m);
+  std::vector<uint64_t> eptr(size_t(m) + 1, 0);
+  std::vector<uint32_t> ecol;
+  {
+    std::vector<uint8_t> flat(m, 0);
+    uint64_t n_flat = 0;
+    if (!order_faithful && flatten_gain > 0) {
+      std::vector<uint64_t> nA(m, 0);
+      for (uint32_t x : bfs) {
+        uint64_t plus = 0, minus = 0;
+        for (uint64_t k = v.row_ptr[x]; k < v.row_ptr[x + 1]; ++k)
+          (v.values[k] < 0.0f ? minus : plus) += 1;
+        const uint32_t p = v.parent[x];
+        nA[x] = p == kVirtual ? plus : nA[p] + plus - minus;
+        const uint64_t dl = plus + minus;
+        if (p != kVirtual && nA[x] < dl + flatten_gain) {
+          flat[x] = 1;
+          ++n_flat;
+        }
+      }
+    }
+    L.n_flattened = uint32_t(n_flat);
+    std::vector<uint64_t> fptr;  // full rows (only when something is flattened)
+    std::vector<uint32_t> fcol;
+    if (n_flat) {
+      // rows from the chain, parents first (reconstruct_rows, builder.cpp:452-490)
+      std::vector<uint64_t> len(m, 0);
+      fptr.assign(m, 0);
+      uint64_t total = 0;
+      for (uint32_t x : bfs) {
+        uint64_t plus = 0, minus = 0;
+        for (uint64_t k = v.row_ptr[x]; k < v.row_ptr[x + 1]; ++k)
+          (v.values[k] < 0.0f ? minus : plus) += 1;
+        const uint32_t p = v.parent[x];
+        len[x] = p == kVirtual ? plus : len[p] + plus - minus;
+        fptr[x] = total;
+        total += len[x];
+      }
+      fcol.resize(total);
+      for (uint32_t x : bfs) {
+        uint32_t* out = fcol.data() + fptr[x];
+        const uint32_t p = v.parent[x];
+        uint64_t k = v.row_ptr[x];
+        const uint64_t ke = v.row_ptr[x + 1];
+        if (p == kVirtual) {
+          for (; k < ke; ++k) *out++ = v.col_idx[k];
+          continue;
+        }
+        const uint32_t* pr = fcol.data() + fptr[p];
+        const uint32_t* pe = pr + len[p];
+        while (pr < pe || k < ke) {  // (parent + plus) - minus, ascending
+          if (k == ke || (pr < pe && *pr < v.col_idx[k])) {
+            *out++ = *pr++;
+          } else if (pr == pe || v.col_idx[k] < *pr) {
+            if (v.values[k] > 0.0f) *out++ = v.col_idx[k];
+            ++k;
+          } else {
+            if (v.values[k] > 0.0f) *out++ = *pr;
+            ++pr;
+            ++k;
+          }
+        }
+      }
+      for (uint32_t x = 0; x < m; ++x)
+        if (flat[x]) eparent[x] = kVirtual;
+      for (uint32_t x = 0; x < m; ++x)
+        eptr[x + 1] = eptr[x] + (flat[x] ? len[x] : v.row_ptr[x + 1] - v.row_ptr[x]);
+    } else {
+      for (uint32_t x = 0; x < m; ++x) eptr[x + 1] = v.row_ptr[x + 1];
+    }
+    ecol.resize(eptr[m]);
+    for (uint32_t x = 0; x < m; ++x) {
+      uint32_t* out = ecol.data() + eptr[x];
+      if (n_flat && flat[x]) {
+        const uint32_t* fr = fcol.data() + fptr[x];
+        for (uint64_t j = 0; j < eptr[x + 1] - eptr[x]; ++j) *out++ = fr[j];
+      } else {
+        for (uint64_t k = v.row_ptr[x]; k < v.row_ptr[x + 1]; ++k)
+          *out++ = v.col_idx[k] | (v.values[k] < 0.0f ? kSignBit : 0u);
+      }
+    }
+    if (n_flat) {  // depths under the effective forest
+      std::fill(depth.begin(), depth.end(), kNoItem);
+      std::vector<uint64_t> kp(size_t(m) + 1, 0);
+      for (uint32_t x = 0; x < m; ++x)
+        if (eparent[x] != kVirtual) ++kp[eparent[x] + 1];
+      std::partial_sum(kp.begin(), kp.end(), kp.begin());
+      std::vector<uint32_t> ks(kp.back());
+      std::vector<uint64_t> cur(kp.begin(), kp.end() - 1);
+      for (uint32_t x = 0; x < m; ++x)
+        if (eparent[x] != kVirtual) ks[cur[eparent[x]]++] = x;
+      bfs.clear();
+      for (uint32_t x = 0; x < m; ++x)
+        if (eparent[x] == kVirtual) {
+          depth[x] = 0;
+          bfs.push_back(x);
+        }
+      for (size_t h = 0; h < bfs.size(); ++h) {
+        const uint32_t u = bfs[h];
+        for (uint64_t k = kp[u]; k < kp[u + 1]; ++k) {
+          depth[ks[k]] = depth[u] + 1;
+          bfs.push_back(ks[k]);
+        }
+      }
+    }
+  }
+  L.nnz_effective = eptr[m];
+
   // ROW items: by depth, ascending row id inside a level (stable counting sort)
   uint32_t max_depth = 0;
   for (uint32_t x = 0; x < m; ++x) max_depth = std::max(max_depth, depth[x]);
@@ -108,7 +223,7 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   if (!order_faithful) {
     for (uint32_t i = 0; i < m; ++i) {
       const uint32_t r = rows[i];
-      const uint64_t len = v.row_ptr[r + 1] - v.row_ptr[r];
+      const uint64_t len = eptr[r + 1] - eptr[r];
       if (len <= split_threshold) continue;
       pieces[i] = uint32_t((len + chunk - 1) / chunk);
       n_leaf += pieces[i] - 1;
@@ -154,12 +269,12 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   for (uint32_t i = 0; i < m; ++i) item_of_row[rows[i]] = L.n_chunk_items + i;
   std::vector<uint8_t> interior(m, 0);
   for (uint32_t x = 0; x < m; ++x)
-    if (v.parent[x] != kVirtual) interior[v.parent[x]] = 1;
+    if (eparent[x] != kVirtual) interior[eparent[x]] = 1;
   std::vector<uint32_t> slot(m, kNoItem);
   for (uint32_t i = 0; i < m; ++i)
     if (interior[rows[i]]) slot[rows[i]] = L.n_interior++;
 
-  L.dcol.resize(nnz);
+  L.dcol.resize(eptr[m]);
   L.rec.assign(size_t(L.n_items) * 8, 0);
   if (L.normalized) L.srow.assign(L.n_items, 0.0f);
   auto R = [&](uint32_t t) { return &L.rec[size_t(t) * 8]; };
@@ -171,7 +286,7 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   }
   for (uint32_t i = 0; i < m; ++i) {
     const uint32_t r = rows[i];
-    const uint64_t lo = v.row_ptr[r], hi = v.row_ptr[r + 1];
+    const uint64_t lo = eptr[r], hi = eptr[r + 1];
     const uint32_t t_row = L.n_chunk_items + i;
     if (pieces[i] < 2) {
       own_lo[t_row] = lo;
@@ -204,7 +319,7 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   for (uint32_t t = 0; t < L.n_items; ++t) {
     R(t)[0] = uint32_t(o);
     for (uint64_t k = own_lo[t]; k < own_hi[t]; ++k)
-      L.dcol[o++] = v.col_idx[k] | (v.values[k] < 0.0f ? kSignBit : 0u);
+      L.dcol[o++] = ecol[k];
     R(t)[1] = uint32_t(o);
   }
   L.item_beg.resize(size_t(L.n_items) + 1);
@@ -213,7 +328,7 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   for (uint32_t i = 0; i < m; ++i) {  // ROW items
     const uint32_t r = rows[i];
     const uint32_t t = L.n_chunk_items + i;
-    const uint32_t p = v.parent[r];
+    const uint32_t p = eparent[r];
     R(t)[2] = r | (interior[r] ? kInteriorBit : 0u);
     R(t)[3] = p == kVirtual ? kNoItem : item_of_row[p];
     R(t)[4] = p == kVirtual ? 0u : (L.normalized ? slot[p] : p);

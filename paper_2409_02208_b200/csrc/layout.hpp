@@ -39,7 +39,9 @@ struct Layout {
   uint32_t n_merge_items = 0;
   uint32_t n_interior = 0;     // rows with children (scratch slots, normalized)
   uint32_t n_levels = 0, n_roots = 0, max_row_deltas = 0;
-  uint64_t nnz = 0;
+  uint64_t nnz = 0;            // deltas of the uploaded CBM
+  uint64_t nnz_effective = 0;  // deltas after flattening (what the kernel sums)
+  uint32_t n_flattened = 0;    // rows summed directly instead of via their parent
   std::vector<uint32_t> dcol;   // column | sign << 31, in item order
   // rec, 8 x u32 per item (two uint4 loads on the device):
   //   [0] beg, [1] end   : the item owns dcol[beg, end)
@@ -60,6 +62,6 @@ struct Layout {
 // Validates the view like load_cbm (io.cpp:346-380) and builds the layout.
 // Throws cbmb::invalid_argument with a reference-style message.
 Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t split_threshold,
-                   uint32_t chunk);
+                   uint32_t chunk, uint32_t flatten_gain);
 
 }  // namespace cbmb

@@ -45,13 +45,14 @@ def test_golden_fixture_bitwise(name, faithful, dev):
         d = P.DeviceCbm(c, order_faithful=faithful)
         v = torch.from_numpy(g["x"]).to(dev)
         got = d.spmv(v).cpu().numpy()
-        split = d.info()["n_chunk_items"] > 0
+        info = d.info()
     else:
         got, d = gpu_spmm(c, g["x"], dev, order_faithful=faithful)
-        split = d.info()["n_chunk_items"] > 0
+        info = d.info()
+    split = info["n_chunk_items"] > 0 or info["n_flattened"] > 0
     integer = np.array_equal(g["x"], np.round(g["x"]))
     if split and not (integer and not c.is_normalized):
-        # chunked long rows change the summation order: tolerance, not bits
+        # chunked / flattened rows change the summation order: tolerance, not bits
         assert normwise_err(got, g["y"]) <= TOL, name
     else:
         assert_bitwise(got, g["y"], name)
@@ -113,12 +114,37 @@ def _suite(normalized, n_cases, seed0):
 @pytest.mark.parametrize("kernel", ["auto", "scalar", "register"])
 @pytest.mark.parametrize("normalized", [False, True])
 def test_random_suite_bitwise(normalized, kernel, dev):
-    """Reference suites (test_kernels.cpp:75-114 style, all d paths, both kernel
-    families): rows are short, nothing is split, so results are bit-identical."""
+    """Reference suites (test_kernels.cpp:75-114 style, all d paths, all kernel
+    families): order-faithful is bit-identical; the default mode is
+    bit-identical unless it flattened/chunked a row, then within tolerance."""
     for k, c, x in _suite(normalized, 60, 9000 + 100 * normalized):
         want = O.oracle_spmm(oracle_arrays(c), x)
-        got, _ = gpu_spmm(c, x, dev, kernel=kernel)
+        got, _ = gpu_spmm(c, x, dev, kernel=kernel, order_faithful=True)
         assert_bitwise(got, want, f"case {k} d={x.shape[1]}")
+        got, h = gpu_spmm(c, x, dev, kernel=kernel)
+        info = h.info()
+        if info["n_flattened"] or info["n_chunk_items"]:
+            assert normwise_err(got, want) <= TOL, f"case {k}"
+        else:
+            assert_bitwise(got, want, f"default case {k}")
+
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_flattened_rows(normalized, dev):
+    """Rows summed directly instead of through their parent (flatten_gain):
+    integer X stays bit-exact for the binary matrix, Gaussian X within 1e-5."""
+    a = P.generate_graph("community", [3000, 100, 0.3, 0.002], 23)
+    c = (P.build_cbm_normalized if normalized else P.build_cbm)(a, 0, threads=8)
+    for gain in (4, 1000):
+        for kind in ("int", "normal"):
+            x = P.generate_dense(kind, 3000, 128, 24, -8, 8)
+            got, h = gpu_spmm(c, x, dev, flatten_gain=gain)
+            assert h.info()["n_flattened"] > 0
+            want = O.oracle_spmm(oracle_arrays(c), x)
+            if kind == "int" and not normalized:
+                assert_bitwise(got, want, f"flatten gain={gain}")
+            else:
+                assert normwise_err(got, want) <= TOL
 
 
 @pytest.mark.parametrize("kernel", ["auto", "register"])
@@ -232,3 +258,20 @@ def test_deep_merge_trees(dev):
     info = h.info()
     assert info["n_chunk_items"] > 1000 and info["max_row_deltas"] > 2000
     assert_bitwise(got, O.oracle_spmm(oracle_arrays(c), x), "deep merge")
+
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_csr_comparator_operator(normalized, dev):
+    """The uncompressed comparator computes the same product (csr_spmm_into,
+    kernels.cpp:152): bit-exact for the binary matrix, within tolerance for
+    the normalized one (scales applied per column / per row, not fused)."""
+    a = P.generate_graph("pa_triangle", [3000, 2, 0.3], 17)
+    x = P.generate_dense("normal", 3000, 64, 18)
+    got, _ = gpu_spmm(P.csr_operator(a, normalized), x, dev, order_faithful=True)
+    c = (P.build_cbm_normalized if normalized else P.build_cbm)(a, 0)
+    want = O.oracle_spmm(oracle_arrays(c), x)
+    if normalized:
+        assert normwise_err(got, want) <= TOL
+    else:
+        vals = np.ones(a.nnz, np.float32)
+        assert_bitwise(got, O.oracle_csr_spmm(a.row_ptr, a.col_idx, vals, x), "csr")

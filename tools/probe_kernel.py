@@ -37,13 +37,12 @@ for name in sys.argv[1].split(","):
         for vn, cc in variants.items():
             if only and vn != only:
                 continue
-            for faithful, kern, segs in ((False, "auto", 0), (False, "register", 0),
-                                         (True, "auto", 0), (True, "register", 0)):
+            for faithful, kern, segs in ((False, "auto", 0), (False, "auto", 4), (False, "auto", 16),
+                                         (False, "auto", 32), (False, "auto", 1 << 30)):
                 if vn != "default" and (faithful or segs):
                     continue
-                if segs and d <= 128:
-                    continue
-                op = P.DeviceCbm(cc, order_faithful=faithful, kernel=kern, max_segments=segs)
+                op = P.DeviceCbm(cc, order_faithful=faithful, kernel=kern,
+                                 flatten_gain=segs if segs else -1)
                 med_f, min_f = timeit(op, x, y, flush)
                 med, mn = timeit(op, x, y, None)
-                print(f"{name} d={d} {vn:8s} faithful={int(faithful)} {kern:8s} flush med {med_f:8.1f}us  noflush med {med:8.1f}us min {mn:8.1f}us  info={ {k: op.info()[k] for k in ('n_levels','n_items','launches_per_call')} }", flush=True)
+                print(f"{name} d={d} {vn:8s} gain={segs} flush med {med_f:8.1f}us  noflush med {med:8.1f}us min {mn:8.1f}us  info={ {k: op.info()[k] for k in ('n_levels','n_items','launches_per_call')} }", flush=True)
