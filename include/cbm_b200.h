@@ -131,6 +131,9 @@ typedef struct cbm_b200_options {
                                 row is summed directly (no wait on its parent;
                                 same value, CSR summation order). -1 = auto (16),
                                 0 = keep every chain link */
+  int32_t prefetch;          /* 1: bulk-prefetch a contiguous X that fits in
+                                half of L2 before gathering; 0 (default): off
+                                (measured neutral on cfg[0]/cfg[1]) */
 } cbm_b200_options;
 
 void cbm_b200_default_options(cbm_b200_options* opt);

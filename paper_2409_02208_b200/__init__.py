@@ -73,7 +73,7 @@ class _Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("order_faithful", C.c_int32),
                 ("split_threshold", C.c_uint32), ("chunk", C.c_uint32), ("prescale", C.c_int32),
                 ("kernel", C.c_int32), ("max_segments", C.c_int32),
-                ("flatten_gain", C.c_int32)]
+                ("flatten_gain", C.c_int32), ("prefetch", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -379,7 +379,8 @@ class DeviceCbm:
 
     def __init__(self, c: CbmMatrix, device: int | None = None, order_faithful: bool = False,
                  split_threshold: int = 0, chunk: int = 0, prescale: int = -1,
-                 kernel: str = "auto", max_segments: int = 0, flatten_gain: int = -1):
+                 kernel: str = "auto", max_segments: int = 0, flatten_gain: int = -1,
+                 prefetch: bool = False):
         opt = _Options()
         _lib.cbm_b200_default_options(C.byref(opt))
         opt.device = -1 if device is None else int(device)
@@ -390,6 +391,7 @@ class DeviceCbm:
         opt.kernel = {"auto": 0, "scalar": 1, "register": 2}[kernel]
         opt.max_segments = max_segments
         opt.flatten_gain = flatten_gain
+        opt.prefetch = int(prefetch)
         self._h = _vp()
         view = c._view()
         _check(_lib.cbm_b200_upload(C.byref(view), C.byref(opt), C.byref(self._h)))

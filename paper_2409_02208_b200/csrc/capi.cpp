@@ -196,6 +196,7 @@ void cbm_b200_default_options(cbm_b200_options* o) {
   o->kernel = 0;
   o->max_segments = 0;
   o->flatten_gain = -1;
+  o->prefetch = 0;
 }
 
 int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,

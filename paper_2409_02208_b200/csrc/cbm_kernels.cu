@@ -149,7 +149,24 @@ struct Params {
   uint32_t total_tickets, total_warps, epoch;
   uint32_t cta_stride;  // CTAs per residency round (grid / CTAs per SM)
   uint32_t relu;        // fused ReLU on Y (relu_inplace, dense.cpp:51-54) for the GCN
+  uint64_t prefetch_bytes;  // > 0: X is one contiguous block of this size, pulled into L2 first
 };
+
+// Every warp streams its share of a contiguous X into L2 with bulk prefetches
+// (sequential HBM reads at full bandwidth instead of first-touch random misses
+// on the gather path). Used when X fits comfortably in L2.
+__device__ __forceinline__ void prefetch_x(const Params& p, uint32_t w) {
+  if (p.prefetch_bytes == 0 || (threadIdx.x & 31) != 0) return;
+  const uint64_t share = ((p.prefetch_bytes + p.total_warps - 1) / p.total_warps + 15) & ~15ull;
+  const uint64_t lo = share * w;
+  if (lo >= p.prefetch_bytes) return;
+  const uint64_t hi = lo + share < p.prefetch_bytes ? lo + share : p.prefetch_bytes;
+  const char* base = reinterpret_cast<const char*>(p.x);
+  for (uint64_t o = lo; o < hi; o += 32768) {
+    const uint32_t n = uint32_t((hi - o < 32768 ? hi - o : 32768) & ~15ull);
+    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"(n) : "memory");
+  }
+}
 
 // acc += partial[first], partial[first+1], ... in order. The producers' ready
 // flags are checked 32 at a time (one lane each), then the partial rows are
@@ -222,6 +239,18 @@ __device__ __forceinline__ typename Vec<V>::T lds(const float* p) {
   else return *p;
 }
 
+template <int V>
+__device__ __forceinline__ typename Vec<V>::T xor_sign(typename Vec<V>::T v, uint32_t m) {
+  if constexpr (V == 4) {
+    return make_float4(__int_as_float(__float_as_int(v.x) ^ m), __int_as_float(__float_as_int(v.y) ^ m),
+                       __int_as_float(__float_as_int(v.z) ^ m), __int_as_float(__float_as_int(v.w) ^ m));
+  } else if constexpr (V == 2) {
+    return make_float2(__int_as_float(__float_as_int(v.x) ^ m), __int_as_float(__float_as_int(v.y) ^ m));
+  } else {
+    return __int_as_float(__float_as_int(v) ^ m);
+  }
+}
+
 constexpr int kWarpsPerCta = 4;
 constexpr uint32_t kRecWin = 64;  // ticket records staged per warp (two groups of 32)
 
@@ -279,7 +308,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   const uint32_t cta = blockIdx.x, wi = threadIdx.x >> 5;
   const uint32_t w = (cta % p.cta_stride) * (p.total_warps / p.cta_stride) +
                      (cta / p.cta_stride) * kWarpsPerCta + wi;
-  if (w >= p.total_warps || w >= p.total_tickets) return;
+  if (w >= p.total_warps) return;
+  prefetch_x(p, w);
+  if (w >= p.total_tickets) return;
   const uint32_t WW = p.total_warps;
   const uint32_t n_w = (p.total_tickets - w + WW - 1) / WW;  // tickets w, w+W, w+2W, ...
 
@@ -297,7 +328,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
 
   // ---- issue cursor: ticket ii, offset iq inside it. win = window of ii,
   // wn1 / wn2 = windows of ii+1 / ii+2 (fetched two tickets ahead)
-  uint32_t ii = 0, iq = 0, ibeg = 0, ilen = 0, icol = 0;
+  uint32_t ii = 0, iq = 0, ibeg = 0, ilen = 0, icol = 0, imask = 0;
   uint32_t win = window(0), wn1 = window(1), wn2 = window(2), wlong = 0;
   uint32_t iseq = 0;   // deltas issued
   uint32_t signs = 0;  // sign bit of the delta in each ring slot
@@ -308,6 +339,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     ibeg = r.beg;
     ilen = r.end - r.beg;
     icol = sm.slab[ii & (kRecWin - 1)] * kSlab + uint32_t(lane) * V;
+    imask = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (icol + uint32_t(u) * kSeg < p.d) imask |= 1u << u;
     wlong = 32 + uint32_t(lane) < ilen ? __ldg(p.dcol + ibeg + 32 + lane) : 0u;
   };
   // step to the next ticket with deltas, shifting the window prefetch;
@@ -340,7 +375,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       const float* src = p.x + (long long)c * p.ldx + icol;
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (icol + uint32_t(u) * kSeg < p.d) cp_async<V>(&sm.ring[s][u][lane * V], src + u * kSeg);
+        if ((imask >> u) & 1u) cp_async<V>(&sm.ring[s][u][lane * V], src + u * kSeg);
       if constexpr (SCALE)
         if (lane == 0) cp_async_f(&sm.sring[s], p.scale + c);
       signs = (signs & ~(1u << s)) | ((cw >> 31) << s);
@@ -378,6 +413,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     const TRec r = sm.rec[k_ci];
     const uint32_t slab = sm.slab[k_ci], t = sm.item[k_ci];
     const uint32_t col = slab * kSlab + uint32_t(lane) * V;
+    uint32_t umask = 0;  // segments of this lane inside the matrix
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (col + uint32_t(u) * kSeg < p.d) umask |= 1u << u;
     T4 acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = W::zero();
@@ -390,13 +429,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
         __syncwarp();  // lane 0's scale copy (covered by its wait) is visible
         sc = sm.sring[s];
       }
-      const bool neg = (signs >> s) & 1u;
+      const uint32_t neg = ((signs >> s) & 1u) << 31;  // fl(a + (-x)) == fl(a - x)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (col + uint32_t(u) * kSeg < p.d) {
+        if ((umask >> u) & 1u) {
           T4 v = lds<V>(&sm.ring[s][u][lane * V]);
           if constexpr (SCALE) v = W::mul(v, sc);
-          acc[u] = neg ? W::sub(acc[u], v) : W::add(acc[u], v);
+          acc[u] = W::add(acc[u], xor_sign<V>(v, neg));
         }
       }
       ++cseq;
@@ -469,18 +508,6 @@ struct alignas(16) RegSmem {
   float srow[NORM ? kRecWin : 1];
 };
 
-template <int V>
-__device__ __forceinline__ typename Vec<V>::T xor_sign(typename Vec<V>::T v, uint32_t m) {
-  if constexpr (V == 4) {
-    return make_float4(__int_as_float(__float_as_int(v.x) ^ m), __int_as_float(__float_as_int(v.y) ^ m),
-                       __int_as_float(__float_as_int(v.z) ^ m), __int_as_float(__float_as_int(v.w) ^ m));
-  } else if constexpr (V == 2) {
-    return make_float2(__int_as_float(__float_as_int(v.x) ^ m), __int_as_float(__float_as_int(v.y) ^ m));
-  } else {
-    return __int_as_float(__float_as_int(v) ^ m);
-  }
-}
-
 template <int V, int U, int G, bool NORM, bool SCALE>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_rkernel(const Params p) {
   using W = Vec<V>;
@@ -495,7 +522,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_rkernel(const Params p)
   const uint32_t cta = blockIdx.x, wi = threadIdx.x >> 5;
   const uint32_t w = (cta % p.cta_stride) * (p.total_warps / p.cta_stride) +
                      (cta / p.cta_stride) * kWarpsPerCta + wi;
-  if (w >= p.total_warps || w >= p.total_tickets) return;
+  if (w >= p.total_warps) return;
+  prefetch_x(p, w);
+  if (w >= p.total_tickets) return;
   const uint32_t n_w = (p.total_tickets - w + p.total_warps - 1) / p.total_warps;
 
   uint32_t g = 0;
@@ -998,6 +1027,13 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   p.total_tickets = uint32_t(tickets);
   p.epoch = h->epoch;
   p.relu = relu ? 1u : 0u;
+  // pull a small, contiguous X into L2 ahead of the gathers
+  const uint64_t xbytes = uint64_t(L.n_cols) * d * sizeof(float);
+  p.prefetch_bytes = (h->opt.prefetch != 0 && uint64_t(ldin) == d && xbytes >= (1u << 20) &&
+                      xbytes <= uint64_t(h->l2_bytes) / 2 &&
+                      (reinterpret_cast<uintptr_t>(xin) & 15) == 0)
+                         ? (xbytes & ~15ull)
+                         : 0;
 
   const bool norm = L.normalized, scl = L.normalized && !prescale;
   if (h->opt.kernel == 2) {  // register-staged group pipeline

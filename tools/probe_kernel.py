@@ -37,12 +37,10 @@ for name in sys.argv[1].split(","):
         for vn, cc in variants.items():
             if only and vn != only:
                 continue
-            for faithful, kern, segs in ((False, "auto", 0), (False, "auto", 4), (False, "auto", 16),
-                                         (False, "auto", 32), (False, "auto", 1 << 30)):
+            for faithful, kern, segs in ((False, "auto", 0), (False, "auto", 1)):
                 if vn != "default" and (faithful or segs):
                     continue
-                op = P.DeviceCbm(cc, order_faithful=faithful, kernel=kern,
-                                 flatten_gain=segs if segs else -1)
+                op = P.DeviceCbm(cc, order_faithful=faithful, kernel=kern, prefetch=bool(segs))
                 med_f, min_f = timeit(op, x, y, flush)
                 med, mn = timeit(op, x, y, None)
-                print(f"{name} d={d} {vn:8s} gain={segs} flush med {med_f:8.1f}us  noflush med {med:8.1f}us min {mn:8.1f}us  info={ {k: op.info()[k] for k in ('n_levels','n_items','launches_per_call')} }", flush=True)
+                print(f"{name} d={d} {vn:8s} prefetch={segs} flush med {med_f:8.1f}us  noflush med {med:8.1f}us min {mn:8.1f}us  info={ {k: op.info()[k] for k in ('n_levels','n_items','launches_per_call')} }", flush=True)
