@@ -52,10 +52,13 @@ inline cbm_b200_cbm_view view_of(const CbmMatrix& c) {
   return v;
 }
 
-// The uploaded operator (the device counterpart of holding a CbmMatrix).
+// The uploaded operator (the device counterpart of holding a CbmMatrix). As a
+// drop-in it defaults to the order-faithful mode: results are bit-identical
+// to cbm::spmm_into for any X. order_faithful = false selects the faster mode
+// (split / flattened rows; bit-exact on integer X, <= 1e-5 normwise otherwise).
 class DeviceCbm {
  public:
-  explicit DeviceCbm(const CbmMatrix& c, int device = -1, bool order_faithful = false) {
+  explicit DeviceCbm(const CbmMatrix& c, int device = -1, bool order_faithful = true) {
     cbm_b200_options opt;
     cbm_b200_default_options(&opt);
     opt.device = device;

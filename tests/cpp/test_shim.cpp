@@ -109,11 +109,16 @@ int main() {
     auto a = community_graph(50, 40, 40, 1, 0xC0FFEE);
     auto c = build_cbm(a, 0);
     auto cn = build_cbm_normalized(a, 0);
-    b200::DeviceCbm dc(c, -1, true), dn(cn, -1, true);
+    b200::DeviceCbm dc(c), dn(cn);
+    b200::DeviceCbm fast(c, -1, /*order_faithful=*/false);
     for (index_t width : {1u, 7u, 64u, 130u}) {
       auto b = random_dense(a.n_cols, width, -1.0, 1.0, width);
       CHECK(bitwise(b200::spmm(dc, b), spmm(c, b)));
       CHECK(bitwise(b200::spmm(dn, b), spmm(cn, b)));
+      // the fast mode on integer operands is exact too
+      DenseMatrix bi(b.n_rows, b.n_cols);
+      for (std::size_t i = 0; i < bi.data.size(); ++i) bi.data[i] = real_t(int(b.data[i] * 8));
+      CHECK(bitwise(b200::spmm(fast, bi), spmm(c, bi)));
     }
   }
   std::printf("test_shim: %d checks, %d failures\n", g_checks, g_fail);
