@@ -211,9 +211,11 @@ __device__ __forceinline__ void add_partials(const Params& p, const uint32_t* fl
 template <int V>
 __device__ __forceinline__ void cp_async(float* dst, const float* src) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-  // .ca: allocate in L1 — adjacent rows of one SM gather the same X rows
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(V * 4)
-               : "memory");
+  if constexpr (V == 4)  // 16 B: stream through L2 only (L1 reuse measured nil)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(V * 4)
+                 : "memory");
 }
 __device__ __forceinline__ void cp_async_f(float* dst, const float* src) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -420,16 +422,52 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     T4 acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = W::zero();
+    // deltas two at a time: one wait covers both slots and both shared-memory
+    // reads are in flight before the adds (the adds stay in delta order)
+    uint32_t k = r.beg;
 #pragma unroll 1
-    for (uint32_t k = r.beg; k < r.end; ++k) {
-      cp_wait<D - 1>();  // this lane's copies of delta `cseq` have landed
+    for (; k + 1 < r.end; k += 2) {
+      cp_wait<D - 2>();  // this lane's copies of deltas cseq, cseq+1 have landed
+      const uint32_t s0 = cseq & (D - 1), s1 = (cseq + 1) & (D - 1);
+      float sc0 = 1.0f, sc1 = 1.0f;
+      if constexpr (SCALE) {
+        __syncwarp();  // lane 0's scale copies (covered by its wait) are visible
+        sc0 = sm.sring[s0];
+        sc1 = sm.sring[s1];
+      }
+      T4 v0[U], v1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v0[u] = ((umask >> u) & 1u) ? lds<V>(&sm.ring[s0][u][lane * V]) : W::zero();
+        v1[u] = ((umask >> u) & 1u) ? lds<V>(&sm.ring[s1][u][lane * V]) : W::zero();
+      }
+      const uint32_t n0 = ((signs >> s0) & 1u) << 31, n1 = ((signs >> s1) & 1u) << 31;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if ((umask >> u) & 1u) {
+          T4 a0 = v0[u], a1 = v1[u];
+          if constexpr (SCALE) {
+            a0 = W::mul(a0, sc0);
+            a1 = W::mul(a1, sc1);
+          }
+          acc[u] = W::add(acc[u], xor_sign<V>(a0, n0));  // fl(a + (-x)) == fl(a - x)
+          acc[u] = W::add(acc[u], xor_sign<V>(a1, n1));
+        }
+      }
+      cseq += 2;
+      __syncwarp();  // slots s0, s1 fully read before their refill
+      issue_one();
+      issue_one();
+    }
+    if (k < r.end) {  // odd tail
+      cp_wait<D - 1>();
       const uint32_t s = cseq & (D - 1);
       float sc = 1.0f;
       if constexpr (SCALE) {
-        __syncwarp();  // lane 0's scale copy (covered by its wait) is visible
+        __syncwarp();
         sc = sm.sring[s];
       }
-      const uint32_t neg = ((signs >> s) & 1u) << 31;  // fl(a + (-x)) == fl(a - x)
+      const uint32_t neg = ((signs >> s) & 1u) << 31;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if ((umask >> u) & 1u) {
@@ -439,7 +477,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
         }
       }
       ++cseq;
-      __syncwarp();  // slot s fully read before its refill
+      __syncwarp();
       issue_one();
     }
     // ---- epilogue: partials, then CHUNK/MERGE publish or ROW stage 2 + 3
