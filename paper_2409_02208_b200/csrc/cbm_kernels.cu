@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   constexpr uint32_t kSlab = kSeg * U;    // floats per ticket
   constexpr int PFp = U >= 4 ? 2 : (U == 2 ? 4 : 8);
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
+  constexpr int B = (D >= 8 && U >= 2) ? 4 : 2;  // deltas consumed per wait (measured)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   using SM = WarpSmem<V, U, D, NORM, SCALE>;
@@ -422,44 +423,42 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     T4 acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = W::zero();
-    // deltas two at a time: one wait covers both slots and both shared-memory
+    // deltas B at a time: one wait covers B slots and all B shared-memory
     // reads are in flight before the adds (the adds stay in delta order)
     uint32_t k = r.beg;
 #pragma unroll 1
-    for (; k + 1 < r.end; k += 2) {
-      cp_wait<D - 2>();  // this lane's copies of deltas cseq, cseq+1 have landed
-      const uint32_t s0 = cseq & (D - 1), s1 = (cseq + 1) & (D - 1);
-      float sc0 = 1.0f, sc1 = 1.0f;
-      if constexpr (SCALE) {
-        __syncwarp();  // lane 0's scale copies (covered by its wait) are visible
-        sc0 = sm.sring[s0];
-        sc1 = sm.sring[s1];
-      }
-      T4 v0[U], v1[U];
+    for (; k + B <= r.end; k += B) {
+      cp_wait<D - B>();  // this lane's copies of deltas cseq .. cseq+B-1 have landed
+      float sc[B];
+      if constexpr (SCALE) __syncwarp();  // lane 0's scale copies are visible
+      T4 v[B][U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        v0[u] = ((umask >> u) & 1u) ? lds<V>(&sm.ring[s0][u][lane * V]) : W::zero();
-        v1[u] = ((umask >> u) & 1u) ? lds<V>(&sm.ring[s1][u][lane * V]) : W::zero();
-      }
-      const uint32_t n0 = ((signs >> s0) & 1u) << 31, n1 = ((signs >> s1) & 1u) << 31;
+      for (int b = 0; b < B; ++b) {
+        const uint32_t sb = (cseq + b) & (D - 1);
+        if constexpr (SCALE) sc[b] = sm.sring[sb];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if ((umask >> u) & 1u) {
-          T4 a0 = v0[u], a1 = v1[u];
-          if constexpr (SCALE) {
-            a0 = W::mul(a0, sc0);
-            a1 = W::mul(a1, sc1);
+        for (int u = 0; u < U; ++u)
+          v[b][u] = ((umask >> u) & 1u) ? lds<V>(&sm.ring[sb][u][lane * V]) : W::zero();
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const uint32_t nb = ((signs >> ((cseq + b) & (D - 1))) & 1u) << 31;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if ((umask >> u) & 1u) {
+            T4 a = v[b][u];
+            if constexpr (SCALE) a = W::mul(a, sc[b]);
+            acc[u] = W::add(acc[u], xor_sign<V>(a, nb));  // fl(a + (-x)) == fl(a - x)
           }
-          acc[u] = W::add(acc[u], xor_sign<V>(a0, n0));  // fl(a + (-x)) == fl(a - x)
-          acc[u] = W::add(acc[u], xor_sign<V>(a1, n1));
         }
       }
-      cseq += 2;
-      __syncwarp();  // slots s0, s1 fully read before their refill
-      issue_one();
-      issue_one();
+      cseq += B;
+      __syncwarp();  // the B slots are fully read before their refill
+#pragma unroll
+      for (int b = 0; b < B; ++b) issue_one();
     }
-    if (k < r.end) {  // odd tail
+#pragma unroll 1
+    for (; k < r.end; ++k) {  // tail, one delta at a time
       cp_wait<D - 1>();
       const uint32_t s = cseq & (D - 1);
       float sc = 1.0f;
