@@ -253,6 +253,23 @@ __device__ __forceinline__ typename Vec<V>::T xor_sign(typename Vec<V>::T v, uin
   }
 }
 
+// acc (+) (+-v) in one instruction per element: fma(v, +-1, acc) forms the
+// exact product +-v and rounds the sum once, i.e. exactly fl(acc + v) or
+// fl(acc - v) (signed zeros included) -- the reference's stage-1 step for a
+// +-1 delta value (kernels.cpp:30-35).
+template <int V>
+__device__ __forceinline__ typename Vec<V>::T fma_sign(typename Vec<V>::T acc,
+                                                       typename Vec<V>::T v, float sg) {
+  if constexpr (V == 4) {
+    return make_float4(__fmaf_rn(v.x, sg, acc.x), __fmaf_rn(v.y, sg, acc.y),
+                       __fmaf_rn(v.z, sg, acc.z), __fmaf_rn(v.w, sg, acc.w));
+  } else if constexpr (V == 2) {
+    return make_float2(__fmaf_rn(v.x, sg, acc.x), __fmaf_rn(v.y, sg, acc.y));
+  } else {
+    return __fmaf_rn(v, sg, acc);
+  }
+}
+
 constexpr int kWarpsPerCta = 4;
 constexpr uint32_t kRecWin = 64;  // ticket records staged per warp (two groups of 32)
 
@@ -416,10 +433,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     const TRec r = sm.rec[k_ci];
     const uint32_t slab = sm.slab[k_ci], t = sm.item[k_ci];
     const uint32_t col = slab * kSlab + uint32_t(lane) * V;
-    uint32_t umask = 0;  // segments of this lane inside the matrix
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (col + uint32_t(u) * kSeg < p.d) umask |= 1u << u;
     T4 acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = W::zero();
@@ -429,27 +442,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
 #pragma unroll 1
     for (; k + B <= r.end; k += B) {
       cp_wait<D - B>();  // this lane's copies of deltas cseq .. cseq+B-1 have landed
+      // Segments outside the matrix read stale ring bytes into accumulators
+      // that are never stored: no per-segment branch on the hot path.
       float sc[B];
       if constexpr (SCALE) __syncwarp();  // lane 0's scale copies are visible
       T4 v[B][U];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
         const uint32_t sb = (cseq + b) & (D - 1);
-        if constexpr (SCALE) sc[b] = sm.sring[sb];
+        const uint32_t nb = ((signs >> sb) & 1u) << 31;
+        // signed factor: -s_c (normalized: fl(-s*x) == -fl(s*x)) or -1
+        sc[b] = __int_as_float(__float_as_int(SCALE ? sm.sring[sb] : 1.0f) ^ nb);
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          v[b][u] = ((umask >> u) & 1u) ? lds<V>(&sm.ring[sb][u][lane * V]) : W::zero();
+        for (int u = 0; u < U; ++u) v[b][u] = lds<V>(&sm.ring[sb][u][lane * V]);
       }
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        const uint32_t nb = ((signs >> ((cseq + b) & (D - 1))) & 1u) << 31;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if ((umask >> u) & 1u) {
-            T4 a = v[b][u];
-            if constexpr (SCALE) a = W::mul(a, sc[b]);
-            acc[u] = W::add(acc[u], xor_sign<V>(a, nb));  // fl(a + (-x)) == fl(a - x)
-          }
+          if constexpr (SCALE) acc[u] = W::add(acc[u], W::mul(v[b][u], sc[b]));
+          else acc[u] = fma_sign<V>(acc[u], v[b][u], sc[b]);
         }
       }
       cseq += B;
@@ -461,19 +473,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     for (; k < r.end; ++k) {  // tail, one delta at a time
       cp_wait<D - 1>();
       const uint32_t s = cseq & (D - 1);
-      float sc = 1.0f;
-      if constexpr (SCALE) {
-        __syncwarp();
-        sc = sm.sring[s];
-      }
+      if constexpr (SCALE) __syncwarp();
       const uint32_t neg = ((signs >> s) & 1u) << 31;
+      const float sc = __int_as_float(__float_as_int(SCALE ? sm.sring[s] : 1.0f) ^ neg);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if ((umask >> u) & 1u) {
-          T4 v = lds<V>(&sm.ring[s][u][lane * V]);
-          if constexpr (SCALE) v = W::mul(v, sc);
-          acc[u] = W::add(acc[u], xor_sign<V>(v, neg));
-        }
+        const T4 v = lds<V>(&sm.ring[s][u][lane * V]);
+        if constexpr (SCALE) acc[u] = W::add(acc[u], W::mul(v, sc));
+        else acc[u] = fma_sign<V>(acc[u], v, sc);
       }
       ++cseq;
       __syncwarp();
