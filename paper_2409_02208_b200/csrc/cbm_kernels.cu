@@ -11,11 +11,12 @@
 //
 // Schedule. A ticket is (column slab, item), ordered slab-major then item
 // order (CHUNK, MERGE, then ROW items by tree depth). The grid is launched
-// cooperatively (every warp co-resident) and ticket T belongs to warp
-// T mod W: no claim counter, no atomics. A warp finishes its tickets in
-// increasing order and every wait (parent row, split-row partials) targets a
-// smaller ticket, so the smallest unfinished ticket is always being worked on
-// and its inputs are complete: no deadlock.
+// cooperatively (every warp co-resident) and each warp walks a host-built
+// list of tickets (schedule_for: list scheduling by estimated work): no claim
+// counter, no atomics. A warp finishes its tickets in increasing order and
+// every wait (parent row, split-row partials) targets a smaller ticket, so the
+// smallest unfinished ticket is always being worked on and its inputs are
+// complete: no deadlock.
 //
 // Streaming. Each warp walks its ticket sequence with two cursors. The issue
 // cursor keeps D X-row segments in flight with cp.async (LDGSTS): every lane
@@ -144,7 +145,8 @@ struct Params {
   float* partial;   // CHUNK / MERGE partial sums, stride dpad
   float* interior;  // unscaled interior rows (normalized), stride dpad
   uint32_t* flags;
-  const uint32_t* __restrict__ wstart;  // per warp: first ticket of its range (total_warps + 1)
+  const uint32_t* __restrict__ sched;   // tickets grouped by warp (host list schedule)
+  const uint32_t* __restrict__ wstart;  // per warp: offset of its tickets in sched (+1 entry)
   uint32_t n_items, n_chunk, d, dpad;
   uint32_t total_tickets, total_warps, epoch;
   uint32_t cta_stride;  // CTAs per residency round (grid / CTAs per SM)
@@ -289,14 +291,14 @@ struct alignas(16) WarpSmem {
   float sring[SCALE ? D : 1];      // the delta's column scale (lane 0 copies, all read)
 };
 
-// Stage the records of warp-sequence tickets [i0, i0+32) (ticket w + i*W).
+// Stage the records of warp-sequence tickets [i0, i0+32) of this warp's list.
 template <class SM>
-__device__ __forceinline__ void stage_recs(const Params& p, SM& sm, uint32_t w, uint32_t i0,
+__device__ __forceinline__ void stage_recs(const Params& p, SM& sm, uint32_t wbase, uint32_t i0,
                                            uint32_t n_w, bool norm) {
   const int lane = threadIdx.x & 31;
   const uint32_t i = i0 + uint32_t(lane);
   if (i < n_w) {
-    const uint32_t T = w + i * p.total_warps;
+    const uint32_t T = __ldg(p.sched + wbase + i);
     const uint32_t sl = T / p.n_items;
     const uint32_t t = T - sl * p.n_items;
     const uint32_t k = i & (kRecWin - 1);
@@ -330,13 +332,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
                      (cta / p.cta_stride) * kWarpsPerCta + wi;
   if (w >= p.total_warps) return;
   prefetch_x(p, w);
-  if (w >= p.total_tickets) return;
-  const uint32_t WW = p.total_warps;
-  const uint32_t n_w = (p.total_tickets - w + WW - 1) / WW;  // tickets w, w+W, w+2W, ...
+  const uint32_t wbase = __ldg(p.wstart + w);
+  const uint32_t n_w = __ldg(p.wstart + w + 1) - wbase;  // this warp's tickets, increasing
+  if (n_w == 0) return;
 
   uint32_t g = 0;  // staged records cover warp-sequence tickets [g, g + 64)
-  stage_recs(p, sm, w, 0, n_w, NORM);
-  stage_recs(p, sm, w, 32, n_w, NORM);
+  stage_recs(p, sm, wbase, 0, n_w, NORM);
+  stage_recs(p, sm, wbase, 32, n_w, NORM);
   __syncwarp();
   auto R = [&](uint32_t i) -> const TRec& { return sm.rec[i & (kRecWin - 1)]; };
   // first 32 column words of ticket i (0 past the end / outside the window)
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   for (uint32_t ci = 0; ci < n_w; ++ci) {
     if (ci - g == 32) {  // slide the record window by one group
       __syncwarp();
-      stage_recs(p, sm, w, g + kRecWin, n_w, NORM);
+      stage_recs(p, sm, wbase, g + kRecWin, n_w, NORM);
       g += 32;
       __syncwarp();
       if (iblocked) {
@@ -568,12 +570,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_rkernel(const Params p)
                      (cta / p.cta_stride) * kWarpsPerCta + wi;
   if (w >= p.total_warps) return;
   prefetch_x(p, w);
-  if (w >= p.total_tickets) return;
-  const uint32_t n_w = (p.total_tickets - w + p.total_warps - 1) / p.total_warps;
+  const uint32_t wbase = __ldg(p.wstart + w);
+  const uint32_t n_w = __ldg(p.wstart + w + 1) - wbase;
+  if (n_w == 0) return;
 
   uint32_t g = 0;
-  stage_recs(p, sm, w, 0, n_w, NORM);
-  stage_recs(p, sm, w, 32, n_w, NORM);
+  stage_recs(p, sm, wbase, 0, n_w, NORM);
+  stage_recs(p, sm, wbase, 32, n_w, NORM);
   __syncwarp();
   auto window = [&](uint32_t i) -> uint32_t {
     if (i >= n_w || i >= g + kRecWin) return 0u;
@@ -714,7 +717,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_rkernel(const Params p)
     // ---- advance: record window, index windows
     if (ci + 1 - g == 32 && ci + 1 < n_w) {
       __syncwarp();
-      stage_recs(p, sm, w, g + kRecWin, n_w, NORM);
+      stage_recs(p, sm, wbase, g + kRecWin, n_w, NORM);
       g += 32;
       __syncwarp();
     }
@@ -725,8 +728,79 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_rkernel(const Params p)
   }
 }
 
+// Static list schedule of the tickets over the resident warps (cbm_kernel).
+// Tickets are taken in order and each goes to the warp that an estimated
+// clock frees first (ties: lowest warp), starting no earlier than its
+// parent / partial producers are estimated to finish; cost ~ per-ticket
+// overhead + deltas + partial rows + parent row. Every warp's list is
+// increasing, which is all the deadlock argument needs (the smallest
+// unfinished ticket is always being worked on). Balancing by work instead of
+// round-robin by count removes the tail where warps holding several 32-delta
+// chunks finish long after the rest.
+const DeviceMatrix::Schedule& schedule_for(DeviceMatrix* h, uint32_t warps, uint32_t slabs,
+                                           cudaStream_t s) {
+  const uint64_t key = (uint64_t(warps) << 32) | slabs;
+  auto it = h->schedules.find(key);
+  if (it != h->schedules.end()) return it->second;
+  const Layout& L = h->info;
+  const uint32_t n = L.n_items;
+  const uint64_t total = uint64_t(n) * slabs;
+  constexpr float kTicket = 4.0f;  // epilogue / record overhead in delta-equivalents
+  std::vector<uint32_t> owner(total);
+  std::vector<uint32_t> count(size_t(warps) + 1, 0);
+  std::vector<float> fin(n);
+  using Slot = std::pair<float, uint32_t>;
+  std::vector<Slot> heap;
+  heap.reserve(warps);
+  for (uint32_t w = 0; w < warps; ++w) heap.emplace_back(0.0f, w);
+  auto later = [](const Slot& a, const Slot& b) { return a > b; };  // min-heap
+  std::make_heap(heap.begin(), heap.end(), later);
+  for (uint32_t sl = 0; sl < slabs; ++sl) {
+    for (uint32_t t = 0; t < n; ++t) {
+      std::pop_heap(heap.begin(), heap.end(), later);
+      Slot& top = heap.back();
+      const uint32_t* dp = &h->item_dep[size_t(t) * 3];
+      float start = top.first;
+      float cost = kTicket + float(L.item_beg[t + 1] - L.item_beg[t]) + float(dp[2]);
+      if (dp[0] != kNoItem) {
+        start = std::max(start, fin[dp[0]]);
+        cost += 1.0f;
+      }
+      for (uint32_t j = 0; j < dp[2]; ++j) start = std::max(start, fin[dp[1] + j]);
+      fin[t] = start + cost;
+      top.first = fin[t];
+      owner[uint64_t(sl) * n + t] = top.second;
+      ++count[top.second + 1];
+      std::push_heap(heap.begin(), heap.end(), later);
+    }
+  }
+  for (uint32_t w = 0; w < warps; ++w) count[w + 1] += count[w];
+  std::vector<uint32_t> list(total);
+  {
+    std::vector<uint32_t> pos(count.begin(), count.end() - 1);
+    for (uint64_t T = 0; T < total; ++T) list[pos[owner[T]]++] = uint32_t(T);
+  }
+  DeviceMatrix::Schedule sc;
+  try {
+    ck(cudaMalloc(&sc.list, std::max<uint64_t>(total, 1) * sizeof(uint32_t)), "schedule");
+    ck(cudaMalloc(&sc.wstart, count.size() * sizeof(uint32_t)), "schedule");
+    // synchronous copies: the schedule is built once per (warps, slabs)
+    ck(cudaMemcpy(sc.list, list.data(), total * sizeof(uint32_t), cudaMemcpyHostToDevice),
+       "schedule upload");
+    ck(cudaMemcpy(sc.wstart, count.data(), count.size() * sizeof(uint32_t),
+                  cudaMemcpyHostToDevice),
+       "schedule upload");
+  } catch (...) {
+    if (sc.list) cudaFree(sc.list);
+    if (sc.wstart) cudaFree(sc.wstart);
+    throw;
+  }
+  (void)s;
+  return h->schedules.emplace(key, sc).first->second;
+}
+
 template <int V, int U, int G, bool NORM, bool SCALE>
-void launch_reg(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
+void launch_reg(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
   constexpr size_t smem = kWarpsPerCta * sizeof(RegSmem<V, U, NORM, SCALE>);
   static int bps = -1;
   if (bps < 0) {
@@ -751,6 +825,9 @@ void launch_reg(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
     grid = int(p.cta_stride) * per_sm;
   }
   p.total_warps = uint32_t(grid * wpb);
+  const auto& sc = schedule_for(h, p.total_warps, slabs, s);
+  p.sched = sc.list;
+  p.wstart = sc.wstart;
   void* args[] = {&p};
   ck(cudaLaunchCooperativeKernel(
          reinterpret_cast<const void*>(&cbm_rkernel<V, U, G, NORM, SCALE>), dim3(grid),
@@ -759,10 +836,11 @@ void launch_reg(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
 }
 
 template <int V, int U, int G>
-void run_reg(Params& p, uint64_t tickets, bool norm, bool scl, DeviceMatrix* h, cudaStream_t s) {
-  if (!norm) launch_reg<V, U, G, false, false>(p, tickets, h, s);
-  else if (scl) launch_reg<V, U, G, true, true>(p, tickets, h, s);
-  else launch_reg<V, U, G, true, false>(p, tickets, h, s);
+void run_reg(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl, DeviceMatrix* h,
+             cudaStream_t s) {
+  if (!norm) launch_reg<V, U, G, false, false>(p, tickets, slabs, h, s);
+  else if (scl) launch_reg<V, U, G, true, true>(p, tickets, slabs, h, s);
+  else launch_reg<V, U, G, true, false>(p, tickets, slabs, h, s);
 }
 
 // xs[c, :] = row_scale[c] (*) x[c, :] — the bit-identical products of the
@@ -781,7 +859,7 @@ __global__ void prescale_kernel(const float* __restrict__ x, long long ldx,
 // Cooperative launch: one full residency wave (all warps co-resident), no
 // more warps than tickets.
 template <int V, int U, int D, bool NORM, bool SCALE>
-void launch_one(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
+void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
   constexpr size_t smem = kWarpsPerCta * sizeof(WarpSmem<V, U, D, NORM, SCALE>);
   static int bps = -1;  // per template instance
   if (bps < 0) {
@@ -808,6 +886,9 @@ void launch_one(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
     grid = int(p.cta_stride) * per_sm;
   }
   p.total_warps = uint32_t(grid * wpb);
+  const auto& sc = schedule_for(h, p.total_warps, slabs, s);
+  p.sched = sc.list;
+  p.wstart = sc.wstart;
   void* args[] = {&p};
   ck(cudaLaunchCooperativeKernel(
          reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SCALE>), dim3(grid),
@@ -816,11 +897,11 @@ void launch_one(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
 }
 
 template <int V, int U, int D>
-void run_kernel(Params& p, uint64_t tickets, bool norm, bool scl, DeviceMatrix* h,
-                cudaStream_t s) {
-  if (!norm) launch_one<V, U, D, false, false>(p, tickets, h, s);
-  else if (scl) launch_one<V, U, D, true, true>(p, tickets, h, s);
-  else launch_one<V, U, D, true, false>(p, tickets, h, s);
+void run_kernel(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl,
+                DeviceMatrix* h, cudaStream_t s) {
+  if (!norm) launch_one<V, U, D, false, false>(p, tickets, slabs, h, s);
+  else if (scl) launch_one<V, U, D, true, true>(p, tickets, slabs, h, s);
+  else launch_one<V, U, D, true, false>(p, tickets, slabs, h, s);
 }
 
 template <typename T>
@@ -955,7 +1036,13 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
     if (!coop) throw cuda_error("device lacks cooperative launch", CBM_B200_ECUDA);
     // keep only sizes on the host
     L.dcol = {};
-    L.rec = {};  // item_beg stays: it drives the per-warp work partition
+    h->item_dep.resize(size_t(L.n_items) * 3);  // for the ticket schedule
+    for (uint32_t t = 0; t < L.n_items; ++t) {
+      h->item_dep[size_t(t) * 3] = L.rec[size_t(t) * 8 + 3];
+      h->item_dep[size_t(t) * 3 + 1] = L.rec[size_t(t) * 8 + 5];
+      h->item_dep[size_t(t) * 3 + 2] = L.rec[size_t(t) * 8 + 6];
+    }
+    L.rec = {};  // item_beg and item_dep stay: they drive the ticket schedule
     L.srow = {};
     L.scale = {};
     h->info = std::move(L);
@@ -975,6 +1062,10 @@ void device_free(DeviceMatrix* h) {
     for (auto e : h->ev) cudaEventDestroy(e);
   }
   if (h->gcn_h) cudaFree(h->gcn_h);
+  for (auto& kv : h->schedules) {
+    cudaFree(kv.second.list);
+    cudaFree(kv.second.wstart);
+  }
   for (void* p : {(void*)h->dcol, (void*)h->rec, (void*)h->srow, (void*)h->scale,
                   (void*)h->flags, (void*)h->partial,
                   (void*)h->interior, (void*)h->xs, (void*)h->xstage, (void*)h->ystage})
@@ -1082,30 +1173,30 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   const bool norm = L.normalized, scl = L.normalized && !prescale;
   if (h->opt.kernel == 2) {  // register-staged group pipeline
     if (V == 4) {
-      if (U == 4) run_reg<4, 4, 2>(p, tickets, norm, scl, h, s);
-      else if (U == 2) run_reg<4, 2, 4>(p, tickets, norm, scl, h, s);
-      else run_reg<4, 1, 8>(p, tickets, norm, scl, h, s);
+      if (U == 4) run_reg<4, 4, 2>(p, tickets, n_slabs, norm, scl, h, s);
+      else if (U == 2) run_reg<4, 2, 4>(p, tickets, n_slabs, norm, scl, h, s);
+      else run_reg<4, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);
     } else if (V == 2) {
-      if (U == 4) run_reg<2, 4, 4>(p, tickets, norm, scl, h, s);
-      else if (U == 2) run_reg<2, 2, 8>(p, tickets, norm, scl, h, s);
-      else run_reg<2, 1, 8>(p, tickets, norm, scl, h, s);
+      if (U == 4) run_reg<2, 4, 4>(p, tickets, n_slabs, norm, scl, h, s);
+      else if (U == 2) run_reg<2, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
+      else run_reg<2, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);
     } else {
-      if (U == 4) run_reg<1, 4, 8>(p, tickets, norm, scl, h, s);
-      else if (U == 2) run_reg<1, 2, 8>(p, tickets, norm, scl, h, s);
-      else run_reg<1, 1, 8>(p, tickets, norm, scl, h, s);
+      if (U == 4) run_reg<1, 4, 8>(p, tickets, n_slabs, norm, scl, h, s);
+      else if (U == 2) run_reg<1, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
+      else run_reg<1, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);
     }
   } else if (V == 4) {
-    if (U == 4) run_kernel<4, 4, 4>(p, tickets, norm, scl, h, s);
-    else if (U == 2) run_kernel<4, 2, 8>(p, tickets, norm, scl, h, s);
-    else run_kernel<4, 1, 8>(p, tickets, norm, scl, h, s);
+    if (U == 4) run_kernel<4, 4, 4>(p, tickets, n_slabs, norm, scl, h, s);
+    else if (U == 2) run_kernel<4, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
+    else run_kernel<4, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);
   } else if (V == 2) {
-    if (U == 4) run_kernel<2, 4, 8>(p, tickets, norm, scl, h, s);
-    else if (U == 2) run_kernel<2, 2, 8>(p, tickets, norm, scl, h, s);
-    else run_kernel<2, 1, 16>(p, tickets, norm, scl, h, s);
+    if (U == 4) run_kernel<2, 4, 8>(p, tickets, n_slabs, norm, scl, h, s);
+    else if (U == 2) run_kernel<2, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
+    else run_kernel<2, 1, 16>(p, tickets, n_slabs, norm, scl, h, s);
   } else {
-    if (U == 4) run_kernel<1, 4, 16>(p, tickets, norm, scl, h, s);
-    else if (U == 2) run_kernel<1, 2, 16>(p, tickets, norm, scl, h, s);
-    else run_kernel<1, 1, 16>(p, tickets, norm, scl, h, s);
+    if (U == 4) run_kernel<1, 4, 16>(p, tickets, n_slabs, norm, scl, h, s);
+    else if (U == 2) run_kernel<1, 2, 16>(p, tickets, n_slabs, norm, scl, h, s);
+    else run_kernel<1, 1, 16>(p, tickets, n_slabs, norm, scl, h, s);
   }
   ck(cudaGetLastError(), "cbm_kernel launch");
   ++h->last_launches;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -45,6 +46,13 @@ struct DeviceMatrix {
   // host-API pipeline: copy-in / copy-out streams and chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev[9] = {};
+  // static ticket -> warp schedules (cbm_kernel), one per (warps, slabs)
+  struct Schedule {
+    uint32_t* list = nullptr;    // tickets, grouped by warp, increasing inside a warp
+    uint32_t* wstart = nullptr;  // warps + 1 offsets into list
+  };
+  std::map<uint64_t, Schedule> schedules;
+  std::vector<uint32_t> item_dep;  // per item: parent item (ppos), first partial, count
   uint32_t epoch = 0;
   uint32_t last_launches = 0;
   std::mutex mu;
