@@ -137,6 +137,7 @@ struct Params {
   const uint4* __restrict__ rec;      // 2 x uint4 per item (layout.hpp)
   const float* __restrict__ srow;     // per item: its row's scale (normalized)
   const uint32_t* __restrict__ dcol;
+  const float* __restrict__ dval;     // per delta: +-row_scale[col] (normalized), dcol order
   const float* __restrict__ scale;    // per column scale (normalized, per-delta products)
   const float* __restrict__ x;
   long long ldx;
@@ -219,10 +220,6 @@ __device__ __forceinline__ void cp_async(float* dst, const float* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(V * 4)
                  : "memory");
 }
-__device__ __forceinline__ void cp_async_f(float* dst, const float* src) {
-  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
-}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -281,14 +278,13 @@ struct alignas(16) TRec {
   uint32_t psrc, first, cnt, slot;
 };
 
-template <int V, int U, int D, bool NORM, bool SCALE>
+template <int V, int U, int D, bool NORM>
 struct alignas(16) WarpSmem {
   float ring[D][U][32 * V];        // slot s, segment u, lane l: [s][u][l*V, l*V+V)
   TRec rec[kRecWin];               // warp-sequence tickets [g, g+64), slot i & 63
   uint32_t item[kRecWin];          // item index of the staged ticket
   uint32_t slab[kRecWin];          // column slab of the staged ticket
   float srow[NORM ? kRecWin : 1];  // row scale per staged ticket
-  float sring[SCALE ? D : 1];      // the delta's column scale (lane 0 copies, all read)
 };
 
 // Stage the records of warp-sequence tickets [i0, i0+32) of this warp's list.
@@ -311,7 +307,11 @@ __device__ __forceinline__ void stage_recs(const Params& p, SM& sm, uint32_t wba
   }
 }
 
-template <int V, int U, int D, bool NORM, bool SCALE>
+// SC: how a delta value enters stage 1.
+//   0  +-1 (binary, or normalized with a pre-scaled X): fma(x, +-1, acc), exact
+//   1  +-s_c, order-faithful: fl(acc + fl(+-s_c * x)), the reference's two roundings
+//   2  +-s_c, default mode: fma(x, +-s_c, acc), one rounding (within tolerance)
+template <int V, int U, int D, bool NORM, int SC>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) {
   using W = Vec<V>;
   using T4 = typename W::T;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   constexpr int B = (D >= 8 && U >= 2) ? 4 : 2;  // deltas consumed per wait (measured)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  using SM = WarpSmem<V, U, D, NORM, SCALE>;
+  using SM = WarpSmem<V, U, D, NORM>;
   SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
   // warp -> position in the round-robin: CTAs b, b+G, b+2G, ... (G = p.cta_stride,
   // one per SM) share an SM, so consecutive tickets (adjacent rows, similar
@@ -341,19 +341,32 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   stage_recs(p, sm, wbase, 32, n_w, NORM);
   __syncwarp();
   auto R = [&](uint32_t i) -> const TRec& { return sm.rec[i & (kRecWin - 1)]; };
-  // first 32 column words of ticket i (0 past the end / outside the window)
-  auto window = [&](uint32_t i) -> uint32_t {
-    if (i >= n_w || i >= g + kRecWin) return 0u;
+  // 32 column words (and values) of a delta block: lane j holds delta k0 + j
+  struct Wd {
+    uint32_t c;
+    float v;
+  };
+  auto fetch = [&](uint32_t k0, uint32_t end) -> Wd {
+    Wd r{0u, 0.0f};
+    if (k0 + lane < end) {
+      r.c = __ldg(p.dcol + k0 + lane);
+      if constexpr (SC != 0) r.v = __ldg(p.dval + k0 + lane);
+    }
+    return r;
+  };
+  // first block of ticket i (empty past the end / outside the staged records)
+  auto window = [&](uint32_t i) -> Wd {
+    if (i >= n_w || i >= g + kRecWin) return Wd{0u, 0.0f};
     const TRec& r = R(i);
-    return r.beg + lane < r.end ? __ldg(p.dcol + r.beg + lane) : 0u;
+    return fetch(r.beg, r.end);
   };
 
   // ---- issue cursor: ticket ii, offset iq inside it. win = window of ii,
   // wn1 / wn2 = windows of ii+1 / ii+2 (fetched two tickets ahead)
   uint32_t ii = 0, iq = 0, ibeg = 0, ilen = 0, icol = 0, imask = 0;
-  uint32_t win = window(0), wn1 = window(1), wn2 = window(2), wlong = 0;
+  Wd win = window(0), wn1 = window(1), wn2 = window(2), wlong{0u, 0.0f};
   uint32_t iseq = 0;   // deltas issued
-  uint32_t signs = 0;  // sign bit of the delta in each ring slot
+  float vring = 0.0f;  // lane s: signed value of the delta in ring slot s
   bool iblocked = false;
   auto load_ticket = [&]() {  // cursor fields of ticket ii (window already in win)
     iq = 0;
@@ -365,7 +378,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (icol + uint32_t(u) * kSeg < p.d) imask |= 1u << u;
-    wlong = 32 + uint32_t(lane) < ilen ? __ldg(p.dcol + ibeg + 32 + lane) : 0u;
+    wlong = fetch(ibeg + 32, r.end);
   };
   // step to the next ticket with deltas, shifting the window prefetch;
   // block while the ticket two ahead is outside the staged records
@@ -391,23 +404,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   };
   auto issue_one = [&]() {
     if (!iblocked && ii < n_w) {
-      const uint32_t cw = __shfl_sync(kFull, win, iq & 31);
+      const uint32_t cw = __shfl_sync(kFull, win.c, iq & 31);
       const uint32_t c = cw & 0x7FFFFFFFu;
       const uint32_t s = iseq & (D - 1);
       const float* src = p.x + (long long)c * p.ldx + icol;
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if ((imask >> u) & 1u) cp_async<V>(&sm.ring[s][u][lane * V], src + u * kSeg);
-      if constexpr (SCALE)
-        if (lane == 0) cp_async_f(&sm.sring[s], p.scale + c);
-      signs = (signs & ~(1u << s)) | ((cw >> 31) << s);
+      float val;  // the delta's signed value (the reference's values[k], kernels.cpp:33)
+      if constexpr (SC != 0) val = __shfl_sync(kFull, win.v, iq & 31);
+      else val = __int_as_float(0x3F800000u | (cw & 0x80000000u));
+      if (uint32_t(lane) == s) vring = val;
       ++iseq;
       ++iq;
       if (iq == ilen) {
         next_ticket();
       } else if ((iq & 31) == 0) {  // next 32-delta block of a long ticket
         win = wlong;
-        wlong = iq + 32 + lane < ilen ? __ldg(p.dcol + ibeg + iq + 32 + lane) : 0u;
+        wlong = fetch(ibeg + iq + 32, ibeg + ilen);
       }
     }
     cp_commit();
@@ -447,14 +461,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       // Segments outside the matrix read stale ring bytes into accumulators
       // that are never stored: no per-segment branch on the hot path.
       float sc[B];
-      if constexpr (SCALE) __syncwarp();  // lane 0's scale copies are visible
       T4 v[B][U];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
         const uint32_t sb = (cseq + b) & (D - 1);
-        const uint32_t nb = ((signs >> sb) & 1u) << 31;
-        // signed factor: -s_c (normalized: fl(-s*x) == -fl(s*x)) or -1
-        sc[b] = __int_as_float(__float_as_int(SCALE ? sm.sring[sb] : 1.0f) ^ nb);
+        sc[b] = __shfl_sync(kFull, vring, sb);  // +-1 or +-s_c
 #pragma unroll
         for (int u = 0; u < U; ++u) v[b][u] = lds<V>(&sm.ring[sb][u][lane * V]);
       }
@@ -462,7 +473,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       for (int b = 0; b < B; ++b) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if constexpr (SCALE) acc[u] = W::add(acc[u], W::mul(v[b][u], sc[b]));
+          if constexpr (SC == 1) acc[u] = W::add(acc[u], W::mul(v[b][u], sc[b]));
           else acc[u] = fma_sign<V>(acc[u], v[b][u], sc[b]);
         }
       }
@@ -475,13 +486,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     for (; k < r.end; ++k) {  // tail, one delta at a time
       cp_wait<D - 1>();
       const uint32_t s = cseq & (D - 1);
-      if constexpr (SCALE) __syncwarp();
-      const uint32_t neg = ((signs >> s) & 1u) << 31;
-      const float sc = __int_as_float(__float_as_int(SCALE ? sm.sring[s] : 1.0f) ^ neg);
+      const float sc = __shfl_sync(kFull, vring, s);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const T4 v = lds<V>(&sm.ring[s][u][lane * V]);
-        if constexpr (SCALE) acc[u] = W::add(acc[u], W::mul(v, sc));
+        if constexpr (SC == 1) acc[u] = W::add(acc[u], W::mul(v, sc));
         else acc[u] = fma_sign<V>(acc[u], v, sc);
       }
       ++cseq;
@@ -858,16 +867,16 @@ __global__ void prescale_kernel(const float* __restrict__ x, long long ldx,
 
 // Cooperative launch: one full residency wave (all warps co-resident), no
 // more warps than tickets.
-template <int V, int U, int D, bool NORM, bool SCALE>
+template <int V, int U, int D, bool NORM, int SC>
 void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
-  constexpr size_t smem = kWarpsPerCta * sizeof(WarpSmem<V, U, D, NORM, SCALE>);
+  constexpr size_t smem = kWarpsPerCta * sizeof(WarpSmem<V, U, D, NORM>);
   static int bps = -1;  // per template instance
   if (bps < 0) {
-    ck(cudaFuncSetAttribute(cbm_kernel<V, U, D, NORM, SCALE>,
+    ck(cudaFuncSetAttribute(cbm_kernel<V, U, D, NORM, SC>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
        "smem attribute");
     int b = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_kernel<V, U, D, NORM, SCALE>,
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_kernel<V, U, D, NORM, SC>,
                                                      kWarpsPerCta * 32, smem),
        "occupancy");
     bps = std::max(1, b);
@@ -891,7 +900,7 @@ void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cu
   p.wstart = sc.wstart;
   void* args[] = {&p};
   ck(cudaLaunchCooperativeKernel(
-         reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SCALE>), dim3(grid),
+         reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SC>), dim3(grid),
          dim3(kWarpsPerCta * 32), args, smem, s),
      "cbm_kernel cooperative launch");
 }
@@ -899,9 +908,10 @@ void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cu
 template <int V, int U, int D>
 void run_kernel(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl,
                 DeviceMatrix* h, cudaStream_t s) {
-  if (!norm) launch_one<V, U, D, false, false>(p, tickets, slabs, h, s);
-  else if (scl) launch_one<V, U, D, true, true>(p, tickets, slabs, h, s);
-  else launch_one<V, U, D, true, false>(p, tickets, slabs, h, s);
+  if (!norm) launch_one<V, U, D, false, 0>(p, tickets, slabs, h, s);
+  else if (!scl) launch_one<V, U, D, true, 0>(p, tickets, slabs, h, s);
+  else if (h->info.order_faithful) launch_one<V, U, D, true, 1>(p, tickets, slabs, h, s);
+  else launch_one<V, U, D, true, 2>(p, tickets, slabs, h, s);
 }
 
 template <typename T>
@@ -1030,6 +1040,14 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
     if (L.normalized) {
       put(h->srow, L.srow, "upload srow");
       put(h->scale, L.scale, "upload scale");
+      // the signed delta values in dcol order (bit-identical to the CBM's
+      // values: +-row_scale[col], validated by plan_layout)
+      std::vector<float> dval(L.dcol.size());
+      for (size_t k = 0; k < dval.size(); ++k) {
+        const float sc = L.scale[L.dcol[k] & 0x7FFFFFFFu];
+        dval[k] = (L.dcol[k] >> 31) ? -sc : sc;
+      }
+      put(h->dval, dval, "upload dval");
     }
     int coop = 0;
     ck(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev), "attr");
@@ -1066,7 +1084,7 @@ void device_free(DeviceMatrix* h) {
     cudaFree(kv.second.list);
     cudaFree(kv.second.wstart);
   }
-  for (void* p : {(void*)h->dcol, (void*)h->rec, (void*)h->srow, (void*)h->scale,
+  for (void* p : {(void*)h->dcol, (void*)h->dval, (void*)h->rec, (void*)h->srow, (void*)h->scale,
                   (void*)h->flags, (void*)h->partial,
                   (void*)h->interior, (void*)h->xs, (void*)h->xstage, (void*)h->ystage})
     if (p) cudaFree(p);
@@ -1145,6 +1163,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   p.rec = reinterpret_cast<const uint4*>(h->rec);
   p.srow = h->srow;
   p.dcol = h->dcol;
+  p.dval = h->dval;
   p.scale = h->scale;
   p.x = xin;
   p.ldx = ldin;

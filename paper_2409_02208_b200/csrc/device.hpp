@@ -24,6 +24,7 @@ struct DeviceMatrix {
   cbm_b200_options opt{};
   // structure (immutable)
   uint32_t* dcol = nullptr;
+  float* dval = nullptr;  // normalized: signed delta values in dcol order
   uint32_t* rec = nullptr;
   float* srow = nullptr;
   float* scale = nullptr;
