@@ -47,7 +47,7 @@ def parse():
                     help="bounded CPU-baseline sample (seconds of reference work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order-faithful", action="store_true")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "register", "scalar"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "scalar"])
     ap.add_argument("--no-csr-comparator", action="store_true",
                     help="skip timing the uncompressed (CSR) matrix with the same kernel")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)

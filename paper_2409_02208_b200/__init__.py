@@ -388,7 +388,9 @@ class DeviceCbm:
         opt.split_threshold = split_threshold
         opt.chunk = chunk
         opt.prescale = prescale
-        opt.kernel = {"auto": 0, "scalar": 1, "register": 2}[kernel]
+        if kernel not in ("auto", "scalar"):
+            raise ValueError("kernel must be 'auto' or 'scalar'")
+        opt.kernel = {"auto": 0, "scalar": 1}[kernel]
         opt.max_segments = max_segments
         opt.flatten_gain = flatten_gain
         opt.prefetch = int(prefetch)

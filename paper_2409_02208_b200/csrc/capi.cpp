@@ -207,6 +207,8 @@ int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
     cbm_b200_options o;
     cbm_b200_default_options(&o);
     if (opt) o = *opt;
+    need(o.kernel == 0 || o.kernel == 1, "upload: options.kernel must be 0 (auto) or 1 (scalar)");
+    need(o.max_segments >= 0 && o.max_segments <= 4, "upload: options.max_segments must be 0..4");
     auto* h = new cbm_b200_matrix{nullptr};
     try {
       h->d = cbmb::device_upload(*c, o);

@@ -33,6 +33,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <string>
 
 #include "device.hpp"
@@ -134,8 +136,6 @@ __device__ __forceinline__ void await(const uint32_t* f, uint32_t epoch) {
 }
 
 struct Params {
-  const uint4* __restrict__ rec;      // 2 x uint4 per item (layout.hpp)
-  const float* __restrict__ srow;     // per item: its row's scale (normalized)
   const uint32_t* __restrict__ dcol;
   const float* __restrict__ dval;     // per delta: +-row_scale[col] (normalized), dcol order
   const float* __restrict__ scale;    // per column scale (normalized, per-delta products)
@@ -146,14 +146,21 @@ struct Params {
   float* partial;   // CHUNK / MERGE partial sums, stride dpad
   float* interior;  // unscaled interior rows (normalized), stride dpad
   uint32_t* flags;
-  const uint32_t* __restrict__ sched;   // tickets grouped by warp (host list schedule)
-  const uint32_t* __restrict__ wstart;  // per warp: offset of its tickets in sched (+1 entry)
+  const uint4* __restrict__ trec;  // per warp: wstride ticket records (3 x uint4), in order
+  uint32_t wstride;                 // records per warp region
   uint32_t n_items, n_chunk, d, dpad;
   uint32_t total_tickets, total_warps, epoch;
   uint32_t cta_stride;  // CTAs per residency round (grid / CTAs per SM)
   uint32_t relu;        // fused ReLU on Y (relu_inplace, dense.cpp:51-54) for the GCN
   uint64_t prefetch_bytes;  // > 0: X is one contiguous block of this size, pulled into L2 first
+  unsigned long long* trace;  // dev tool (CBM_B200_TRACE): 4 x u64 per warp, else null
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Every warp streams its share of a contiguous X into L2 with bulk prefetches
 // (sequential HBM reads at full bandwidth instead of first-touch random misses
@@ -272,39 +279,35 @@ __device__ __forceinline__ typename Vec<V>::T fma_sign(typename Vec<V>::T acc,
 constexpr int kWarpsPerCta = 4;
 constexpr uint32_t kRecWin = 64;  // ticket records staged per warp (two groups of 32)
 
-// One ticket's record in shared memory (2 x 16 bytes) + its item and slab.
+// One ticket's record (3 x 16 bytes), as stored in the warp's region of the
+// ticket stream and staged in shared memory: the item's layout record, the
+// ticket's item and column slab, the row scale, and (first record of a region
+// only) the warp's ticket count.
 struct alignas(16) TRec {
   uint32_t beg, end, rowk, ppos;
   uint32_t psrc, first, cnt, slot;
+  uint32_t item, slab, srow, nw;
 };
 
-template <int V, int U, int D, bool NORM>
+template <int V, int U, int D>
 struct alignas(16) WarpSmem {
-  float ring[D][U][32 * V];        // slot s, segment u, lane l: [s][u][l*V, l*V+V)
-  TRec rec[kRecWin];               // warp-sequence tickets [g, g+64), slot i & 63
-  uint32_t item[kRecWin];          // item index of the staged ticket
-  uint32_t slab[kRecWin];          // column slab of the staged ticket
-  float srow[NORM ? kRecWin : 1];  // row scale per staged ticket
+  float ring[D][U][32 * V];  // slot s, segment u, lane l: [s][u][l*V, l*V+V)
+  TRec rec[kRecWin];         // warp-sequence tickets [g, g+64), slot i & 63
 };
 
-// Stage the records of warp-sequence tickets [i0, i0+32) of this warp's list.
+// Stage the records of warp-sequence tickets [i0, i0+32). Regions are padded
+// (zero records past a warp's count, 64 more after the last region), so the
+// loads need no bound: one dependent hop from the kernel start to the records.
 template <class SM>
-__device__ __forceinline__ void stage_recs(const Params& p, SM& sm, uint32_t wbase, uint32_t i0,
-                                           uint32_t n_w, bool norm) {
+__device__ __forceinline__ void stage_recs(const Params& p, SM& sm, uint32_t w, uint32_t i0) {
   const int lane = threadIdx.x & 31;
   const uint32_t i = i0 + uint32_t(lane);
-  if (i < n_w) {
-    const uint32_t T = __ldg(p.sched + wbase + i);
-    const uint32_t sl = T / p.n_items;
-    const uint32_t t = T - sl * p.n_items;
-    const uint32_t k = i & (kRecWin - 1);
-    TRec& r = sm.rec[k];
-    *reinterpret_cast<uint4*>(&r.beg) = __ldg(p.rec + 2 * (size_t)t);
-    *reinterpret_cast<uint4*>(&r.psrc) = __ldg(p.rec + 2 * (size_t)t + 1);
-    sm.item[k] = t;
-    sm.slab[k] = sl;
-    if (norm) sm.srow[k] = __ldg(p.srow + t);
-  }
+  const uint4* src = p.trec + 3 * ((size_t)w * p.wstride + i);
+  uint4* dst = reinterpret_cast<uint4*>(&sm.rec[i & (kRecWin - 1)]);
+  const uint4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
+  dst[0] = a;
+  dst[1] = b;
+  dst[2] = c;
 }
 
 // SC: how a delta value enters stage 1.
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   constexpr int B = (D >= 8 && U >= 2) ? 4 : 2;  // deltas consumed per wait (measured)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  using SM = WarpSmem<V, U, D, NORM>;
+  using SM = WarpSmem<V, U, D>;
   SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
   // warp -> position in the round-robin: CTAs b, b+G, b+2G, ... (G = p.cta_stride,
   // one per SM) share an SM, so consecutive tickets (adjacent rows, similar
@@ -331,15 +334,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   const uint32_t w = (cta % p.cta_stride) * (p.total_warps / p.cta_stride) +
                      (cta / p.cta_stride) * kWarpsPerCta + wi;
   if (w >= p.total_warps) return;
+  const unsigned long long t_start = p.trace ? globaltimer() : 0ull;
   prefetch_x(p, w);
-  const uint32_t wbase = __ldg(p.wstart + w);
-  const uint32_t n_w = __ldg(p.wstart + w + 1) - wbase;  // this warp's tickets, increasing
-  if (n_w == 0) return;
-
   uint32_t g = 0;  // staged records cover warp-sequence tickets [g, g + 64)
-  stage_recs(p, sm, wbase, 0, n_w, NORM);
-  stage_recs(p, sm, wbase, 32, n_w, NORM);
+  stage_recs(p, sm, w, 0);
+  stage_recs(p, sm, w, 32);
   __syncwarp();
+  const uint32_t n_w = sm.rec[0].nw;  // this warp's tickets (increasing ticket order)
+  if (n_w == 0) return;
   auto R = [&](uint32_t i) -> const TRec& { return sm.rec[i & (kRecWin - 1)]; };
   // 32 column words (and values) of a delta block: lane j holds delta k0 + j
   struct Wd {
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     const TRec& r = R(ii);
     ibeg = r.beg;
     ilen = r.end - r.beg;
-    icol = sm.slab[ii & (kRecWin - 1)] * kSlab + uint32_t(lane) * V;
+    icol = r.slab * kSlab + uint32_t(lane) * V;
     imask = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -433,11 +435,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   for (int q = 0; q < D; ++q) issue_one();
 
   uint32_t cseq = 0;  // deltas consumed
+  unsigned long long t_first = 0ull;
 #pragma unroll 1
   for (uint32_t ci = 0; ci < n_w; ++ci) {
     if (ci - g == 32) {  // slide the record window by one group
       __syncwarp();
-      stage_recs(p, sm, wbase, g + kRecWin, n_w, NORM);
+      stage_recs(p, sm, w, g + kRecWin);
       g += 32;
       __syncwarp();
       if (iblocked) {
@@ -447,7 +450,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     }
     const uint32_t k_ci = ci & (kRecWin - 1);
     const TRec r = sm.rec[k_ci];
-    const uint32_t slab = sm.slab[k_ci], t = sm.item[k_ci];
+    const uint32_t slab = r.slab, t = r.item;
     const uint32_t col = slab * kSlab + uint32_t(lane) * V;
     T4 acc[U];
 #pragma unroll
@@ -458,6 +461,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
 #pragma unroll 1
     for (; k + B <= r.end; k += B) {
       cp_wait<D - B>();  // this lane's copies of deltas cseq .. cseq+B-1 have landed
+      if (p.trace && t_first == 0ull) t_first = globaltimer();
       // Segments outside the matrix read stale ring bytes into accumulators
       // that are never stored: no per-segment branch on the hot path.
       float sc[B];
@@ -530,7 +534,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
           if (col + uint32_t(u) * kSeg < p.d) W::st(dst + col + u * kSeg, acc[u]);
         publish(flag_base + t, p.epoch);
       }
-      const float sr = sm.srow[k_ci];
+      const float sr = __uint_as_float(r.srow);
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (col + uint32_t(u) * kSeg < p.d) {
@@ -546,194 +550,40 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     }
   }
   cp_wait<0>();  // no copy may target shared memory after exit
+  if (p.trace && lane == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    unsigned long long* o = p.trace + 4 * (size_t)w;
+    o[0] = t_start;
+    o[1] = t_first;
+    o[2] = globaltimer();
+    o[3] = (unsigned long long)smid | ((unsigned long long)n_w << 16) |
+           ((unsigned long long)cseq << 32);
+  }
 }
 
-// ------------------------------------------------------------ register kernel
-// Same schedule, records and epilogues as cbm_kernel; the X rows are staged in
-// registers instead: deltas are taken in groups of G, the group after the
-// current one (possibly the first group of the warp's next ticket) is loaded
-// while the current one is summed (two register buffers), the delta's sign is
-// applied with one XOR per float (fl(a + (-x)) == fl(a - x)), and column bounds
-// are resolved once per ticket. ~20 instructions per delta and segment.
-template <int V, int U, bool NORM, bool SCALE>
-struct alignas(16) RegSmem {
-  TRec rec[kRecWin];
-  uint32_t item[kRecWin];
-  uint32_t slab[kRecWin];
-  float srow[NORM ? kRecWin : 1];
-};
-
-template <int V, int U, int G, bool NORM, bool SCALE>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_rkernel(const Params p) {
-  using W = Vec<V>;
-  using T4 = typename W::T;
-  constexpr uint32_t kSeg = 32u * V;
-  constexpr uint32_t kSlab = kSeg * U;
-  constexpr int PFp = U >= 4 ? 2 : (U == 2 ? 4 : 8);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31;
-  using SM = RegSmem<V, U, NORM, SCALE>;
-  SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
-  const uint32_t cta = blockIdx.x, wi = threadIdx.x >> 5;
-  const uint32_t w = (cta % p.cta_stride) * (p.total_warps / p.cta_stride) +
-                     (cta / p.cta_stride) * kWarpsPerCta + wi;
-  if (w >= p.total_warps) return;
-  prefetch_x(p, w);
-  const uint32_t wbase = __ldg(p.wstart + w);
-  const uint32_t n_w = __ldg(p.wstart + w + 1) - wbase;
-  if (n_w == 0) return;
-
-  uint32_t g = 0;
-  stage_recs(p, sm, wbase, 0, n_w, NORM);
-  stage_recs(p, sm, wbase, 32, n_w, NORM);
-  __syncwarp();
-  auto window = [&](uint32_t i) -> uint32_t {
-    if (i >= n_w || i >= g + kRecWin) return 0u;
-    const TRec& r = sm.rec[i & (kRecWin - 1)];
-    return r.beg + lane < r.end ? __ldg(p.dcol + r.beg + lane) : 0u;
-  };
-  // a ticket as the loader sees it
-  struct Tk {
-    uint32_t beg, len, win;
-    const float* xcol;  // this lane's column base for segment 0
-    uint32_t umask;     // bit u: segment u inside the matrix
-  };
-  auto ticket = [&](uint32_t i, uint32_t win) {
-    Tk t;
-    const TRec& r = sm.rec[i & (kRecWin - 1)];
-    t.beg = r.beg;
-    t.len = i < n_w ? r.end - r.beg : 0u;
-    t.win = win;
-    const uint32_t col = sm.slab[i & (kRecWin - 1)] * kSlab + uint32_t(lane) * V;
-    t.xcol = p.x + col;
-    t.umask = 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (col + uint32_t(u) * kSeg < p.d) t.umask |= 1u << u;
-    return t;
-  };
-  // load group q of ticket t into (buf, cw, sc)
-  auto load = [&](T4 (&buf)[G][U], uint32_t (&cw)[G], float (&sc)[G], const Tk& t, uint32_t q) {
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const uint32_t k = q * G + j;
-      const uint32_t fromw = __shfl_sync(kFull, t.win, k & 31);
-      uint32_t c = 0;
-      if (k < t.len) c = k < 32 ? fromw : __ldg(p.dcol + t.beg + k);
-      cw[j] = c;
-      const float* row = t.xcol + (long long)(c & 0x7FFFFFFFu) * p.ldx;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        buf[j][u] = (k < t.len && (t.umask >> u) & 1u) ? W::ldg(row + u * kSeg) : W::zero();
-      if constexpr (SCALE) sc[j] = k < t.len ? __ldg(p.scale + (c & 0x7FFFFFFFu)) : 0.0f;
-    }
-  };
-  auto consume = [&](const T4 (&buf)[G][U], const uint32_t (&cw)[G], const float (&sc)[G],
-                     uint32_t len, uint32_t q, T4 (&acc)[U]) {
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      if (q * G + j < len) {
-        const uint32_t m = cw[j] & 0x80000000u;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          T4 v = buf[j][u];
-          if constexpr (SCALE) v = W::mul(v, sc[j]);
-          acc[u] = W::add(acc[u], xor_sign<V>(v, m));
-        }
+// Gathers each warp's ticket records into its region of the ticket stream.
+__global__ void build_ticket_stream(const uint4* __restrict__ rec, const float* __restrict__ srow,
+                                    const uint32_t* __restrict__ list,
+                                    const uint32_t* __restrict__ wstart, uint32_t n_items,
+                                    uint32_t warps, uint32_t stride, uint64_t n_rec,
+                                    TRec* __restrict__ out) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n_rec;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    TRec r{};
+    const uint64_t w = k / stride, i = k - w * stride;
+    if (w < warps) {
+      const uint32_t lo = wstart[w], n = wstart[w + 1] - lo;
+      if (i < n) {
+        const uint32_t T = list[lo + i];
+        const uint32_t sl = T / n_items, t = T - sl * n_items;
+        const uint4 a = rec[2 * (size_t)t], b = rec[2 * (size_t)t + 1];
+        r = TRec{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w,
+                 t, sl, srow ? __float_as_uint(srow[t]) : 0u, 0u};
       }
+      if (i == 0) r.nw = n;
     }
-  };
-
-  T4 bufA[G][U], bufB[G][U];
-  uint32_t cwA[G], cwB[G];
-  float scA[G], scB[G];
-  uint32_t wn1 = window(1), wn2 = window(2);
-  Tk cur = ticket(0, window(0));
-  Tk nxt = ticket(1, wn1);
-  load(bufA, cwA, scA, cur, 0);
-  bool in_a = true;  // the group about to be consumed sits in bufA
-#pragma unroll 1
-  for (uint32_t ci = 0; ci < n_w; ++ci) {
-    const uint32_t k_ci = ci & (kRecWin - 1);
-    const TRec r = sm.rec[k_ci];
-    const uint32_t slab = sm.slab[k_ci], t = sm.item[k_ci];
-    const uint32_t col = slab * kSlab + uint32_t(lane) * V;
-    const uint32_t ng = cur.len ? (cur.len + G - 1) / G : 1u;
-    T4 acc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = W::zero();
-#pragma unroll 1
-    for (uint32_t q = 0; q < ng; ++q) {
-      const bool last = q + 1 == ng;
-      if (in_a) {
-        if (!last) load(bufB, cwB, scB, cur, q + 1);
-        else load(bufB, cwB, scB, nxt, 0);
-        consume(bufA, cwA, scA, cur.len, q, acc);
-      } else {
-        if (!last) load(bufA, cwA, scA, cur, q + 1);
-        else load(bufA, cwA, scA, nxt, 0);
-        consume(bufB, cwB, scB, cur.len, q, acc);
-      }
-      in_a = !in_a;
-    }
-    // ---- epilogue (stages 2 + 3) while the next ticket's first group is in flight
-    uint32_t* flag_base = p.flags + (size_t)slab * p.n_items;
-    if (r.cnt) add_partials<V, U, PFp>(p, flag_base, r.first, r.cnt, col, acc);
-    if (t < p.n_chunk) {
-      float* dst = p.partial + (size_t)t * p.dpad;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if ((cur.umask >> u) & 1u) W::st(dst + col + u * kSeg, acc[u]);
-      publish(flag_base + t, p.epoch);
-    } else {
-      if (r.ppos != 0xFFFFFFFFu) {  // + unscaled parent row
-        await(flag_base + r.ppos, p.epoch);
-        const float* src =
-            NORM ? p.interior + (size_t)r.psrc * p.dpad : p.y + (long long)r.psrc * p.ldy;
-        T4 pv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          pv[u] = ((cur.umask >> u) & 1u) ? W::ldcg(src + col + u * kSeg) : W::zero();
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc[u] = W::add(acc[u], pv[u]);
-      }
-      const uint32_t row = r.rowk & 0x7FFFFFFFu;
-      const bool is_parent = (r.rowk >> 31) != 0;
-      float* yrow = p.y + (long long)row * p.ldy;
-      if constexpr (NORM) {
-        if (is_parent) {
-          float* dst = p.interior + (size_t)r.slot * p.dpad;
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if ((cur.umask >> u) & 1u) W::st(dst + col + u * kSeg, acc[u]);
-          publish(flag_base + t, p.epoch);
-        }
-        const float sr = sm.srow[k_ci];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if ((cur.umask >> u) & 1u) {
-            T4 yv = W::mul(acc[u], sr);
-            if (p.relu) yv = relu_v<V>(yv);
-            W::st(yrow + col + u * kSeg, yv);
-          }
-      } else {
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if ((cur.umask >> u) & 1u) W::st(yrow + col + u * kSeg, p.relu ? relu_v<V>(acc[u]) : acc[u]);
-        if (is_parent) publish(flag_base + t, p.epoch);
-      }
-    }
-    // ---- advance: record window, index windows
-    if (ci + 1 - g == 32 && ci + 1 < n_w) {
-      __syncwarp();
-      stage_recs(p, sm, wbase, g + kRecWin, n_w, NORM);
-      g += 32;
-      __syncwarp();
-    }
-    cur = nxt;
-    wn1 = wn2;
-    wn2 = window(ci + 3);
-    nxt = ticket(ci + 2, wn1);
+    out[k] = r;
   }
 }
 
@@ -783,73 +633,46 @@ const DeviceMatrix::Schedule& schedule_for(DeviceMatrix* h, uint32_t warps, uint
       std::push_heap(heap.begin(), heap.end(), later);
     }
   }
-  for (uint32_t w = 0; w < warps; ++w) count[w + 1] += count[w];
+  uint32_t most = 0;
+  for (uint32_t w = 0; w < warps; ++w) {
+    most = std::max(most, count[w + 1]);
+    count[w + 1] += count[w];
+  }
   std::vector<uint32_t> list(total);
   {
     std::vector<uint32_t> pos(count.begin(), count.end() - 1);
     for (uint64_t T = 0; T < total; ++T) list[pos[owner[T]]++] = uint32_t(T);
   }
+  // the ticket stream: warp w's records at [w * stride, w * stride + count_w),
+  // zero records after them and 64 more after the last region
   DeviceMatrix::Schedule sc;
+  sc.wstride = std::max<uint32_t>(32, (most + 31) & ~31u);
+  const uint64_t n_rec = uint64_t(warps) * sc.wstride + kRecWin;
+  uint32_t *d_list = nullptr, *d_start = nullptr;
   try {
-    ck(cudaMalloc(&sc.list, std::max<uint64_t>(total, 1) * sizeof(uint32_t)), "schedule");
-    ck(cudaMalloc(&sc.wstart, count.size() * sizeof(uint32_t)), "schedule");
-    // synchronous copies: the schedule is built once per (warps, slabs)
-    ck(cudaMemcpy(sc.list, list.data(), total * sizeof(uint32_t), cudaMemcpyHostToDevice),
+    ck(cudaMalloc(&sc.trec, n_rec * sizeof(TRec)), "schedule");
+    ck(cudaMalloc(&d_list, std::max<uint64_t>(total, 1) * sizeof(uint32_t)), "schedule");
+    ck(cudaMalloc(&d_start, count.size() * sizeof(uint32_t)), "schedule");
+    ck(cudaMemcpyAsync(d_list, list.data(), total * sizeof(uint32_t), cudaMemcpyHostToDevice, s),
        "schedule upload");
-    ck(cudaMemcpy(sc.wstart, count.data(), count.size() * sizeof(uint32_t),
-                  cudaMemcpyHostToDevice),
+    ck(cudaMemcpyAsync(d_start, count.data(), count.size() * sizeof(uint32_t),
+                       cudaMemcpyHostToDevice, s),
        "schedule upload");
+    const int grid = int(std::min<uint64_t>((n_rec + 255) / 256, uint64_t(h->num_sms) * 32));
+    build_ticket_stream<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(h->rec), h->srow,
+                                             d_list, d_start, L.n_items, warps, sc.wstride,
+                                             n_rec, reinterpret_cast<TRec*>(sc.trec));
+    ck(cudaGetLastError(), "schedule build");
+    ck(cudaStreamSynchronize(s), "schedule build");  // the host vectors go out of scope
   } catch (...) {
-    if (sc.list) cudaFree(sc.list);
-    if (sc.wstart) cudaFree(sc.wstart);
+    if (sc.trec) cudaFree(sc.trec);
+    cudaFree(d_list);
+    cudaFree(d_start);
     throw;
   }
-  (void)s;
+  cudaFree(d_list);
+  cudaFree(d_start);
   return h->schedules.emplace(key, sc).first->second;
-}
-
-template <int V, int U, int G, bool NORM, bool SCALE>
-void launch_reg(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
-  constexpr size_t smem = kWarpsPerCta * sizeof(RegSmem<V, U, NORM, SCALE>);
-  static int bps = -1;
-  if (bps < 0) {
-    ck(cudaFuncSetAttribute(cbm_rkernel<V, U, G, NORM, SCALE>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-       "smem attribute");
-    int b = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_rkernel<V, U, G, NORM, SCALE>,
-                                                     kWarpsPerCta * 32, smem),
-       "occupancy");
-    bps = std::max(1, b);
-  }
-  constexpr uint64_t wpb = kWarpsPerCta;
-  const uint64_t cap = uint64_t(h->num_sms) * bps * wpb;
-  const uint64_t warps = std::max<uint64_t>(1, std::min(cap, tickets));
-  int grid = int((warps + wpb - 1) / wpb);
-  const int per_sm = std::max(1, (grid + h->num_sms - 1) / h->num_sms);
-  p.cta_stride = uint32_t((grid + per_sm - 1) / per_sm);
-  grid = int(p.cta_stride) * per_sm;
-  if (uint64_t(grid) > uint64_t(h->num_sms) * bps) {
-    p.cta_stride = uint32_t(grid / per_sm);
-    grid = int(p.cta_stride) * per_sm;
-  }
-  p.total_warps = uint32_t(grid * wpb);
-  const auto& sc = schedule_for(h, p.total_warps, slabs, s);
-  p.sched = sc.list;
-  p.wstart = sc.wstart;
-  void* args[] = {&p};
-  ck(cudaLaunchCooperativeKernel(
-         reinterpret_cast<const void*>(&cbm_rkernel<V, U, G, NORM, SCALE>), dim3(grid),
-         dim3(kWarpsPerCta * 32), args, smem, s),
-     "cbm_rkernel cooperative launch");
-}
-
-template <int V, int U, int G>
-void run_reg(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl, DeviceMatrix* h,
-             cudaStream_t s) {
-  if (!norm) launch_reg<V, U, G, false, false>(p, tickets, slabs, h, s);
-  else if (scl) launch_reg<V, U, G, true, true>(p, tickets, slabs, h, s);
-  else launch_reg<V, U, G, true, false>(p, tickets, slabs, h, s);
 }
 
 // xs[c, :] = row_scale[c] (*) x[c, :] — the bit-identical products of the
@@ -869,7 +692,7 @@ __global__ void prescale_kernel(const float* __restrict__ x, long long ldx,
 // more warps than tickets.
 template <int V, int U, int D, bool NORM, int SC>
 void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
-  constexpr size_t smem = kWarpsPerCta * sizeof(WarpSmem<V, U, D, NORM>);
+  constexpr size_t smem = kWarpsPerCta * sizeof(WarpSmem<V, U, D>);
   static int bps = -1;  // per template instance
   if (bps < 0) {
     ck(cudaFuncSetAttribute(cbm_kernel<V, U, D, NORM, SC>,
@@ -896,8 +719,8 @@ void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cu
   }
   p.total_warps = uint32_t(grid * wpb);
   const auto& sc = schedule_for(h, p.total_warps, slabs, s);
-  p.sched = sc.list;
-  p.wstart = sc.wstart;
+  p.trec = reinterpret_cast<const uint4*>(sc.trec);
+  p.wstride = sc.wstride;
   void* args[] = {&p};
   ck(cudaLaunchCooperativeKernel(
          reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SC>), dim3(grid),
@@ -1080,10 +903,7 @@ void device_free(DeviceMatrix* h) {
     for (auto e : h->ev) cudaEventDestroy(e);
   }
   if (h->gcn_h) cudaFree(h->gcn_h);
-  for (auto& kv : h->schedules) {
-    cudaFree(kv.second.list);
-    cudaFree(kv.second.wstart);
-  }
+  for (auto& kv : h->schedules) cudaFree(kv.second.trec);
   for (void* p : {(void*)h->dcol, (void*)h->dval, (void*)h->rec, (void*)h->srow, (void*)h->scale,
                   (void*)h->flags, (void*)h->partial,
                   (void*)h->interior, (void*)h->xs, (void*)h->xstage, (void*)h->ystage})
@@ -1145,7 +965,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   }
   // lanes x V floats per column slab: V = 4 (LDG.128) when rows are 16-byte
   // aligned multiples, else 2 or 1; kernel option 1 forces scalar lanes
-  const uint32_t V = h->opt.kernel == 1 ? 1u : pick_vec(d, xin, ldin, y, ldy);  // 2: register kernel
+  const uint32_t V = h->opt.kernel == 1 ? 1u : pick_vec(d, xin, ldin, y, ldy);
   // segments of 32*V columns per ticket: wide X shares one ticket's record,
   // indices and epilogue across up to 4 segments ...
   const uint32_t segs = (d + 32 * V - 1) / (32 * V);
@@ -1160,8 +980,6 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     h->epoch = 1;
   }
   Params p;
-  p.rec = reinterpret_cast<const uint4*>(h->rec);
-  p.srow = h->srow;
   p.dcol = h->dcol;
   p.dval = h->dval;
   p.scale = h->scale;
@@ -1190,21 +1008,17 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
                          : 0;
 
   const bool norm = L.normalized, scl = L.normalized && !prescale;
-  if (h->opt.kernel == 2) {  // register-staged group pipeline
-    if (V == 4) {
-      if (U == 4) run_reg<4, 4, 2>(p, tickets, n_slabs, norm, scl, h, s);
-      else if (U == 2) run_reg<4, 2, 4>(p, tickets, n_slabs, norm, scl, h, s);
-      else run_reg<4, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);
-    } else if (V == 2) {
-      if (U == 4) run_reg<2, 4, 4>(p, tickets, n_slabs, norm, scl, h, s);
-      else if (U == 2) run_reg<2, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
-      else run_reg<2, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);
-    } else {
-      if (U == 4) run_reg<1, 4, 8>(p, tickets, n_slabs, norm, scl, h, s);
-      else if (U == 2) run_reg<1, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
-      else run_reg<1, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);
-    }
-  } else if (V == 4) {
+  // dev tool: CBM_B200_TRACE=<file> appends per-warp timestamps of every call
+  const char* trace_path = std::getenv("CBM_B200_TRACE");
+  unsigned long long* trace = nullptr;
+  const size_t trace_n = size_t(h->num_sms) * 64 * 4;
+  p.trace = nullptr;
+  if (trace_path) {
+    ck(cudaMalloc(&trace, trace_n * 8), "trace");
+    ck(cudaMemsetAsync(trace, 0, trace_n * 8, s), "trace");
+    p.trace = trace;
+  }
+  if (V == 4) {
     if (U == 4) run_kernel<4, 4, 4>(p, tickets, n_slabs, norm, scl, h, s);
     else if (U == 2) run_kernel<4, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
     else run_kernel<4, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);
@@ -1219,6 +1033,19 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   }
   ck(cudaGetLastError(), "cbm_kernel launch");
   ++h->last_launches;
+  if (trace) {
+    std::vector<unsigned long long> t(trace_n);
+    ck(cudaStreamSynchronize(s), "trace");
+    ck(cudaMemcpy(t.data(), trace, trace_n * 8, cudaMemcpyDeviceToHost), "trace");
+    cudaFree(trace);
+    if (FILE* f = std::fopen(trace_path, "a")) {
+      std::fprintf(f, "call warps=%u tickets=%llu\n", p.total_warps, (unsigned long long)tickets);
+      for (uint32_t w = 0; w < p.total_warps; ++w)
+        std::fprintf(f, "%u %llu %llu %llu %llu\n", w, t[4 * w], t[4 * w + 1], t[4 * w + 2],
+                     t[4 * w + 3]);
+      std::fclose(f);
+    }
+  }
 }
 
 // Host-buffer entry point. Columns are independent (kernels.cpp:27-62), so X
@@ -1238,10 +1065,12 @@ void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, voi
     for (auto& e : h->ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   }
   const uint64_t bytes = (uint64_t(L.n_cols) + L.n_rows) * d * sizeof(float);
+  // column chunks of >= 64 floats (256-byte rows keep the 2D copies at ~53 GB/s;
+  // tools/ubench_pcie.cu): more chunks shorten the exposed first H2D / last D2H
   uint32_t chunks = 1;
-  if (bytes >= (8u << 20) && d >= 256) chunks = std::min<uint32_t>(4, d / 128);
+  if (bytes >= (8u << 20) && d >= 128) chunks = std::min<uint32_t>(kHostChunks, d / 64);
   const uint32_t cw = ((d + chunks - 1) / chunks + 3) & ~3u;  // chunk width, 16-byte aligned
-  // ev[0]: caller's prior work on s; ev[1+k]: X chunk k landed; ev[5+k]: Y chunk k ready
+  // ev[0]: caller's prior work on s; ev[1+k]: X chunk k landed; ev[1+C+k]: Y chunk k ready
   ck(cudaEventRecord(h->ev[0], s), "event");
   ck(cudaStreamWaitEvent(h->s_in, h->ev[0], 0), "wait");
   ck(cudaStreamWaitEvent(h->s_out, h->ev[0], 0), "wait");
@@ -1258,8 +1087,8 @@ void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, voi
     ck(cudaStreamWaitEvent(s, h->ev[1 + k], 0), "wait");
     device_spmm(h, h->xstage + c0, dpad, w, h->ystage + c0, dpad, stream, false);
     launches += h->last_launches;
-    ck(cudaEventRecord(h->ev[5 + k], s), "event");
-    ck(cudaStreamWaitEvent(h->s_out, h->ev[5 + k], 0), "wait");
+    ck(cudaEventRecord(h->ev[1 + kHostChunks + k], s), "event");
+    ck(cudaStreamWaitEvent(h->s_out, h->ev[1 + kHostChunks + k], 0), "wait");
     ck(cudaMemcpy2DAsync(y + c0, d * sizeof(float), h->ystage + c0, dpad * sizeof(float),
                          w * sizeof(float), L.n_rows, cudaMemcpyDeviceToHost, h->s_out),
        "D2H Y");

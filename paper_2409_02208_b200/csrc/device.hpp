@@ -16,6 +16,8 @@
 
 namespace cbmb {
 
+inline constexpr uint32_t kHostChunks = 8;  // column chunks of the host-buffer pipeline
+
 struct DeviceMatrix {
   int device = 0;
   int num_sms = 148;
@@ -46,11 +48,11 @@ struct DeviceMatrix {
   uint64_t ystage_cap = 0;
   // host-API pipeline: copy-in / copy-out streams and chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t ev[9] = {};
+  cudaEvent_t ev[1 + 2 * kHostChunks] = {};
   // static ticket -> warp schedules (cbm_kernel), one per (warps, slabs)
   struct Schedule {
-    uint32_t* list = nullptr;    // tickets, grouped by warp, increasing inside a warp
-    uint32_t* wstart = nullptr;  // warps + 1 offsets into list
+    void* trec = nullptr;    // ticket stream: per warp, its records in increasing order
+    uint32_t wstride = 0;    // records per warp region
   };
   std::map<uint64_t, Schedule> schedules;
   std::vector<uint32_t> item_dep;  // per item: parent item (ppos), first partial, count

@@ -114,7 +114,7 @@ def _suite(normalized, n_cases, seed0):
         yield k, c, x
 
 
-@pytest.mark.parametrize("kernel", ["auto", "scalar", "register"])
+@pytest.mark.parametrize("kernel", ["auto", "scalar"])
 @pytest.mark.parametrize("normalized", [False, True])
 def test_random_suite_bitwise(normalized, kernel, dev):
     """Reference suites (test_kernels.cpp:75-114 style, all d paths, all kernel
@@ -150,7 +150,7 @@ def test_flattened_rows(normalized, dev):
                 assert normwise_err(got, want) <= TOL
 
 
-@pytest.mark.parametrize("kernel", ["auto", "register"])
+@pytest.mark.parametrize("kernel", ["auto", "scalar"])
 @pytest.mark.parametrize("normalized", [False, True])
 def test_split_rows_integer_bitexact_and_gaussian_tolerance(normalized, kernel, dev):
     """Force every long row through the CHUNK path (split_threshold=4, chunk=2)."""
@@ -232,12 +232,12 @@ def test_cfg0_full_size_integer_bitexact(dev):
     x = P.generate_dense("int", 4096, 64, 0xC0F61000, -8, 8)
     want = O.oracle_spmm(oracle_arrays(c), x)
     for faithful in (True, False):
-        for kernel in ("auto", "scalar", "register"):
+        for kernel in ("auto", "scalar"):
             got, _ = gpu_spmm(c, x, dev, order_faithful=faithful, kernel=kernel)
             assert_bitwise(got, want, f"cfg0 faithful={faithful} kernel={kernel}")
 
 
-@pytest.mark.parametrize("kernel", ["auto", "scalar", "register"])
+@pytest.mark.parametrize("kernel", ["auto", "scalar"])
 def test_cfg1_full_size_gaussian(kernel, dev):
     """cfg[1]: n=19,717 normalized, X N(0,1), d=512: order-faithful is
     bit-exact, the default split mode within 1e-5 normwise."""
