@@ -322,7 +322,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   constexpr uint32_t kSlab = kSeg * U;    // floats per ticket
   constexpr int PFp = U >= 4 ? 2 : (U == 2 ? 4 : 8);
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
-  constexpr int B = (D >= 8 && U >= 2) ? 4 : 2;  // deltas consumed per wait (measured)
+  // deltas per ring group: copies are issued, committed and awaited B at a
+  // time (a group never spans two tickets; its unused slots stay idle)
+  constexpr int B = D >= 8 ? 4 : 2;
+  constexpr int G = D / B;  // groups in flight
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   using SM = WarpSmem<V, U, D>;
@@ -404,21 +407,27 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       }
     }
   };
-  auto issue_one = [&]() {
+  auto issue_group = [&]() {
     if (!iblocked && ii < n_w) {
-      const uint32_t cw = __shfl_sync(kFull, win.c, iq & 31);
-      const uint32_t c = cw & 0x7FFFFFFFu;
-      const uint32_t s = iseq & (D - 1);
-      const float* src = p.x + (long long)c * p.ldx + icol;
+      const uint32_t n = min(uint32_t(B), ilen - iq);
+      const uint32_t s0 = iseq & (D - 1);  // a multiple of B
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if ((imask >> u) & 1u) cp_async<V>(&sm.ring[s][u][lane * V], src + u * kSeg);
-      float val;  // the delta's signed value (the reference's values[k], kernels.cpp:33)
-      if constexpr (SC != 0) val = __shfl_sync(kFull, win.v, iq & 31);
-      else val = __int_as_float(0x3F800000u | (cw & 0x80000000u));
-      if (uint32_t(lane) == s) vring = val;
-      ++iseq;
-      ++iq;
+      for (int b = 0; b < B; ++b) {
+        if (uint32_t(b) < n) {
+          const uint32_t cw = __shfl_sync(kFull, win.c, (iq + b) & 31);
+          const float* src = p.x + (long long)(cw & 0x7FFFFFFFu) * p.ldx + icol;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if ((imask >> u) & 1u) cp_async<V>(&sm.ring[s0 + b][u][lane * V], src + u * kSeg);
+          // the delta's signed value (the reference's values[k], kernels.cpp:33)
+          float val;
+          if constexpr (SC != 0) val = __shfl_sync(kFull, win.v, (iq + b) & 31);
+          else val = __int_as_float(0x3F800000u | (cw & 0x80000000u));
+          if (uint32_t(lane) == s0 + b) vring = val;
+        }
+      }
+      iseq += B;
+      iq += n;
       if (iq == ilen) {
         next_ticket();
       } else if ((iq & 31) == 0) {  // next 32-delta block of a long ticket
@@ -432,7 +441,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   if (R(0).end != R(0).beg) load_ticket();
   else next_ticket();
 #pragma unroll 1
-  for (int q = 0; q < D; ++q) issue_one();
+  for (int q = 0; q < G; ++q) issue_group();
 
   uint32_t cseq = 0;  // deltas consumed
   unsigned long long t_first = 0ull;
@@ -455,51 +464,36 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     T4 acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = W::zero();
-    // deltas B at a time: one wait covers B slots and all B shared-memory
-    // reads are in flight before the adds (the adds stay in delta order)
-    uint32_t k = r.beg;
+    // one ring group (B slots) per wait: all B shared-memory reads are in
+    // flight before the adds, which stay in delta order. Segments outside the
+    // matrix read stale ring bytes into accumulators that are never stored.
 #pragma unroll 1
-    for (; k + B <= r.end; k += B) {
-      cp_wait<D - B>();  // this lane's copies of deltas cseq .. cseq+B-1 have landed
+    for (uint32_t k = r.beg; k < r.end; k += B) {
+      const uint32_t nb = min(uint32_t(B), r.end - k);
+      cp_wait<G - 1>();  // this lane's copies of the group have landed
       if (p.trace && t_first == 0ull) t_first = globaltimer();
-      // Segments outside the matrix read stale ring bytes into accumulators
-      // that are never stored: no per-segment branch on the hot path.
+      const uint32_t s0 = cseq & (D - 1);
       float sc[B];
       T4 v[B][U];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        const uint32_t sb = (cseq + b) & (D - 1);
-        sc[b] = __shfl_sync(kFull, vring, sb);  // +-1 or +-s_c
+        sc[b] = __shfl_sync(kFull, vring, s0 + b);  // +-1 or +-s_c
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[b][u] = lds<V>(&sm.ring[sb][u][lane * V]);
+        for (int u = 0; u < U; ++u) v[b][u] = lds<V>(&sm.ring[s0 + b][u][lane * V]);
       }
 #pragma unroll
       for (int b = 0; b < B; ++b) {
+        if (uint32_t(b) < nb) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if constexpr (SC == 1) acc[u] = W::add(acc[u], W::mul(v[b][u], sc[b]));
-          else acc[u] = fma_sign<V>(acc[u], v[b][u], sc[b]);
+          for (int u = 0; u < U; ++u) {
+            if constexpr (SC == 1) acc[u] = W::add(acc[u], W::mul(v[b][u], sc[b]));
+            else acc[u] = fma_sign<V>(acc[u], v[b][u], sc[b]);
+          }
         }
       }
       cseq += B;
-      __syncwarp();  // the B slots are fully read before their refill
-#pragma unroll
-      for (int b = 0; b < B; ++b) issue_one();
-    }
-#pragma unroll 1
-    for (; k < r.end; ++k) {  // tail, one delta at a time
-      cp_wait<D - 1>();
-      const uint32_t s = cseq & (D - 1);
-      const float sc = __shfl_sync(kFull, vring, s);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const T4 v = lds<V>(&sm.ring[s][u][lane * V]);
-        if constexpr (SC == 1) acc[u] = W::add(acc[u], W::mul(v, sc));
-        else acc[u] = fma_sign<V>(acc[u], v, sc);
-      }
-      ++cseq;
-      __syncwarp();
-      issue_one();
+      __syncwarp();  // the group's slots are fully read before their refill
+      issue_group();
     }
     // ---- epilogue: partials, then CHUNK/MERGE publish or ROW stage 2 + 3
     uint32_t* flag_base = p.flags + (size_t)slab * p.n_items;

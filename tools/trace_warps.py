@@ -40,7 +40,12 @@ def main():
     nw = (rows[:, 4] >> 16) & 0xFFFF
     deltas = rows[:, 4] >> 32
     q = lambda a: " ".join(f"{v:7.2f}" for v in np.percentile(a, [0, 10, 50, 90, 99, 100]))
-    print(f"{name}: warps {len(rows)}  pctl 0/10/50/90/99/100 (us from first warp start)")
+    info = d.info()
+    span = end.max()
+    gb = info["nnz_effective"] * w.d * 4 / 1e9
+    print(f"{name}: warps {len(rows)}  span {span:.1f} us  gathers {gb:.2f} GB -> "
+          f"{gb / span * 1e3:.1f} TB/s over the span  info {info}")
+    print("  pctl 0/10/50/90/99/100 (us from first warp start)")
     print("  start      ", q(st))
     print("  first data ", q(first))
     print("  end        ", q(end))
