@@ -834,7 +834,16 @@ void device_gcn_forward(DeviceMatrix* h, const float* x, uint32_t n, uint32_t f,
 DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& opt) {
   // validate + plan on the host first: malformed input is EINVAL, never a CUDA error
   const uint32_t gain = opt.flatten_gain < 0 ? 16u : uint32_t(opt.flatten_gain);
-  Layout L = plan_layout(v, opt.order_faithful != 0, opt.split_threshold, opt.chunk, gain);
+  // resident warps for the auto split: ~20 per SM (the multiply's occupancy);
+  // without a device the upload fails after validation anyway
+  int sms = 148, cur = 0;
+  if (cudaGetDevice(&cur) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount,
+                             opt.device >= 0 ? opt.device : cur) != cudaSuccess)
+    sms = 148;
+  cudaGetLastError();  // a failed probe must not leak into later error checks
+  Layout L = plan_layout(v, opt.order_faithful != 0, opt.split_threshold, opt.chunk, gain,
+                         uint32_t(sms) * 20);
   auto* h = new DeviceMatrix;
   try {
     int dev = opt.device;

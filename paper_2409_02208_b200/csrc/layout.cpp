@@ -10,7 +10,7 @@
 namespace cbmb {
 
 Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t split_threshold,
-                   uint32_t chunk, uint32_t flatten_gain) {
+                   uint32_t chunk, uint32_t flatten_gain, uint32_t warps_hint) {
   const uint32_t m = v.n_rows;
   Layout L;
   L.n_rows = m;
@@ -215,8 +215,17 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   }
 
   // split plan for long rows (default mode only)
-  if (split_threshold == 0) split_threshold = 32;
-  if (chunk == 0) chunk = 32;
+  // auto: split rows longer than ~1/8 of a warp's share of the deltas (a
+  // power of two in [32, 256]): small matrices need short pieces to spread
+  // over the grid, large ones lose more to the partial-sum hand-offs than
+  // they gain in balance (tools/probe_split.py: cfg[1] best at 32, cfg[2] and
+  // cfg[3] at 256 / 64)
+  if (split_threshold == 0) {
+    const uint64_t share = L.nnz_effective / std::max<uint32_t>(1, warps_hint) / 8;
+    split_threshold = 32;
+    while (split_threshold < 256 && uint64_t(split_threshold) * 2 <= share) split_threshold *= 2;
+  }
+  if (chunk == 0) chunk = std::max<uint32_t>(32, split_threshold / 4);
   if (chunk > split_threshold) chunk = split_threshold;
   std::vector<uint32_t> pieces(m, 1);  // per ROW position i
   uint64_t n_leaf = 0;

@@ -61,7 +61,8 @@ struct Layout {
 
 // Validates the view like load_cbm (io.cpp:346-380) and builds the layout.
 // Throws cbmb::invalid_argument with a reference-style message.
+// warps_hint: resident warps of the target device (sizes the auto split).
 Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t split_threshold,
-                   uint32_t chunk, uint32_t flatten_gain);
+                   uint32_t chunk, uint32_t flatten_gain, uint32_t warps_hint);
 
 }  // namespace cbmb
