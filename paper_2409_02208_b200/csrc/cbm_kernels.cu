@@ -950,9 +950,11 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   bool prescale = false;
   if (L.normalized) {
     if (h->opt.prescale > 0) prescale = true;
-    // auto: the per-delta FMUL costs nnz*d ALU ops; pre-scaling costs an
-    // extra 8*n*d bytes of HBM traffic (prescale).
-    else if (h->opt.prescale < 0) prescale = L.nnz_effective > 48ull * L.n_cols;
+    // auto: in the order-faithful mode the per-delta FMUL costs nnz*d ALU ops
+    // and pre-scaling an extra 8*n*d bytes of HBM traffic; the
+    // default mode fuses the product into the FMA, so there is nothing to save
+    else if (h->opt.prescale < 0)
+      prescale = L.order_faithful && L.nnz_effective > 48ull * L.n_cols;
   }
   const float* xin = x;
   int64_t ldin = ldx;
