@@ -105,8 +105,10 @@ int cbm_b200_count_ops(const cbm_b200_cbm_view* c, uint64_t* multiply_adds,
 
 /* ------------------------------------------------------------------------
  * Device operator: the CBM uploaded once into the level-ordered device layout
- * (DESIGN.md §Layout). Immutable after upload. Calls on one handle must be
- * issued on one stream at a time (the handle owns its per-call workspace).
+ * (DESIGN.md §Layout). Immutable after upload and shareable: calls from any
+ * thread are safe, and calls on distinct streams may run concurrently (each
+ * stream gets its own per-call workspace; the reference's CbmMatrix is
+ * likewise immutable and shareable).
  * --------------------------------------------------------------------- */
 typedef struct cbm_b200_matrix cbm_b200_matrix;
 
@@ -163,6 +165,21 @@ int cbm_b200_spmm(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_
 int cbm_b200_spmm_host(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_cols,
                        float* y, int64_t y_rows, int64_t y_cols, void* stream);
 
+/* Column sharding: every stage of the multiply acts on one
+ * column (kernels.cpp:27-62), so device k of n multiplies the contiguous
+ * column slab cbm_b200_column_slab(d, n, k) against a full replica of the
+ * CBM; no collective is needed and the slabs are bit-identical to the
+ * single-device result. */
+int cbm_b200_column_slab(int64_t d, int32_t world, int32_t rank, int64_t* lo, int64_t* hi);
+
+/* Single-process multi-device spmm_into on HOST buffers: handles[k] (one
+ * upload of the same CBM per device, distinct handles) multiplies column slab
+ * k of X into slab k of Y; the devices' copies and kernels overlap; returns
+ * when Y is complete. Shape errors as spmm_into. */
+int cbm_b200_spmm_sharded(cbm_b200_matrix* const* handles, int32_t n_handles, const float* x,
+                          int64_t x_rows, int64_t x_cols, float* y, int64_t y_rows,
+                          int64_t y_cols);
+
 /* u = A v (spmv_into, kernels.hpp:41-44, kernels.cpp:70-97): v is n_cols x 1. */
 int cbm_b200_spmv(cbm_b200_matrix* h, const float* v, int64_t v_rows, int64_t v_cols,
                   float* u, int64_t u_rows, int64_t u_cols, void* stream);
@@ -184,8 +201,11 @@ int cbm_b200_gcn_forward(cbm_b200_matrix* h, const float* x, int64_t n, int64_t 
                          float* out, void* stream);
 
 /* Pre-size the per-call workspace for up to d_max columns so later calls
- * never allocate (the device analogue of Property 3, kernels.hpp:36-39). */
+ * never allocate (the device analogue of Property 3, kernels.hpp:36-39):
+ * cbm_b200_reserve for the legacy default stream, cbm_b200_reserve_on for a
+ * given stream. */
 int cbm_b200_reserve(cbm_b200_matrix* h, int64_t d_max);
+int cbm_b200_reserve_on(cbm_b200_matrix* h, int64_t d_max, void* stream);
 
 typedef struct cbm_b200_info {
   uint32_t n_rows, n_cols;

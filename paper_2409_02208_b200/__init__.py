@@ -109,6 +109,11 @@ _sig = {
     "cbm_b200_upload": (C.c_int, [C.POINTER(_CbmView), C.POINTER(_Options), C.POINTER(_vp)]),
     "cbm_b200_free": (None, [_vp]),
     "cbm_b200_reserve": (C.c_int, [_vp, _i64]),
+    "cbm_b200_reserve_on": (C.c_int, [_vp, _i64, _vp]),
+    "cbm_b200_column_slab": (C.c_int, [_i64, C.c_int32, C.c_int32, C.POINTER(_i64),
+                                       C.POINTER(_i64)]),
+    "cbm_b200_spmm_sharded": (C.c_int, [C.POINTER(_vp), C.c_int32, _vp, _i64, _i64, _vp, _i64,
+                                        _i64]),
     "cbm_b200_spmm": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp]),
     "cbm_b200_spmm_host": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp]),
     "cbm_b200_spmv": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp]),
@@ -353,6 +358,30 @@ def generate_dense(kind: str, rows: int, cols: int, seed: int, lo: float = -1.0,
     return out
 
 
+def column_slab(d: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) columns of `rank` of `world` (cbm_b200_column_slab)."""
+    lo, hi = _i64(), _i64()
+    _check(_lib.cbm_b200_column_slab(d, world, rank, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def spmm_sharded(ops, x: np.ndarray, y: np.ndarray | None = None) -> np.ndarray:
+    """Y = A X on host arrays with the columns split over `ops` (one DeviceCbm
+    of the same matrix per device; cbm_b200_spmm_sharded)."""
+    ops = list(ops)
+    if not ops:
+        raise ValueError("spmm_sharded: no handles")
+    x = np.ascontiguousarray(x, np.float32)
+    if x.ndim != 2:
+        raise ValueError("spmm: operand must be 2-D")
+    if y is None:
+        y = np.empty((ops[0].n_rows, x.shape[1]), np.float32)
+    hs = (_vp * len(ops))(*[o._h for o in ops])
+    _check(_lib.cbm_b200_spmm_sharded(hs, len(ops), x.ctypes.data, x.shape[0], x.shape[1],
+                                      y.ctypes.data, y.shape[0], y.shape[1]))
+    return y
+
+
 def dense_matmul(a, b, stream=None):
     """dense_matmul (dense.hpp:48-50) on CUDA float32 tensors, reference-exact."""
     torch = _torch()
@@ -413,8 +442,9 @@ class DeviceCbm:
         _check(_lib.cbm_b200_get_info(self._h, C.byref(i)))
         return {k: getattr(i, k) for k, _ in _Info._fields_}
 
-    def reserve(self, d_max: int):
-        _check(_lib.cbm_b200_reserve(self._h, d_max))
+    def reserve(self, d_max: int, stream=None):
+        """Pre-size the workspace of `stream` (default: the current stream)."""
+        _check(_lib.cbm_b200_reserve_on(self._h, d_max, self._stream(stream)))
 
     @staticmethod
     def _stream(stream):

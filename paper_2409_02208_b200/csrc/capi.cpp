@@ -1,10 +1,13 @@
 // extern "C" boundary (include/cbm_b200.h). Exceptions never cross it: each
 // entry point maps them onto a status code plus a thread-local message, the
 // way the reference raises std::invalid_argument / std::logic_error.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/cbm_b200.h"
 #include "cbm_host.hpp"
@@ -230,7 +233,15 @@ int cbm_b200_reserve(cbm_b200_matrix* h, int64_t d_max) {
   return guard([&] {
     need(h && d_max >= 0, "reserve: bad argument");
     std::lock_guard<std::mutex> lk(h->d->mu);
-    cbmb::device_reserve(h->d, uint64_t(d_max));
+    cbmb::device_reserve(h->d, uint64_t(d_max), nullptr);
+  });
+}
+
+int cbm_b200_reserve_on(cbm_b200_matrix* h, int64_t d_max, void* stream) {
+  return guard([&] {
+    need(h && d_max >= 0, "reserve: bad argument");
+    std::lock_guard<std::mutex> lk(h->d->mu);
+    cbmb::device_reserve(h->d, uint64_t(d_max), stream);
   });
 }
 
@@ -254,7 +265,56 @@ int cbm_b200_spmm_host(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64
     check_spmm_shapes(h->d->info, x_rows, x_cols, y_rows, y_cols, "spmm");
     need((x || x_rows * x_cols == 0) && (y || y_rows * y_cols == 0), "spmm: null data");
     std::lock_guard<std::mutex> lk(h->d->mu);
-    cbmb::device_spmm_host(h->d, x, uint32_t(x_cols), y, stream);
+    cbmb::device_spmm_host(h->d, x, x_cols, uint32_t(x_cols), y, y_cols, stream);
+  });
+}
+
+int cbm_b200_column_slab(int64_t d, int32_t world, int32_t rank, int64_t* lo, int64_t* hi) {
+  return guard([&] {
+    need(lo && hi && d >= 0 && world >= 1 && rank >= 0 && rank < world,
+         "column_slab: bad rank/world");
+    // contiguous, balanced in units of 4 columns (16-byte rows for LDG.128)
+    const int64_t units = (d + 3) / 4;
+    *lo = std::min<int64_t>(d, units * rank / world * 4);
+    *hi = std::max<int64_t>(*lo, std::min<int64_t>(d, units * (rank + 1) / world * 4));
+  });
+}
+
+int cbm_b200_spmm_sharded(cbm_b200_matrix* const* handles, int32_t n_handles, const float* x,
+                          int64_t x_rows, int64_t x_cols, float* y, int64_t y_rows,
+                          int64_t y_cols) {
+  return guard([&] {
+    need(handles && n_handles >= 1, "spmm_sharded: no handles");
+    for (int32_t k = 0; k < n_handles; ++k) {
+      need(handles[k] != nullptr, "spmm_sharded: null handle");
+      for (int32_t j = 0; j < k; ++j)
+        need(handles[j] != handles[k], "spmm_sharded: a handle appears twice");
+    }
+    const auto& L0 = handles[0]->d->info;
+    for (int32_t k = 1; k < n_handles; ++k) {
+      const auto& L = handles[k]->d->info;
+      need(L.n_rows == L0.n_rows && L.n_cols == L0.n_cols && L.normalized == L0.normalized &&
+               L.nnz == L0.nnz,
+           "spmm_sharded: handles hold different matrices");
+    }
+    check_spmm_shapes(L0, x_rows, x_cols, y_rows, y_cols, "spmm");
+    need((x || x_rows * x_cols == 0) && (y || y_rows * y_cols == 0), "spmm: null data");
+    // lock every handle (distinct, in address order), queue every slab, then wait:
+    // the devices' copies and kernels run concurrently
+    std::vector<cbm_b200_matrix*> order(handles, handles + n_handles);
+    std::sort(order.begin(), order.end());
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (auto* h : order) locks.emplace_back(h->d->mu);
+    std::vector<int32_t> queued;
+    for (int32_t k = 0; k < n_handles; ++k) {
+      int64_t lo = 0, hi = 0;
+      cbm_b200_column_slab(x_cols, n_handles, k, &lo, &hi);
+      if (hi == lo) continue;
+      cbmb::device_spmm_host(handles[k]->d, x + lo, x_cols, uint32_t(hi - lo), y + lo, y_cols,
+                             nullptr, /*wait=*/false);
+      queued.push_back(k);
+    }
+    for (int32_t k : queued) cbmb::device_spmm_host_wait(handles[k]->d, nullptr);
   });
 }
 

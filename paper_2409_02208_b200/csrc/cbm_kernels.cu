@@ -817,9 +817,10 @@ void device_gcn_forward(DeviceMatrix* h, const float* x, uint32_t n, uint32_t f,
                         float* out, void* stream) {
   ck(cudaSetDevice(h->device), "cudaSetDevice");
   const uint32_t hp = (hid + 3) & ~3u;
-  grow(h->gcn_h, h->gcn_h_cap, uint64_t(n) * hp * 2, "gcn workspace");
-  float* h0 = h->gcn_h;
-  float* h1 = h->gcn_h + uint64_t(n) * hp;
+  auto& ws = h->ws[stream];
+  grow(ws.gcn_h, ws.gcn_h_cap, uint64_t(n) * hp * 2, "gcn workspace");
+  float* h0 = ws.gcn_h;
+  float* h1 = ws.gcn_h + uint64_t(n) * hp;
   uint32_t launches = 0;
   device_dense_matmul(x, n, f, w0, hid, h0, stream);  // packed n x hid
   ++launches;
@@ -905,11 +906,13 @@ void device_free(DeviceMatrix* h) {
     cudaStreamDestroy(h->s_out);
     for (auto e : h->ev) cudaEventDestroy(e);
   }
-  if (h->gcn_h) cudaFree(h->gcn_h);
   for (auto& kv : h->schedules) cudaFree(kv.second.trec);
+  for (auto& kv : h->ws)
+    for (void* p : {(void*)kv.second.flags, (void*)kv.second.partial, (void*)kv.second.interior,
+                    (void*)kv.second.xs, (void*)kv.second.gcn_h})
+      if (p) cudaFree(p);
   for (void* p : {(void*)h->dcol, (void*)h->dval, (void*)h->rec, (void*)h->srow, (void*)h->scale,
-                  (void*)h->flags, (void*)h->partial,
-                  (void*)h->interior, (void*)h->xs, (void*)h->xstage, (void*)h->ystage})
+                  (void*)h->xstage, (void*)h->ystage})
     if (p) cudaFree(p);
   delete h;
 }
@@ -923,18 +926,19 @@ uint32_t pick_vec(uint32_t d, const float* x, int64_t ldx, const float* y, int64
 }
 }  // namespace
 
-void device_reserve(DeviceMatrix* h, uint64_t d) {
+void device_reserve(DeviceMatrix* h, uint64_t d, void* stream) {
   const Layout& L = h->info;
   const uint64_t dpad = (d + 3) & ~uint64_t(3);
   const uint64_t slabs = (d + 31) / 32;  // worst case (V = 1)
   ck(cudaSetDevice(h->device), "cudaSetDevice");
-  if (uint64_t(L.n_items) * slabs > h->flags_cap) {
-    grow(h->flags, h->flags_cap, uint64_t(L.n_items) * slabs, "workspace flags");
-    ck(cudaMemset(h->flags, 0, h->flags_cap * sizeof(uint32_t)), "flags memset");
-    h->epoch = 0;
+  auto& ws = h->ws[stream];
+  if (uint64_t(L.n_items) * slabs > ws.flags_cap) {
+    grow(ws.flags, ws.flags_cap, uint64_t(L.n_items) * slabs, "workspace flags");
+    ck(cudaMemset(ws.flags, 0, ws.flags_cap * sizeof(uint32_t)), "flags memset");
+    ws.epoch = 0;
   }
-  grow(h->partial, h->partial_cap, uint64_t(L.n_chunk_items) * dpad, "workspace partial");
-  if (L.normalized) grow(h->interior, h->interior_cap, uint64_t(L.n_interior) * dpad,
+  grow(ws.partial, ws.partial_cap, uint64_t(L.n_chunk_items) * dpad, "workspace partial");
+  if (L.normalized) grow(ws.interior, ws.interior_cap, uint64_t(L.n_interior) * dpad,
                          "workspace interior");
 }
 
@@ -945,7 +949,8 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   h->last_launches = 0;
   if (L.n_rows == 0 || d == 0) return;
   ck(cudaSetDevice(h->device), "cudaSetDevice");
-  device_reserve(h, d);
+  device_reserve(h, d, stream);
+  auto& ws = h->ws[stream];
   const uint32_t dpad = (d + 3) & ~3u;
   bool prescale = false;
   if (L.normalized) {
@@ -959,13 +964,13 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   const float* xin = x;
   int64_t ldin = ldx;
   if (prescale) {
-    grow(h->xs, h->xs_cap, uint64_t(L.n_cols) * dpad, "workspace prescale");
+    grow(ws.xs, ws.xs_cap, uint64_t(L.n_cols) * dpad, "workspace prescale");
     const uint64_t total = uint64_t(L.n_cols) * d;
     const int grid = int(std::min<uint64_t>((total + 255) / 256, uint64_t(h->num_sms) * 16));
-    prescale_kernel<<<grid, 256, 0, s>>>(x, ldx, h->scale, L.n_cols, d, h->xs, dpad);
+    prescale_kernel<<<grid, 256, 0, s>>>(x, ldx, h->scale, L.n_cols, d, ws.xs, dpad);
     ck(cudaGetLastError(), "prescale launch");
     ++h->last_launches;
-    xin = h->xs;
+    xin = ws.xs;
     ldin = dpad;
   }
   // lanes x V floats per column slab: V = 4 (LDG.128) when rows are 16-byte
@@ -980,9 +985,9 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   // (narrower slabs that fit X in L2 were measured slower on cfg[2]/cfg[3]:
   // the extra per-ticket work outweighs the L2 misses they remove)
   const uint32_t n_slabs = (d + 32 * V * U - 1) / (32 * V * U);
-  if (++h->epoch == 0) {  // wrapped: re-zero the flags
-    ck(cudaMemsetAsync(h->flags, 0, h->flags_cap * sizeof(uint32_t), s), "flags memset");
-    h->epoch = 1;
+  if (++ws.epoch == 0) {  // wrapped: re-zero the flags
+    ck(cudaMemsetAsync(ws.flags, 0, ws.flags_cap * sizeof(uint32_t), s), "flags memset");
+    ws.epoch = 1;
   }
   Params p;
   p.dcol = h->dcol;
@@ -992,9 +997,9 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   p.ldx = ldin;
   p.y = y;
   p.ldy = ldy;
-  p.partial = h->partial;
-  p.interior = h->interior;
-  p.flags = h->flags;
+  p.partial = ws.partial;
+  p.interior = ws.interior;
+  p.flags = ws.flags;
   p.n_items = L.n_items;
   p.n_chunk = L.n_chunk_items;
   p.d = d;
@@ -1002,7 +1007,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   const uint64_t tickets = uint64_t(L.n_items) * n_slabs;
   if (tickets >= 0x7FFFFFFFull) throw invalid_argument("spmm: too many work tickets");
   p.total_tickets = uint32_t(tickets);
-  p.epoch = h->epoch;
+  p.epoch = ws.epoch;
   p.relu = relu ? 1u : 0u;
   // pull a small, contiguous X into L2 ahead of the gathers
   const uint64_t xbytes = uint64_t(L.n_cols) * d * sizeof(float);
@@ -1057,7 +1062,8 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
 // and Y move in column chunks on three streams: H2D of chunk k+1 and D2H of
 // chunk k-1 run while chunk k multiplies, and the two copy directions overlap
 // on the full-duplex PCIe link. One chunk when the operand is small.
-void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, void* stream) {
+void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
+                      int64_t ldy, void* stream, bool wait) {
   const Layout& L = h->info;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ck(cudaSetDevice(h->device), "cudaSetDevice");
@@ -1081,7 +1087,7 @@ void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, voi
   ck(cudaStreamWaitEvent(h->s_out, h->ev[0], 0), "wait");
   for (uint32_t k = 0, c0 = 0; c0 < d; ++k, c0 += cw) {
     const uint32_t w = std::min(cw, d - c0);
-    ck(cudaMemcpy2DAsync(h->xstage + c0, dpad * sizeof(float), x + c0, d * sizeof(float),
+    ck(cudaMemcpy2DAsync(h->xstage + c0, dpad * sizeof(float), x + c0, ldx * sizeof(float),
                          w * sizeof(float), L.n_cols, cudaMemcpyHostToDevice, h->s_in),
        "H2D X");
     ck(cudaEventRecord(h->ev[1 + k], h->s_in), "event");
@@ -1094,13 +1100,21 @@ void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, voi
     launches += h->last_launches;
     ck(cudaEventRecord(h->ev[1 + kHostChunks + k], s), "event");
     ck(cudaStreamWaitEvent(h->s_out, h->ev[1 + kHostChunks + k], 0), "wait");
-    ck(cudaMemcpy2DAsync(y + c0, d * sizeof(float), h->ystage + c0, dpad * sizeof(float),
+    ck(cudaMemcpy2DAsync(y + c0, ldy * sizeof(float), h->ystage + c0, dpad * sizeof(float),
                          w * sizeof(float), L.n_rows, cudaMemcpyDeviceToHost, h->s_out),
        "D2H Y");
   }
   h->last_launches = launches;  // kernels launched by this call (one per chunk)
+  // the caller's stream resumes after the last copy-out
+  ck(cudaEventRecord(h->ev[0], h->s_out), "event");
+  ck(cudaStreamWaitEvent(s, h->ev[0], 0), "wait");
+  if (wait) device_spmm_host_wait(h, stream);
+}
+
+void device_spmm_host_wait(DeviceMatrix* h, void* stream) {
+  ck(cudaSetDevice(h->device), "cudaSetDevice");
   ck(cudaStreamSynchronize(h->s_out), "spmm_host synchronize");
-  ck(cudaStreamSynchronize(s), "spmm_host synchronize");
+  ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "spmm_host synchronize");
 }
 
 }  // namespace cbmb

@@ -31,19 +31,24 @@ struct DeviceMatrix {
   float* srow = nullptr;
   float* scale = nullptr;
   uint64_t device_bytes = 0;
-  // per-call workspace (grown on demand, or by cbm_b200_reserve)
-  uint32_t* flags = nullptr;
-  uint64_t flags_cap = 0;        // entries
-  float* partial = nullptr;
-  uint64_t partial_cap = 0;      // floats
-  float* interior = nullptr;
-  uint64_t interior_cap = 0;
-  float* xs = nullptr;           // pre-scaled operand (normalized, prescale on)
-  uint64_t xs_cap = 0;
+  // per-call workspace, one per stream (concurrent calls on distinct streams
+  // never share flags or scratch); grown on demand, or by cbm_b200_reserve
+  struct Workspace {
+    uint32_t* flags = nullptr;
+    uint64_t flags_cap = 0;      // entries
+    float* partial = nullptr;
+    uint64_t partial_cap = 0;    // floats
+    float* interior = nullptr;
+    uint64_t interior_cap = 0;
+    float* xs = nullptr;         // pre-scaled operand (normalized, prescale on)
+    uint64_t xs_cap = 0;
+    float* gcn_h = nullptr;      // GCN hidden activations (2 x n x hid)
+    uint64_t gcn_h_cap = 0;
+    uint32_t epoch = 0;          // ready-flag stamp of the last call
+  };
+  std::map<void*, Workspace> ws;
   float* xstage = nullptr;       // host-API staging
   uint64_t xstage_cap = 0;
-  float* gcn_h = nullptr;        // GCN hidden activations (2 x n x hid)
-  uint64_t gcn_h_cap = 0;
   float* ystage = nullptr;
   uint64_t ystage_cap = 0;
   // host-API pipeline: copy-in / copy-out streams and chunk events
@@ -56,14 +61,13 @@ struct DeviceMatrix {
   };
   std::map<uint64_t, Schedule> schedules;
   std::vector<uint32_t> item_dep;  // per item: parent item (ppos), first partial, count
-  uint32_t epoch = 0;
   uint32_t last_launches = 0;
   std::mutex mu;
 };
 
 DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& opt);
 void device_free(DeviceMatrix* h);
-void device_reserve(DeviceMatrix* h, uint64_t d);
+void device_reserve(DeviceMatrix* h, uint64_t d, void* stream);
 // Y = A X; x/y are device pointers; d = columns. Shapes already validated.
 void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
                  int64_t ldy, void* stream, bool relu = false);
@@ -72,6 +76,11 @@ void device_dense_matmul(const float* a, uint32_t m, uint32_t k, const float* b,
 void device_gcn_forward(DeviceMatrix* h, const float* x, uint32_t n, uint32_t f,
                         const float* w0, uint32_t hid, const float* w1, uint32_t classes,
                         float* out, void* stream);
-void device_spmm_host(DeviceMatrix* h, const float* x, uint32_t d, float* y, void* stream);
+// Host buffers (row-major, leading dimensions ldx/ldy in floats): column
+// chunks of X in, multiply, Y out, copies overlapped on the handle's copy
+// streams. wait = false leaves the work queued (device_spmm_host_wait).
+void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
+                      int64_t ldy, void* stream, bool wait = true);
+void device_spmm_host_wait(DeviceMatrix* h, void* stream);
 
 }  // namespace cbmb

@@ -9,16 +9,17 @@ columns (16-byte rows for the LDG.128 lanes) where the width allows.
 """
 from __future__ import annotations
 
+from . import column_slab as _native_slab
 
-def column_slab(d: int, world: int, rank: int, align: int = 4) -> tuple[int, int]:
-    """[lo, hi) columns of `rank`: contiguous, balanced in units of `align`."""
+
+def column_slab(d: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) columns of `rank`: contiguous, balanced in units of 4 columns
+    (the library's cbm_b200_column_slab, so every rank and the single-process
+    cbm_b200_spmm_sharded agree on the partition)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("column_slab: bad rank/world")
-    units = (d + align - 1) // align
-    lo = min(d, units * rank // world * align)
-    hi = min(d, units * (rank + 1) // world * align)
-    return lo, max(lo, hi)
+    return _native_slab(d, world, rank)
 
 
-def all_slabs(d: int, world: int, align: int = 4) -> list[tuple[int, int]]:
-    return [column_slab(d, world, r, align) for r in range(world)]
+def all_slabs(d: int, world: int) -> list[tuple[int, int]]:
+    return [column_slab(d, world, r) for r in range(world)]

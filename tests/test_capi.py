@@ -72,3 +72,17 @@ def test_random_binary_generator_matches_reference_stream():
     a = P.generate_graph("random_binary", [20, 30, 0.3], 77)
     rp, ci = O.oracle_random_binary(20, 30, 0.3, 77)
     assert np.array_equal(a.row_ptr, rp) and np.array_equal(a.col_idx, ci)
+
+
+def test_upload_rejects_unknown_kernel_option():
+    c = P.build_cbm(P.CsrBinaryMatrix.from_rows(3, [[0, 1], [0, 1], [2]]), 0)
+    with pytest.raises(ValueError, match="kernel must be"):
+        P.DeviceCbm(c, kernel="register")
+    opt = P._Options()
+    P._lib.cbm_b200_default_options(ctypes.byref(opt))
+    opt.kernel = 2
+    h = ctypes.c_void_p()
+    view = c._view()
+    rc = P._lib.cbm_b200_upload(ctypes.byref(view), ctypes.byref(opt), ctypes.byref(h))
+    assert rc == 1 and b"options.kernel" in P._lib.cbm_b200_last_error()
+    assert not h.value

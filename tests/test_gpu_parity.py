@@ -278,3 +278,43 @@ def test_csr_comparator_operator(normalized, dev):
     else:
         vals = np.ones(a.nnz, np.float32)
         assert_bitwise(got, O.oracle_csr_spmm(a.row_ptr, a.col_idx, vals, x), "csr")
+
+
+def test_concurrent_streams_share_one_handle(dev):
+    """The uploaded operator is shareable: interleaved calls on two streams
+    (each with its own workspace) give the same bits as serial calls."""
+    a = P.generate_graph("community", [3000, 100, 0.4, 0.002], 61)
+    c = P.build_cbm_normalized(a, 0)
+    d = P.DeviceCbm(c)
+    xa = torch.from_numpy(P.generate_dense("normal", 3000, 96, 62)).to(dev)
+    xb = torch.from_numpy(P.generate_dense("normal", 3000, 96, 63)).to(dev)
+    want_a, want_b = d.spmm(xa), d.spmm(xb)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    ya = [torch.empty_like(want_a) for _ in range(20)]
+    yb = [torch.empty_like(want_b) for _ in range(20)]
+    for i in range(20):
+        d.spmm_into(xa, ya[i], s1)
+        d.spmm_into(xb, yb[i], s2)
+    torch.cuda.synchronize()
+    for i in range(20):
+        assert torch.equal(ya[i], want_a) and torch.equal(yb[i], want_b), i
+
+
+@pytest.mark.parametrize("n_handles", [1, 2, 3])
+def test_spmm_sharded_host_buffers_bitwise(n_handles, dev):
+    """cbm_b200_spmm_sharded: column slabs over several handles (all on
+    cuda:0 here; one per device in production) reassemble the single-handle
+    result bit for bit."""
+    a = P.generate_graph("pa_triangle", [4000, 2, 0.3], 71)
+    c = P.build_cbm_normalized(a, 0)
+    x = P.generate_dense("normal", 4000, 200, 72)
+    want = P.DeviceCbm(c).spmm_host(x)
+    ops = [P.DeviceCbm(c, device=0) for _ in range(n_handles)]
+    got = P.spmm_sharded(ops, x)
+    assert_bitwise(got, want, f"sharded x{n_handles}")
+    with pytest.raises(ValueError, match="inner dimensions"):
+        P.spmm_sharded(ops, x[:100])
+    if n_handles > 1:
+        with pytest.raises(ValueError, match="appears twice"):
+            P.spmm_sharded([ops[0], ops[0]], x)

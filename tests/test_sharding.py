@@ -29,6 +29,17 @@ def test_slabs_partition_columns(d, world):
         assert lo % 4 == 0
 
 
+@pytest.mark.parametrize("d,world", [(512, 8), (64, 8), (130, 4), (7, 2), (1, 2), (0, 3)])
+def test_native_slabs_match_the_balanced_unit_partition(d, world):
+    units = (d + 3) // 4
+    for r in range(world):
+        lo = min(d, units * r // world * 4)
+        hi = max(lo, min(d, units * (r + 1) // world * 4))
+        assert column_slab(d, world, r) == (lo, hi)
+    with pytest.raises(ValueError):
+        column_slab(d, world, world)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
