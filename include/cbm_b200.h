@@ -159,6 +159,14 @@ int cbm_b200_spmm(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_
                   int64_t ldx, float* y, int64_t y_rows, int64_t y_cols, int64_t ldy,
                   void* stream);
 
+/* cbm_b200_spmm with epilogue flags: CBM_B200_RELU applies relu_inplace
+ * (dense.cpp:51-54: v < 0 -> +0) to Y in the multiply's epilogue, as the
+ * first GCN layer does (gcn.cpp:29-30). */
+#define CBM_B200_RELU 1u
+int cbm_b200_spmm_ex(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_cols,
+                     int64_t ldx, float* y, int64_t y_rows, int64_t y_cols, int64_t ldy,
+                     uint32_t flags, void* stream);
+
 /* Same with HOST buffers (the drop-in for spmm_into on DenseMatrix data):
  * H2D of X, the multiply, D2H of Y, then a stream synchronize. Pinned host
  * memory gives full-bandwidth copies; pageable memory works too. */

@@ -110,6 +110,8 @@ _sig = {
     "cbm_b200_free": (None, [_vp]),
     "cbm_b200_reserve": (C.c_int, [_vp, _i64]),
     "cbm_b200_reserve_on": (C.c_int, [_vp, _i64, _vp]),
+    "cbm_b200_spmm_ex": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, C.c_uint32,
+                                   _vp]),
     "cbm_b200_column_slab": (C.c_int, [_i64, C.c_int32, C.c_int32, C.POINTER(_i64),
                                        C.POINTER(_i64)]),
     "cbm_b200_spmm_sharded": (C.c_int, [C.POINTER(_vp), C.c_int32, _vp, _i64, _i64, _vp, _i64,
@@ -452,19 +454,25 @@ class DeviceCbm:
             return _torch().cuda.current_stream().cuda_stream
         return getattr(stream, "cuda_stream", stream)
 
-    def spmm_into(self, x, y, stream=None):
-        """Y = A X on CUDA float32 tensors (row-major; Y fully overwritten)."""
+    def spmm_into(self, x, y, stream=None, relu: bool = False):
+        """Y = A X on CUDA float32 tensors (row-major; Y fully overwritten);
+        relu=True fuses relu_inplace (dense.cpp:51-54) into the epilogue."""
         xs, ys = x.stride(), y.stride()
         if x.dim() != 2 or y.dim() != 2 or xs[1] != 1 or ys[1] != 1:
             raise ValueError("spmm: operands must be 2-D row-major")
+        if relu:
+            _check(_lib.cbm_b200_spmm_ex(self._h, x.data_ptr(), x.shape[0], x.shape[1], xs[0],
+                                         y.data_ptr(), y.shape[0], y.shape[1], ys[0], 1,
+                                         self._stream(stream)))
+            return
         _check(_lib.cbm_b200_spmm(self._h, x.data_ptr(), x.shape[0], x.shape[1], xs[0],
                                   y.data_ptr(), y.shape[0], y.shape[1], ys[0],
                                   self._stream(stream)))
 
-    def spmm(self, x, stream=None):
+    def spmm(self, x, stream=None, relu: bool = False):
         torch = _torch()
         y = torch.empty((self.n_rows, x.shape[1]), dtype=torch.float32, device=x.device)
-        self.spmm_into(x, y, stream)
+        self.spmm_into(x, y, stream, relu)
         return y
 
     def spmv_into(self, v, u, stream=None):

@@ -258,6 +258,21 @@ int cbm_b200_spmm(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_
   });
 }
 
+int cbm_b200_spmm_ex(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_cols,
+                     int64_t ldx, float* y, int64_t y_rows, int64_t y_cols, int64_t ldy,
+                     uint32_t flags, void* stream) {
+  return guard([&] {
+    need(h != nullptr, "spmm: null handle");
+    need((flags & ~CBM_B200_RELU) == 0, "spmm: unknown flags");
+    check_spmm_shapes(h->d->info, x_rows, x_cols, y_rows, y_cols, "spmm");
+    need(ldx >= x_cols && ldy >= y_cols, "spmm: leading dimension smaller than the width");
+    need((x || x_rows * x_cols == 0) && (y || y_rows * y_cols == 0), "spmm: null data");
+    std::lock_guard<std::mutex> lk(h->d->mu);
+    cbmb::device_spmm(h->d, x, ldx, uint32_t(x_cols), y, ldy, stream,
+                      (flags & CBM_B200_RELU) != 0);
+  });
+}
+
 int cbm_b200_spmm_host(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_cols,
                        float* y, int64_t y_rows, int64_t y_cols, void* stream) {
   return guard([&] {

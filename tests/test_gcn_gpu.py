@@ -63,3 +63,27 @@ def test_gcn_errors_mirror_reference():
     norm = P.DeviceCbm(P.build_cbm_normalized(a, 0))
     with pytest.raises(ValueError, match="feature rows must match nodes"):
         norm.gcn_forward(torch.zeros((4, 4), device="cuda"), w0, w1)
+
+
+def test_gcn_sharded_nccl_world1_bitwise():
+    """gcn_forward_sharded through NCCL (one rank here; the same code path
+    all-gathers the hidden slabs at N>1) equals gcn_forward bit for bit."""
+    import os
+    import torch.distributed as dist
+    from paper_2409_02208_b200.sharding import gcn_forward_sharded
+    a = P.generate_graph("community", [3000, 500, 0.8, 1e-4], 91)
+    c = P.build_cbm_normalized(a, 0, threads=8)
+    x = P.generate_dense("normal", 3000, 64, 92)
+    w0 = P.generate_dense("glorot", 64, 96, 93)
+    w1 = P.generate_dense("glorot", 96, 40, 94)
+    op = P.DeviceCbm(c, order_faithful=True)
+    want = op.gcn_forward(_t(x), _t(w0), _t(w1)).cpu().numpy()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        got = gcn_forward_sharded(op, _t(x), _t(w0), _t(w1)).cpu().numpy()
+    finally:
+        dist.destroy_process_group()
+    assert_bitwise(got, want, "sharded gcn")
+    assert_bitwise(got, O.oracle_gcn_forward(oracle_arrays(c), x, w0, w1), "vs oracle")

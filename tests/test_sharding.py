@@ -83,3 +83,61 @@ def test_gloo_world2_column_shards_reassemble_bitwise():
     x = P.generate_dense("normal", a.n_cols, 96, 6)
     want = O.oracle_spmm(oracle_arrays(c), x)
     assert np.array_equal(y.view(np.uint32), want.view(np.uint32))
+
+
+class _OracleCompute:
+    """Test stand-in for a rank's GPU: the oracle restatement on CPU tensors
+    (the product's compute is _DeviceCompute; this exercises the partition,
+    the all-gathers and the repacking)."""
+
+    def __init__(self, arrays):
+        self.arrays = arrays
+
+    def matmul(self, a, b):
+        return torch.from_numpy(O.oracle_dense_matmul(a.numpy(), b.contiguous().numpy()))
+
+    def spmm(self, x, relu=False):
+        y = O.oracle_spmm(self.arrays, np.ascontiguousarray(x.numpy()))
+        if relu:
+            y = np.where(y < 0, np.float32(0), y)
+        return torch.from_numpy(np.ascontiguousarray(y, np.float32))
+
+
+def _gcn_inputs():
+    a = P.generate_graph("community", [600, 50, 0.5, 0.01], 81)
+    c = P.build_cbm_normalized(a, 0)
+    x = P.generate_dense("normal", 600, 24, 82)
+    w0 = P.generate_dense("glorot", 24, 40, 83)
+    w1 = P.generate_dense("glorot", 40, 10, 84)
+    return c, x, w0, w1
+
+
+def _gcn_worker(rank, world, port, out):
+    from paper_2409_02208_b200.sharding import gcn_forward_sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c, x, w0, w1 = _gcn_inputs()
+    got = gcn_forward_sharded(None, torch.from_numpy(x), torch.from_numpy(w0),
+                              torch.from_numpy(w1), compute=_OracleCompute(oracle_arrays(c)))
+    out.put((rank, got.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_gcn_bitwise():
+    """Hidden-column shards + all-gather (gcn_forward_sharded) on 2 gloo ranks:
+    both ranks hold the single-device gcn_forward output bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gcn_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    results = dict(q.get(timeout=240) for _ in range(2))
+    for p_ in procs:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    c, x, w0, w1 = _gcn_inputs()
+    want = O.oracle_gcn_forward(oracle_arrays(c), x, w0, w1)
+    for r in range(2):
+        assert np.array_equal(results[r].view(np.uint32), want.view(np.uint32)), r
