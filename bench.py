@@ -345,6 +345,7 @@ def run_ours(args, wl):
                       "order_faithful": bool(args.order_faithful), "kernel": args.kernel,
                       "l2": "flushed (256 MiB write) before every timed step",
                       "levels": info["n_levels"], "chunk_items": info["n_chunk_items"],
+                      "actual_ops_per_step": int(sum(P.count_scalar_ops(c)) * d_local),
                       "build_s": t_build, "upload_s": t_upload},
            "roofline": roofline,
            "cpu_baseline": cpu,
