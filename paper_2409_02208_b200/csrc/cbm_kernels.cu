@@ -152,6 +152,7 @@ struct Params {
   uint32_t total_tickets, total_warps, epoch;
   uint32_t cta_stride;  // CTAs per residency round (grid / CTAs per SM)
   uint32_t relu;        // fused ReLU on Y (relu_inplace, dense.cpp:51-54) for the GCN
+  uint32_t faithful;    // order-faithful mode (spmv: sequential adds)
   uint64_t prefetch_bytes;  // > 0: X is one contiguous block of this size, pulled into L2 first
   unsigned long long* trace;  // dev tool (CBM_B200_TRACE): 4 x u64 per warp, else null
 };
@@ -556,6 +557,113 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   }
 }
 
+// ------------------------------------------------------------------ spmv
+// d = 1 (spmv_into / spmv, kernels.cpp:70-103). A column of width one leaves
+// 31 lanes idle in cbm_kernel, so here the 32 lanes take 32 consecutive
+// deltas of a ticket at once: column word, value and the gathered x element
+// are loaded in parallel. Order-faithful: the products are added to the
+// accumulator one by one in delta order (shuffled from their lanes, every
+// lane carrying the same accumulator), exactly as the reference. Default:
+// each lane accumulates its deltas (fma), then a fixed butterfly reduction.
+// Same tickets, schedule, flags, partials and epilogue as cbm_kernel.
+struct alignas(16) SpmvSmem {
+  TRec rec[kRecWin];
+};
+
+template <bool NORM, int SC>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_spmv_kernel(const Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  SpmvSmem& sm = reinterpret_cast<SpmvSmem*>(smem_raw)[threadIdx.x >> 5];
+  const uint32_t cta = blockIdx.x, wi = threadIdx.x >> 5;
+  const uint32_t w = (cta % p.cta_stride) * (p.total_warps / p.cta_stride) +
+                     (cta / p.cta_stride) * kWarpsPerCta + wi;
+  if (w >= p.total_warps) return;
+  uint32_t g = 0;
+  stage_recs(p, sm, w, 0);
+  stage_recs(p, sm, w, 32);
+  __syncwarp();
+  const uint32_t n_w = sm.rec[0].nw;
+  if (n_w == 0) return;
+  const bool faithful = SC == 1 || p.faithful;
+#pragma unroll 1
+  for (uint32_t ci = 0; ci < n_w; ++ci) {
+    if (ci - g == 32) {
+      __syncwarp();
+      stage_recs(p, sm, w, g + kRecWin);
+      g += 32;
+      __syncwarp();
+    }
+    const TRec r = sm.rec[ci & (kRecWin - 1)];
+    const uint32_t t = r.item;
+    float acc = 0.0f;   // faithful: the running sum (same on every lane)
+    float part = 0.0f;  // default: this lane's partial sum
+#pragma unroll 1
+    for (uint32_t k0 = r.beg; k0 < r.end; k0 += 32) {
+      const uint32_t n = min(32u, r.end - k0);
+      float xv = 0.0f, val = 0.0f;
+      if (uint32_t(lane) < n) {
+        const uint32_t cw = __ldg(p.dcol + k0 + lane);
+        xv = __ldg(p.x + (long long)(cw & 0x7FFFFFFFu) * p.ldx);
+        if constexpr (SC != 0) val = __ldg(p.dval + k0 + lane);
+        else val = __int_as_float(0x3F800000u | (cw & 0x80000000u));
+      }
+      if (faithful) {
+        // fl(v * x): exact for +-1 (a sign flip), the reference's rounded
+        // product for +-s_c; then ascending adds (kernels.cpp:18-24)
+        const float prod = __fmul_rn(val, xv);
+        for (uint32_t j = 0; j < n; ++j) acc = __fadd_rn(acc, __shfl_sync(kFull, prod, j));
+      } else {
+        part = __fmaf_rn(xv, val, part);  // idle lanes add 0 * 0
+      }
+    }
+    if (!faithful) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part = __fadd_rn(part, __shfl_xor_sync(kFull, part, o));
+      acc = part;
+    }
+    // ---- epilogue (cbm_kernel's, one column)
+    const uint32_t* flag_base = p.flags;
+    if (r.cnt) {  // + partial sums in order
+      for (uint32_t b0 = 0; b0 < r.cnt; b0 += 32) {
+        const uint32_t nb = min(32u, r.cnt - b0);
+        float pv = 0.0f;
+        if (uint32_t(lane) < nb) {
+          const uint32_t* f = flag_base + r.first + b0 + lane;
+          while (ld_acquire(f) != p.epoch) __nanosleep(128);
+          pv = __ldcg(p.partial + (size_t)(r.first + b0 + lane) * p.dpad);
+        }
+        for (uint32_t j = 0; j < nb; ++j) acc = __fadd_rn(acc, __shfl_sync(kFull, pv, j));
+      }
+    }
+    if (t < p.n_chunk) {
+      if (lane == 0) p.partial[(size_t)t * p.dpad] = acc;
+      publish(p.flags + t, p.epoch);
+      continue;
+    }
+    if (r.ppos != 0xFFFFFFFFu) {  // + unscaled parent (kernels.cpp:84-90)
+      await(flag_base + r.ppos, p.epoch);
+      const float* src =
+          NORM ? p.interior + (size_t)r.psrc * p.dpad : p.y + (long long)r.psrc * p.ldy;
+      acc = __fadd_rn(acc, __ldcg(src));
+    }
+    const uint32_t row = r.rowk & 0x7FFFFFFFu;
+    const bool is_parent = (r.rowk >> 31) != 0;
+    if constexpr (NORM) {
+      if (is_parent) {
+        if (lane == 0) p.interior[(size_t)r.slot * p.dpad] = acc;
+        publish(p.flags + t, p.epoch);
+      }
+      float yv = __fmul_rn(acc, __uint_as_float(r.srow));
+      if (p.relu) yv = relu1(yv);
+      if (lane == 0) p.y[(long long)row * p.ldy] = yv;
+    } else {
+      if (lane == 0) p.y[(long long)row * p.ldy] = p.relu ? relu1(acc) : acc;
+      if (is_parent) publish(p.flags + t, p.epoch);
+    }
+  }
+}
+
 // Gathers each warp's ticket records into its region of the ticket stream.
 __global__ void build_ticket_stream(const uint4* __restrict__ rec, const float* __restrict__ srow,
                                     const uint32_t* __restrict__ list,
@@ -684,17 +792,13 @@ __global__ void prescale_kernel(const float* __restrict__ x, long long ldx,
 
 // Cooperative launch: one full residency wave (all warps co-resident), no
 // more warps than tickets.
-template <int V, int U, int D, bool NORM, int SC>
-void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
-  constexpr size_t smem = kWarpsPerCta * sizeof(WarpSmem<V, U, D>);
-  static int bps = -1;  // per template instance
+void launch_coop(const void* kernel, size_t smem, int& bps, Params& p, uint64_t tickets,
+                 uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
   if (bps < 0) {
-    ck(cudaFuncSetAttribute(cbm_kernel<V, U, D, NORM, SC>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
        "smem attribute");
     int b = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cbm_kernel<V, U, D, NORM, SC>,
-                                                     kWarpsPerCta * 32, smem),
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kWarpsPerCta * 32, smem),
        "occupancy");
     bps = std::max(1, b);
   }
@@ -716,10 +820,22 @@ void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cu
   p.trec = reinterpret_cast<const uint4*>(sc.trec);
   p.wstride = sc.wstride;
   void* args[] = {&p};
-  ck(cudaLaunchCooperativeKernel(
-         reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SC>), dim3(grid),
-         dim3(kWarpsPerCta * 32), args, smem, s),
+  ck(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(kWarpsPerCta * 32), args, smem, s),
      "cbm_kernel cooperative launch");
+}
+
+template <int V, int U, int D, bool NORM, int SC>
+void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
+  static int bps = -1;  // per template instance
+  launch_coop(reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SC>),
+              kWarpsPerCta * sizeof(WarpSmem<V, U, D>), bps, p, tickets, slabs, h, s);
+}
+
+template <bool NORM, int SC>
+void launch_spmv(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
+  static int bps = -1;
+  launch_coop(reinterpret_cast<const void*>(&cbm_spmv_kernel<NORM, SC>),
+              kWarpsPerCta * sizeof(SpmvSmem), bps, p, tickets, 1, h, s);
 }
 
 template <int V, int U, int D>
@@ -1028,7 +1144,13 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     ck(cudaMemsetAsync(trace, 0, trace_n * 8, s), "trace");
     p.trace = trace;
   }
-  if (V == 4) {
+  p.faithful = L.order_faithful ? 1u : 0u;
+  if (d == 1) {  // spmv: lanes over deltas
+    if (!norm) launch_spmv<false, 0>(p, tickets, h, s);
+    else if (!scl) launch_spmv<true, 0>(p, tickets, h, s);
+    else if (L.order_faithful) launch_spmv<true, 1>(p, tickets, h, s);
+    else launch_spmv<true, 2>(p, tickets, h, s);
+  } else if (V == 4) {
     if (U == 4) run_kernel<4, 4, 4>(p, tickets, n_slabs, norm, scl, h, s);
     else if (U == 2) run_kernel<4, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
     else run_kernel<4, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);

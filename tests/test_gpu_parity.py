@@ -126,7 +126,8 @@ def test_random_suite_bitwise(normalized, kernel, dev):
         assert_bitwise(got, want, f"case {k} d={x.shape[1]}")
         got, h = gpu_spmm(c, x, dev, kernel=kernel)
         info = h.info()
-        if info["n_flattened"] or info["n_chunk_items"] or normalized:
+        # default mode: spmv (d = 1) sums a row's deltas lane-parallel
+        if info["n_flattened"] or info["n_chunk_items"] or normalized or x.shape[1] == 1:
             assert normwise_err(got, want) <= TOL, f"case {k}"
         else:
             assert_bitwise(got, want, f"default case {k}")
@@ -318,3 +319,31 @@ def test_spmm_sharded_host_buffers_bitwise(n_handles, dev):
     if n_handles > 1:
         with pytest.raises(ValueError, match="appears twice"):
             P.spmm_sharded([ops[0], ops[0]], x)
+
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_spmv_lane_parallel(normalized, dev):
+    """spmv (d = 1, kernels.cpp:70-103): the lane-per-delta kernel. Order-
+    faithful: bit-identical for any v (sequential adds). Default: bit-exact on
+    integer v for the binary matrix, 1e-5 normwise otherwise; with long rows
+    split into chunks and merge trees too."""
+    for kind, params, seed in (("community", [3000, 100, 0.3, 0.002], 101),
+                               ("pa_triangle", [4000, 2, 0.3], 102)):
+        a = P.generate_graph(kind, params, seed)
+        c = (P.build_cbm_normalized if normalized else P.build_cbm)(a, 0)
+        arrays = oracle_arrays(c)
+        for vkind in ("int", "normal"):
+            v = P.generate_dense(vkind, a.n_cols, 1, seed + 1, -8, 8)
+            want = O.oracle_spmm(arrays, v)
+            vt = torch.from_numpy(v).to(dev)
+            got = P.DeviceCbm(c, order_faithful=True).spmv(vt).cpu().numpy()
+            assert_bitwise(got, want, f"spmv faithful {kind} {vkind}")
+            for opts in ({}, {"split_threshold": 4, "chunk": 2}):
+                h = P.DeviceCbm(c, **opts)
+                got = h.spmv(vt).cpu().numpy()
+                if opts:
+                    assert h.info()["n_chunk_items"] > 0
+                if vkind == "int" and not normalized:
+                    assert_bitwise(got, want, f"spmv default {kind} {opts}")
+                else:
+                    assert normwise_err(got, want) <= TOL
