@@ -1198,25 +1198,42 @@ void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, 
     for (auto& e : h->ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   }
   const uint64_t bytes = (uint64_t(L.n_cols) + L.n_rows) * d * sizeof(float);
-  // column chunks of >= 64 floats (256-byte rows keep the 2D copies at ~53 GB/s;
-  // tools/ubench_pcie.cu): more chunks shorten the exposed first H2D / last D2H
+  // Column chunks (16-byte aligned): the first chunk's H2D and the last
+  // chunk's D2H cannot overlap anything, so those two are narrow (d/8) and
+  // the middle is cut in three (tools/probe_e2e.py: uniform x4 1109 us,
+  // x8 1151 us on cfg[1]; rows narrower than 64 floats slow the 2D copies).
+  std::vector<std::pair<uint32_t, uint32_t>> parts;  // (first column, width)
+  auto r4 = [](uint32_t v) { return (v + 3) & ~3u; };
   uint32_t chunks = 1;
-  if (bytes >= (8u << 20) && d >= 128) chunks = std::min<uint32_t>(kHostChunks, d / 64);
-  const uint32_t cw = ((d + chunks - 1) / chunks + 3) & ~3u;  // chunk width, 16-byte aligned
+  if (bytes >= (8u << 20) && d >= 128) chunks = d >= 256 ? 5 : 2;
+  if (const char* e = std::getenv("CBM_B200_HOST_CHUNKS"))  // dev tool: uniform chunks
+    chunks = std::max<uint32_t>(1, std::min<uint32_t>({kHostChunks, uint32_t(std::atoi(e)), d}));
+  if (chunks == 5 && !std::getenv("CBM_B200_HOST_CHUNKS")) {  // d >= 256
+    const uint32_t edge = r4(d / 8), rest = d - 2 * edge, mid = r4((rest + 2) / 3);
+    uint32_t c0 = 0;
+    const uint32_t m3 = (rest - 2 * mid) & ~3u;  // every chunk starts 16-byte aligned
+    for (uint32_t w : {edge, mid, mid, m3, d - edge - 2 * mid - m3}) {
+      parts.emplace_back(c0, w);
+      c0 += w;
+    }
+  } else {
+    const uint32_t cw = r4((d + chunks - 1) / chunks);
+    for (uint32_t c0 = 0; c0 < d; c0 += cw) parts.emplace_back(c0, std::min(cw, d - c0));
+  }
   // ev[0]: caller's prior work on s; ev[1+k]: X chunk k landed; ev[1+C+k]: Y chunk k ready
   ck(cudaEventRecord(h->ev[0], s), "event");
   ck(cudaStreamWaitEvent(h->s_in, h->ev[0], 0), "wait");
   ck(cudaStreamWaitEvent(h->s_out, h->ev[0], 0), "wait");
-  for (uint32_t k = 0, c0 = 0; c0 < d; ++k, c0 += cw) {
-    const uint32_t w = std::min(cw, d - c0);
+  for (size_t k = 0; k < parts.size(); ++k) {
+    const auto [c0, w] = parts[k];
     ck(cudaMemcpy2DAsync(h->xstage + c0, dpad * sizeof(float), x + c0, ldx * sizeof(float),
                          w * sizeof(float), L.n_cols, cudaMemcpyHostToDevice, h->s_in),
        "H2D X");
     ck(cudaEventRecord(h->ev[1 + k], h->s_in), "event");
   }
   uint32_t launches = 0;
-  for (uint32_t k = 0, c0 = 0; c0 < d; ++k, c0 += cw) {
-    const uint32_t w = std::min(cw, d - c0);
+  for (size_t k = 0; k < parts.size(); ++k) {
+    const auto [c0, w] = parts[k];
     ck(cudaStreamWaitEvent(s, h->ev[1 + k], 0), "wait");
     device_spmm(h, h->xstage + c0, dpad, w, h->ystage + c0, dpad, stream, false);
     launches += h->last_launches;

@@ -1,7 +1,9 @@
-"""Dev tool: kernel time vs (split_threshold, chunk) upload options.
+"""Dev tool: kernel time vs DeviceCbm upload options.
 
 Usage: python tools/probe_split.py cfg3,cfg2 "32:32,128:32,256:64,1024:128"
+       python tools/probe_split.py cfg1 '[{"max_segments": 2}, {}]'   (JSON option dicts)
 """
+import json
 import os
 import sys
 
@@ -32,7 +34,11 @@ def timeit(op, x, y, flush, reps=20):
 def main():
     dev = torch.device("cuda:0")
     flush = torch.empty(64 << 20, device=dev)
-    grid = [tuple(int(v) for v in g.split(":")) for g in sys.argv[2].split(",")]
+    if sys.argv[2].lstrip().startswith("["):
+        grid = json.loads(sys.argv[2])
+    else:
+        grid = [dict(zip(("split_threshold", "chunk"), (int(v) for v in g.split(":"))))
+                for g in sys.argv[2].split(",")]
     for name in sys.argv[1].split(","):
         wl = WORKLOADS[name]
         a = wl.graph()
@@ -40,15 +46,15 @@ def main():
         x = torch.from_numpy(wl.operand(a.n_cols)).to(dev)
         y = torch.empty((a.n_rows, wl.d), device=dev)
         ref = None
-        for split, chunk in grid:
-            op = P.DeviceCbm(c, split_threshold=split, chunk=chunk)
+        for opts in grid:
+            op = P.DeviceCbm(c, **opts)
             t = timeit(op, x, y, flush)
             got = y.clone()
             if ref is None:
                 ref = got
             err = float((got - ref).abs().max() / ref.abs().max())
             info = op.info()
-            print(f"{name} split={split:5d} chunk={chunk:4d}: {t:9.1f} us  items={info['n_items']} "
+            print(f"{name} {json.dumps(opts):45s}: {t:9.1f} us  items={info['n_items']} "
                   f"chunks={info['n_chunk_items']} launches={info['launches_per_call']} "
                   f"err_vs_first={err:.2e}", flush=True)
             op.close()
