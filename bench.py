@@ -330,9 +330,35 @@ def run_ours(args, wl):
                    "note": "uncompressed matrix through the same kernel (every parent virtual)"}
         del csr_op
 
+    # spmv (d = 1, the lane-per-delta kernel) on the same matrix: reported
+    # beside the headline, with the reference's spmv_into on the host cores
+    spmv = None
+    if rank == 0:
+        v = torch.from_numpy(wl.operand(a.n_cols, 1)).to(dev)
+        u = torch.empty((a.n_rows, 1), dtype=torch.float32, device=dev)
+        op.reserve(1)
+        for _ in range(3):
+            op.spmv_into(v, u, stream)
+        torch.cuda.synchronize()
+        t_v = []
+        for i in range(min(args.steps, 50)):
+            flush.fill_(float(i))
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            op.spmv_into(v, u, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t_v.append(e0.elapsed_time(e1))
+        spmv_ms = float(statistics.mean(t_v))
+        spmv = {"ms_per_call": spmv_ms, "value": 2.0 * nnz / (spmv_ms * 1e-3) / 1e9,
+                "unit": UNIT, "kernel": "cbm_spmv_kernel", "l2": "flushed before every call"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, wl, c, nnz)
+        if spmv is not None and cpu is not None:
+            spmv["cpu_reference"] = cpu_spmv(args, wl, c, nnz)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
@@ -350,6 +376,7 @@ def run_ours(args, wl):
            "roofline": roofline,
            "cpu_baseline": cpu,
            "gpu_csr_comparator": gpu_csr,
+           "spmv": spmv,
            "e2e": {"value": e2e_value, "unit": UNIT,
                    "h2d_bytes_per_step": int(a.n_cols * d_local * 4),
                    "d2h_bytes_per_step": int(a.n_rows * d_local * 4),
@@ -378,6 +405,18 @@ def cpu_baseline(args, wl, c, nnz):
             "kind": "reference",
             "sample": f"full {wl.name} multiply (reference spmm_into, f32 build) x {runs} calls "
                       f"after 1 warm-up, {t * 1e3:.2f} ms/call"}
+
+
+def cpu_spmv(args, wl, c, nnz):
+    """The reference's spmv_into on this host (oracle/_ref), same CBM, d = 1."""
+    import oracle as O
+    rc = O.RefCbm.from_arrays(O.RefCbmArrays(c.n_rows, c.n_cols, c.alpha, c.is_normalized,
+                                             c.parent, c.row_ptr, c.col_idx, c.values,
+                                             c.row_scale))
+    v = wl.operand(c.n_cols, 1)
+    t, runs = rc.time_spmv(v, args.threads, 3, min(2.0, args.cpu_seconds))
+    return {"value": 2.0 * nnz / t / 1e9, "unit": UNIT, "cores": args.threads,
+            "kind": "reference", "sample": f"spmv_into x {runs} calls, {t * 1e3:.3f} ms/call"}
 
 
 def main():

@@ -21,6 +21,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "cbm/builder.hpp"
 #include "cbm/dense.hpp"
@@ -112,6 +113,17 @@ inline DenseMatrix spmv(const DeviceCbm& c, const DenseMatrix& v, int threads = 
   DenseMatrix out(c.n_rows(), 1);
   spmv_into(c, v, out, threads);
   return out;
+}
+
+// Column-sharded spmm_into over several devices: one DeviceCbm
+// of the same CbmMatrix per device; slab k of the columns runs on shards[k].
+// Bit-identical to the single-device result.
+inline void spmm_sharded_into(const std::vector<const DeviceCbm*>& shards, const DenseMatrix& b,
+                              DenseMatrix& out) {
+  std::vector<cbm_b200_matrix*> hs;
+  for (const DeviceCbm* d : shards) hs.push_back(d->handle());
+  check(cbm_b200_spmm_sharded(hs.data(), int32_t(hs.size()), b.data.data(), b.n_rows, b.n_cols,
+                              out.data.data(), out.n_rows, out.n_cols));
 }
 
 // One-shot overloads with the reference's exact signatures: upload, multiply.

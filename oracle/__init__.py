@@ -382,15 +382,19 @@ class RefCbm:
         _check(lib, lib.ref_spmm_sequential(self.h, x, x.shape[0], x.shape[1], y))
         return y
 
-    def time_spmm(self, x, threads, runs, min_seconds=0.0):
+    def time_spmm(self, x, threads, runs, min_seconds=0.0, kind=0):
+        """Mean seconds per reference spmm_into (kind 0) or spmv_into (kind 2)."""
         lib = ref()
         x = np.ascontiguousarray(x, np.float32)
         done = C.c_int()
-        t = lib.ref_time(0, self.h, x, x.shape[0], x.shape[1], threads, runs, min_seconds,
+        t = lib.ref_time(kind, self.h, x, x.shape[0], x.shape[1], threads, runs, min_seconds,
                          C.byref(done))
         if t < 0:
             raise RefError(_err(lib))
         return t, done.value
+
+    def time_spmv(self, v, threads, runs, min_seconds=0.0):
+        return self.time_spmm(v, threads, runs, min_seconds, kind=2)
 
     def gcn_forward(self, x, w0, w1, threads=1):
         lib = ref()

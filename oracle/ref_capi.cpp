@@ -261,7 +261,19 @@ double ref_time(int kind, void* h, const float* x, uint32_t rows,
   double result = -1.0;
   guard([&] {
     const auto b = dense_from(x, rows, cols);
-    if (kind == 0) {
+    if (kind == 2) {  // spmv_into (kernels.cpp:70-97), cols == 1
+      const auto& c = *static_cast<cbm::CbmMatrix*>(h);
+      cbm::DenseMatrix out(c.n_rows, 1);
+      cbm::spmv_into(c, b, out, threads);
+      const auto t0 = Clock::now();
+      int r = 0;
+      while (r < runs || since(t0) < min_seconds) {
+        cbm::spmv_into(c, b, out, threads);
+        ++r;
+      }
+      result = since(t0) / r;
+      *runs_done = r;
+    } else if (kind == 0) {
       const auto& c = *static_cast<cbm::CbmMatrix*>(h);
       cbm::DenseMatrix out(c.n_rows, cols);
       cbm::spmm_into(c, b, out, threads);

@@ -38,6 +38,8 @@ __all__ = [
 VIRTUAL_PARENT = 0xFFFFFFFF
 _HERE = os.path.dirname(os.path.abspath(__file__))
 library_path = os.path.join(_HERE, "libcbm_b200.so")
+if os.environ.get("CBM_B200_LIB"):  # dev tool: A/B a second in-tree build of the library
+    library_path = os.path.join(_HERE, os.path.basename(os.environ["CBM_B200_LIB"]))
 
 if not os.path.exists(library_path):
     raise ImportError(

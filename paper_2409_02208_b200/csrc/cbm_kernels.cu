@@ -155,6 +155,7 @@ struct Params {
   uint32_t faithful;    // order-faithful mode (spmv: sequential adds)
   uint64_t prefetch_bytes;  // > 0: X is one contiguous block of this size, pulled into L2 first
   unsigned long long* trace;  // dev tool (CBM_B200_TRACE): 4 x u64 per warp, else null
+  uint32_t ldx32;             // ldx in floats (< 2^31): 32x32->64 address multiply
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -218,20 +219,39 @@ __device__ __forceinline__ void add_partials(const Params& p, const uint32_t* fl
 }
 
 // cp.async (LDGSTS) helpers: each lane copies its own V floats of an X row
-// into its own slice of a shared-memory slot.
+// into its own slice of a shared-memory slot (16 B: through L2 only, L1 reuse
+// measured nil).
+// Predicated form: `on` = false copies nothing and zero-fills the lane's slot
+// (src-size 0), so a ring group is always written in full without a branch.
 template <int V>
-__device__ __forceinline__ void cp_async(float* dst, const float* src) {
+__device__ __forceinline__ void cp_async_n(float* dst, const float* src, uint32_t n) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-  if constexpr (V == 4)  // 16 B: stream through L2 only (L1 reuse measured nil)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(V * 4)
+  if constexpr (V == 4)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n)
                  : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(V * 4),
+                 "r"(n)
+                 : "memory");
+}
+template <int V>
+__device__ __forceinline__ void cp_async_z(float* dst, const float* src, bool on) {
+  cp_async_n<V>(dst, src, on ? uint32_t(V * 4) : 0u);
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// Wait until at most n (<= N) of the most recently committed groups are pending.
+template <int N>
+__device__ __forceinline__ void cp_wait_upto(uint32_t n) {
+  if constexpr (N == 0) {
+    cp_wait<0>();
+  } else {
+    if (n >= uint32_t(N)) cp_wait<N>();
+    else cp_wait_upto<N - 1>(n);
+  }
 }
 // relu_inplace (dense.cpp:51-54): v < 0 -> +0, everything else (-0.0 too) kept
 __device__ __forceinline__ float relu1(float v) { return v < 0.0f ? 0.0f : v; }
@@ -370,8 +390,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   // ---- issue cursor: ticket ii, offset iq inside it. win = window of ii,
   // wn1 / wn2 = windows of ii+1 / ii+2 (fetched two tickets ahead)
   uint32_t ii = 0, iq = 0, ibeg = 0, ilen = 0, icol = 0, imask = 0;
+  bool ifull = true;  // warp-uniform: every segment of every lane inside the matrix
   Wd win = window(0), wn1 = window(1), wn2 = window(2), wlong{0u, 0.0f};
-  uint32_t iseq = 0;   // deltas issued
+  uint32_t iseq = 0;     // ring slots issued (B per group)
+  uint32_t icommit = 0;  // ring groups committed; the consumer's k-th group is the k-th
+  uint32_t cgroup = 0;   // groups consumed
   float vring = 0.0f;  // lane s: signed value of the delta in ring slot s
   bool iblocked = false;
   auto load_ticket = [&]() {  // cursor fields of ticket ii (window already in win)
@@ -384,6 +407,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (icol + uint32_t(u) * kSeg < p.d) imask |= 1u << u;
+    ifull = __all_sync(kFull, imask == (1u << U) - 1u);
     wlong = fetch(ibeg + 32, r.end);
   };
   // step to the next ticket with deltas, shifting the window prefetch;
@@ -412,20 +436,36 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     if (!iblocked && ii < n_w) {
       const uint32_t n = min(uint32_t(B), ilen - iq);
       const uint32_t s0 = iseq & (D - 1);  // a multiple of B
+      // all B column words / values first (no shuffle under a branch), then
+      // B predicated copies: slots past the ticket's end are zero-filled with
+      // value 0, so the consumer adds exact zeros there (acc is never -0)
+      uint32_t cwb[B];
+      float vb[B];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        if (uint32_t(b) < n) {
-          const uint32_t cw = __shfl_sync(kFull, win.c, (iq + b) & 31);
-          const float* src = p.x + (long long)(cw & 0x7FFFFFFFu) * p.ldx + icol;
+        cwb[b] = __shfl_sync(kFull, win.c, (iq + b) & 31);
+        if constexpr (SC != 0) vb[b] = __shfl_sync(kFull, win.v, (iq + b) & 31);
+      }
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if ((imask >> u) & 1u) cp_async<V>(&sm.ring[s0 + b][u][lane * V], src + u * kSeg);
-          // the delta's signed value (the reference's values[k], kernels.cpp:33)
-          float val;
-          if constexpr (SC != 0) val = __shfl_sync(kFull, win.v, (iq + b) & 31);
-          else val = __int_as_float(0x3F800000u | (cw & 0x80000000u));
-          if (uint32_t(lane) == s0 + b) vring = val;
+      for (int b = 0; b < B; ++b) {
+        const bool on = uint32_t(b) < n;
+        const uint32_t c = on ? (cwb[b] & 0x7FFFFFFFu) : 0u;
+        const float* src = p.x + (uint64_t)c * p.ldx32 + icol;
+        if (ifull) {  // one size for all segments, immediate segment offsets
+          const uint32_t sz = on ? uint32_t(V * 4) : 0u;
+#pragma unroll
+          for (int u = 0; u < U; ++u) cp_async_n<V>(&sm.ring[s0 + b][u][lane * V], src + u * kSeg, sz);
+        } else {  // the matrix edge: out-of-range segments copy nothing
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool ok = on && ((imask >> u) & 1u);
+            cp_async_z<V>(&sm.ring[s0 + b][u][lane * V], ok ? src + u * kSeg : p.x, ok);
+          }
         }
+        // the delta's signed value (the reference's values[k], kernels.cpp:33)
+        float val = SC != 0 ? vb[b] : __int_as_float(0x3F800000u | (cwb[b] & 0x80000000u));
+        if (!on) val = 0.0f;
+        if (uint32_t(lane) == s0 + b) vring = val;
       }
       iseq += B;
       iq += n;
@@ -435,17 +475,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
         win = wlong;
         wlong = fetch(ibeg + iq + 32, ibeg + ilen);
       }
+      cp_commit();  // only real groups are committed: group k is the consumer's k-th
+      ++icommit;
     }
-    cp_commit();
+  };
+  // keep G groups in flight (after a consumed group, and when the issue
+  // cursor resumes after waiting for the record window to slide)
+  auto refill = [&]() {
+    while (icommit - cgroup < uint32_t(G) && !iblocked && ii < n_w) issue_group();
   };
 
   if (R(0).end != R(0).beg) load_ticket();
   else next_ticket();
-#pragma unroll 1
-  for (int q = 0; q < G; ++q) issue_group();
+  refill();
 
   uint32_t cseq = 0;  // deltas consumed
-  unsigned long long t_first = 0ull;
 #pragma unroll 1
   for (uint32_t ci = 0; ci < n_w; ++ci) {
     if (ci - g == 32) {  // slide the record window by one group
@@ -456,6 +500,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       if (iblocked) {
         iblocked = false;
         next_ticket();
+        refill();
       }
     }
     const uint32_t k_ci = ci & (kRecWin - 1);
@@ -470,9 +515,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     // matrix read stale ring bytes into accumulators that are never stored.
 #pragma unroll 1
     for (uint32_t k = r.beg; k < r.end; k += B) {
-      const uint32_t nb = min(uint32_t(B), r.end - k);
-      cp_wait<G - 1>();  // this lane's copies of the group have landed
-      if (p.trace && t_first == 0ull) t_first = globaltimer();
+      // this group was committed (the issue cursor is never behind the
+      // consumer: it only stops at a record-window edge the consumer reaches
+      // first); wait until its copies have landed
+      if (icommit <= cgroup) __trap();
+      cp_wait_upto<G - 1>(icommit - 1 - cgroup);
       const uint32_t s0 = cseq & (D - 1);
       float sc[B];
       T4 v[B][U];
@@ -484,17 +531,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       }
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        if (uint32_t(b) < nb) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if constexpr (SC == 1) acc[u] = W::add(acc[u], W::mul(v[b][u], sc[b]));
-            else acc[u] = fma_sign<V>(acc[u], v[b][u], sc[b]);
-          }
+        for (int u = 0; u < U; ++u) {
+          if constexpr (SC == 1) acc[u] = W::add(acc[u], W::mul(v[b][u], sc[b]));
+          else acc[u] = fma_sign<V>(acc[u], v[b][u], sc[b]);
         }
       }
       cseq += B;
+      ++cgroup;
       __syncwarp();  // the group's slots are fully read before their refill
-      issue_group();
+      refill();
     }
     // ---- epilogue: partials, then CHUNK/MERGE publish or ROW stage 2 + 3
     uint32_t* flag_base = p.flags + (size_t)slab * p.n_items;
@@ -550,7 +596,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
     unsigned long long* o = p.trace + 4 * (size_t)w;
     o[0] = t_start;
-    o[1] = t_first;
+    o[1] = 0ull;  // (first-data stamp removed from the hot loop)
     o[2] = globaltimer();
     o[3] = (unsigned long long)smid | ((unsigned long long)n_w << 16) |
            ((unsigned long long)cseq << 32);
@@ -599,22 +645,39 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_spmv_kernel(const Param
     float acc = 0.0f;   // faithful: the running sum (same on every lane)
     float part = 0.0f;  // default: this lane's partial sum
 #pragma unroll 1
-    for (uint32_t k0 = r.beg; k0 < r.end; k0 += 32) {
-      const uint32_t n = min(32u, r.end - k0);
-      float xv = 0.0f, val = 0.0f;
-      if (uint32_t(lane) < n) {
-        const uint32_t cw = __ldg(p.dcol + k0 + lane);
-        xv = __ldg(p.x + (long long)(cw & 0x7FFFFFFFu) * p.ldx);
-        if constexpr (SC != 0) val = __ldg(p.dval + k0 + lane);
-        else val = __int_as_float(0x3F800000u | (cw & 0x80000000u));
+    // batches of K blocks of 32 deltas: all K index loads, then all K
+    // gathers are in flight together (two latencies per batch, not per block)
+    constexpr int K = 8;
+#pragma unroll 1
+    for (uint32_t k0 = r.beg; k0 < r.end; k0 += 32 * K) {
+      uint32_t cw[K];
+      float val[K], xv[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        const uint32_t k = k0 + 32u * q + lane;
+        const bool on = k < r.end;
+        cw[q] = on ? __ldg(p.dcol + k) : 0u;
+        if constexpr (SC != 0) val[q] = on ? __ldg(p.dval + k) : 0.0f;
       }
-      if (faithful) {
-        // fl(v * x): exact for +-1 (a sign flip), the reference's rounded
-        // product for +-s_c; then ascending adds (kernels.cpp:18-24)
-        const float prod = __fmul_rn(val, xv);
-        for (uint32_t j = 0; j < n; ++j) acc = __fadd_rn(acc, __shfl_sync(kFull, prod, j));
-      } else {
-        part = __fmaf_rn(xv, val, part);  // idle lanes add 0 * 0
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        const bool on = k0 + 32u * q + lane < r.end;
+        xv[q] = on ? __ldg(p.x + (uint64_t)(cw[q] & 0x7FFFFFFFu) * p.ldx32) : 0.0f;
+        if constexpr (SC == 0) val[q] = on ? __int_as_float(0x3F800000u | (cw[q] & 0x80000000u)) : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        const uint32_t kb = k0 + 32u * q;
+        if (kb >= r.end) break;
+        if (faithful) {
+          // fl(v * x): exact for +-1 (a sign flip), the reference's rounded
+          // product for +-s_c; then ascending adds (kernels.cpp:18-24)
+          const float prod = __fmul_rn(val[q], xv[q]);
+          const uint32_t n = min(32u, r.end - kb);
+          for (uint32_t j = 0; j < n; ++j) acc = __fadd_rn(acc, __shfl_sync(kFull, prod, j));
+        } else {
+          part = __fmaf_rn(xv[q], val[q], part);  // idle lanes add 0 * 0
+        }
       }
     }
     if (!faithful) {
@@ -1064,6 +1127,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   h->last_launches = 0;
   if (L.n_rows == 0 || d == 0) return;
+  if (ldx >= (int64_t(1) << 31)) throw invalid_argument("spmm: leading dimension too large");
   ck(cudaSetDevice(h->device), "cudaSetDevice");
   device_reserve(h, d, stream);
   auto& ws = h->ws[stream];
@@ -1145,6 +1209,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     p.trace = trace;
   }
   p.faithful = L.order_faithful ? 1u : 0u;
+  p.ldx32 = uint32_t(ldin);
   if (d == 1) {  // spmv: lanes over deltas
     if (!norm) launch_spmv<false, 0>(p, tickets, h, s);
     else if (!scl) launch_spmv<true, 0>(p, tickets, h, s);

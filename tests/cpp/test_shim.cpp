@@ -121,6 +121,19 @@ int main() {
       CHECK(bitwise(b200::spmm(fast, bi), spmm(c, bi)));
     }
   }
+  // column-sharded multiply over several uploads (one per device in production)
+  {
+    auto a = community_graph(30, 40, 40, 1, 0xBEEF);
+    auto c = build_cbm_normalized(a, 0);
+    b200::DeviceCbm s0(c, 0), s1(c, 0), s2(c, 0);
+    auto b = random_dense(a.n_cols, 100, -1.0, 1.0, 77);
+    DenseMatrix out(c.n_rows, 100);
+    b200::spmm_sharded_into({&s0, &s1, &s2}, b, out);
+    CHECK(bitwise(out, spmm(c, b)));
+    DenseMatrix bad(c.n_rows, 3);
+    CHECK_THROWS_AS(b200::spmm_sharded_into({&s0, &s1}, DenseMatrix(4, 3), bad),
+                    std::invalid_argument);
+  }
   std::printf("test_shim: %d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

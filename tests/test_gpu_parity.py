@@ -347,3 +347,55 @@ def test_spmv_lane_parallel(normalized, dev):
                     assert_bitwise(got, want, f"spmv default {kind} {opts}")
                 else:
                     assert normwise_err(got, want) <= TOL
+
+
+@pytest.mark.parametrize("d", [1100, 2048])
+def test_wide_operands_span_several_slabs(d, dev):
+    """d > 512: several 512-column slabs per item (plus a partial one), each
+    with its own ready flags; faithful bitwise, default integer bitwise."""
+    a = P.generate_graph("community", [1500, 100, 0.4, 0.003], 111)
+    c = P.build_cbm(a, 0)
+    arrays = oracle_arrays(c)
+    xi = P.generate_dense("int", 1500, d, 112, -8, 8)
+    xg = P.generate_dense("normal", 1500, d, 113)
+    got, _ = gpu_spmm(c, xg, dev, order_faithful=True)
+    assert_bitwise(got, O.oracle_spmm(arrays, xg), f"faithful d={d}")
+    got, _ = gpu_spmm(c, xi, dev)
+    assert_bitwise(got, O.oracle_spmm(arrays, xi), f"default int d={d}")
+
+
+@pytest.mark.parametrize("sprinkle", [0, 7])
+def test_long_runs_of_empty_tickets(sprinkle, dev):
+    """Rows equal to their parent have no deltas. Long runs of such tickets
+    let the issue cursor run past the staged record window, stall there and
+    resume (refilling the copy ring) when the window slides. 400k rows in
+    chains of 100: one 20-delta root per chain, every `sprinkle`-th chain row
+    one fresh delta."""
+    rng = np.random.default_rng(131)
+    n, n_cols, chain = 400_000, 6000, 100
+    parent = np.empty(n, np.uint32)
+    counts = np.zeros(n, np.int64)
+    cols = []
+    for r0 in range(0, n, chain):
+        parent[r0] = 0xFFFFFFFF
+        root_cols = np.sort(rng.choice(1000, 20, replace=False)).astype(np.uint32)
+        cols.append(root_cols)
+        counts[r0] = 20
+        nxt = 1000
+        for j in range(1, chain):
+            parent[r0 + j] = r0 + j - 1
+            if sprinkle and j % sprinkle == 0:
+                cols.append(np.array([nxt + int(rng.integers(0, 40))], np.uint32))
+                nxt += 50
+                counts[r0 + j] = 1
+    row_ptr = np.zeros(n + 1, np.uint64)
+    row_ptr[1:] = np.cumsum(counts)
+    col_idx = np.concatenate(cols).astype(np.uint32)
+    vals = np.ones(col_idx.shape[0], np.float32)
+    c = P.CbmMatrix(n, n_cols, 0, False, parent, row_ptr, col_idx, vals)
+    arrays = oracle_arrays(c)
+    x = P.generate_dense("int", n_cols, 64, 132, -8, 8)
+    want = O.oracle_spmm(arrays, x)
+    for faithful in (True, False):
+        got, _ = gpu_spmm(c, x, dev, order_faithful=faithful)
+        assert_bitwise(got, want, f"empty runs faithful={faithful}")
