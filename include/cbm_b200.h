@@ -176,8 +176,9 @@ int cbm_b200_spmm_host(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64
 /* Column sharding: every stage of the multiply acts on one
  * column (kernels.cpp:27-62), so device k of n multiplies the contiguous
  * column slab cbm_b200_column_slab(d, n, k) against a full replica of the
- * CBM; no collective is needed and the slabs are bit-identical to the
- * single-device result. */
+ * CBM; no collective is needed. Order-faithful handles give the single-device
+ * bits; default-mode slabs may round differently (the kernel variant follows
+ * the slab width) within the same tolerance. */
 int cbm_b200_column_slab(int64_t d, int32_t world, int32_t rank, int64_t* lo, int64_t* hi);
 
 /* Single-process multi-device spmm_into on HOST buffers: handles[k] (one

@@ -285,6 +285,18 @@ __device__ __forceinline__ typename Vec<V>::T xor_sign(typename Vec<V>::T v, uin
 // fl(acc - v) (signed zeros included) -- the reference's stage-1 step for a
 // +-1 delta value (kernels.cpp:30-35).
 template <int V>
+__device__ __forceinline__ typename Vec<V>::T shfl_xor_v(typename Vec<V>::T v, uint32_t off) {
+  if constexpr (V == 4) {
+    return make_float4(__shfl_xor_sync(kFull, v.x, off), __shfl_xor_sync(kFull, v.y, off),
+                       __shfl_xor_sync(kFull, v.z, off), __shfl_xor_sync(kFull, v.w, off));
+  } else if constexpr (V == 2) {
+    return make_float2(__shfl_xor_sync(kFull, v.x, off), __shfl_xor_sync(kFull, v.y, off));
+  } else {
+    return __shfl_xor_sync(kFull, v, off);
+  }
+}
+
+template <int V>
 __device__ __forceinline__ typename Vec<V>::T fma_sign(typename Vec<V>::T acc,
                                                        typename Vec<V>::T v, float sg) {
   if constexpr (V == 4) {
@@ -335,11 +347,19 @@ __device__ __forceinline__ void stage_recs(const Params& p, SM& sm, uint32_t w, 
 //   0  +-1 (binary, or normalized with a pre-scaled X): fma(x, +-1, acc), exact
 //   1  +-s_c, order-faithful: fl(acc + fl(+-s_c * x)), the reference's two roundings
 //   2  +-s_c, default mode: fma(x, +-s_c, acc), one rounding (within tolerance)
-template <int V, int U, int D, bool NORM, int SC>
+// H: deltas per warp instruction. H = 1: the 32 lanes span one X row segment.
+//   H = 2 / 4 (narrow X, default mode only): the warp splits into H lane
+//   groups, each takes every H-th delta of the ticket, and the H partial sums
+//   are combined once per ticket by a fixed shuffle tree (summation order
+//   changes; integer sums stay exact).
+template <int V, int U, int D, bool NORM, int SC, int H = 1>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) {
   using W = Vec<V>;
   using T4 = typename W::T;
-  constexpr uint32_t kSeg = 32u * V;      // floats of one segment (one LDGSTS per lane)
+  static_assert(H == 1 || (U == 1 && SC != 1), "lane groups: one segment, default mode");
+  static_assert(D * H <= 32, "one value-ring lane per (slot, lane group)");
+  constexpr uint32_t kLanes = 32u / H;    // lanes per delta
+  constexpr uint32_t kSeg = kLanes * V;   // floats of one segment (one LDGSTS per lane)
   constexpr uint32_t kSlab = kSeg * U;    // floats per ticket
   constexpr int PFp = U >= 4 ? 2 : (U == 2 ? 4 : 8);
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
@@ -347,8 +367,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   // time (a group never spans two tickets; its unused slots stay idle)
   constexpr int B = D >= 8 ? 4 : 2;
   constexpr int G = D / B;  // groups in flight
+  constexpr uint32_t kGroup = uint32_t(B) * H;  // deltas per ring group
+  static_assert(32 % kGroup == 0, "a ring group never spans two index windows");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
+  const uint32_t hl = uint32_t(lane) / kLanes;          // lane group
+  const uint32_t jv = (uint32_t(lane) % kLanes) * V;    // column offset in a segment
   using SM = WarpSmem<V, U, D>;
   SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
   // warp -> position in the round-robin: CTAs b, b+G, b+2G, ... (G = p.cta_stride,
@@ -402,7 +426,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     const TRec& r = R(ii);
     ibeg = r.beg;
     ilen = r.end - r.beg;
-    icol = r.slab * kSlab + uint32_t(lane) * V;
+    icol = r.slab * kSlab + jv;
     imask = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -434,21 +458,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   };
   auto issue_group = [&]() {
     if (!iblocked && ii < n_w) {
-      const uint32_t n = min(uint32_t(B), ilen - iq);
+      const uint32_t n = min(kGroup, ilen - iq);
       const uint32_t s0 = iseq & (D - 1);  // a multiple of B
       // all B column words / values first (no shuffle under a branch), then
       // B predicated copies: slots past the ticket's end are zero-filled with
       // value 0, so the consumer adds exact zeros there (acc is never -0)
+      // slot s0 + b holds deltas b*H + h of the group, lane group h each
       uint32_t cwb[B];
       float vb[B];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        cwb[b] = __shfl_sync(kFull, win.c, (iq + b) & 31);
-        if constexpr (SC != 0) vb[b] = __shfl_sync(kFull, win.v, (iq + b) & 31);
+        cwb[b] = __shfl_sync(kFull, win.c, (iq + uint32_t(b) * H + hl) & 31);
+        if constexpr (SC != 0 && H == 1) vb[b] = __shfl_sync(kFull, win.v, (iq + b) & 31);
       }
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        const bool on = uint32_t(b) < n;
+        const bool on = uint32_t(b) * H + hl < n;
         const uint32_t c = on ? (cwb[b] & 0x7FFFFFFFu) : 0u;
         const float* src = p.x + (uint64_t)c * p.ldx32 + icol;
         if (ifull) {  // one size for all segments, immediate segment offsets
@@ -462,10 +487,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
             cp_async_z<V>(&sm.ring[s0 + b][u][lane * V], ok ? src + u * kSeg : p.x, ok);
           }
         }
-        // the delta's signed value (the reference's values[k], kernels.cpp:33)
-        float val = SC != 0 ? vb[b] : __int_as_float(0x3F800000u | (cwb[b] & 0x80000000u));
-        if (!on) val = 0.0f;
-        if (uint32_t(lane) == s0 + b) vring = val;
+        // the delta's signed value (the reference's values[k], kernels.cpp:33),
+        // held by lane (s0 + b) * H + h of the value ring
+        if constexpr (H == 1) {
+          float val = SC != 0 ? vb[b] : __int_as_float(0x3F800000u | (cwb[b] & 0x80000000u));
+          if (!on) val = 0.0f;
+          if (uint32_t(lane) == s0 + b) vring = val;
+        } else {
+          const uint32_t hh = uint32_t(lane) - (s0 + b) * H;  // < H on the holder lanes
+          const uint32_t q = uint32_t(b) * H + (hh < H ? hh : 0u);
+          float val;
+          if constexpr (SC != 0) {
+            val = __shfl_sync(kFull, win.v, (iq + q) & 31);
+          } else {
+            const uint32_t cv = __shfl_sync(kFull, win.c, (iq + q) & 31);
+            val = __int_as_float(0x3F800000u | (cv & 0x80000000u));
+          }
+          if (hh < H) vring = q < n ? val : 0.0f;
+        }
       }
       iseq += B;
       iq += n;
@@ -506,7 +545,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     const uint32_t k_ci = ci & (kRecWin - 1);
     const TRec r = sm.rec[k_ci];
     const uint32_t slab = r.slab, t = r.item;
-    const uint32_t col = slab * kSlab + uint32_t(lane) * V;
+    const uint32_t col = slab * kSlab + jv;
+    const bool writer = H == 1 || hl == 0;  // lane groups hold equal rows after the combine
     T4 acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = W::zero();
@@ -514,7 +554,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     // flight before the adds, which stay in delta order. Segments outside the
     // matrix read stale ring bytes into accumulators that are never stored.
 #pragma unroll 1
-    for (uint32_t k = r.beg; k < r.end; k += B) {
+    for (uint32_t k = r.beg; k < r.end; k += kGroup) {
       // this group was committed (the issue cursor is never behind the
       // consumer: it only stops at a record-window edge the consumer reaches
       // first); wait until its copies have landed
@@ -525,7 +565,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       T4 v[B][U];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        sc[b] = __shfl_sync(kFull, vring, s0 + b);  // +-1 or +-s_c
+        sc[b] = __shfl_sync(kFull, vring, (s0 + b) * H + hl);  // +-1 or +-s_c
 #pragma unroll
         for (int u = 0; u < U; ++u) v[b][u] = lds<V>(&sm.ring[s0 + b][u][lane * V]);
       }
@@ -542,6 +582,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       __syncwarp();  // the group's slots are fully read before their refill
       refill();
     }
+    if constexpr (H > 1) {  // combine the lane groups: a fixed tree, equal bits everywhere
+#pragma unroll
+      for (uint32_t off = kLanes; off < 32u; off *= 2u)
+        acc[0] = W::add(acc[0], shfl_xor_v<V>(acc[0], off));
+    }
     // ---- epilogue: partials, then CHUNK/MERGE publish or ROW stage 2 + 3
     uint32_t* flag_base = p.flags + (size_t)slab * p.n_items;
     if (r.cnt) add_partials<V, U, PFp>(p, flag_base, r.first, r.cnt, col, acc);
@@ -549,7 +594,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
       float* dst = p.partial + (size_t)t * p.dpad;
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (col + uint32_t(u) * kSeg < p.d) W::st(dst + col + u * kSeg, acc[u]);
+        if (writer && col + uint32_t(u) * kSeg < p.d) W::st(dst + col + u * kSeg, acc[u]);
       publish(flag_base + t, p.epoch);
       continue;
     }
@@ -572,13 +617,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
         float* dst = p.interior + (size_t)r.slot * p.dpad;
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          if (col + uint32_t(u) * kSeg < p.d) W::st(dst + col + u * kSeg, acc[u]);
+          if (writer && col + uint32_t(u) * kSeg < p.d) W::st(dst + col + u * kSeg, acc[u]);
         publish(flag_base + t, p.epoch);
       }
       const float sr = __uint_as_float(r.srow);
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (col + uint32_t(u) * kSeg < p.d) {
+        if (writer && col + uint32_t(u) * kSeg < p.d) {
           T4 yv = W::mul(acc[u], sr);
           if (p.relu) yv = relu_v<V>(yv);
           W::st(yrow + col + u * kSeg, yv);
@@ -586,7 +631,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
     } else {
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (col + uint32_t(u) * kSeg < p.d) W::st(yrow + col + u * kSeg, p.relu ? relu_v<V>(acc[u]) : acc[u]);
+        if (writer && col + uint32_t(u) * kSeg < p.d)
+          W::st(yrow + col + u * kSeg, p.relu ? relu_v<V>(acc[u]) : acc[u]);
       if (is_parent) publish(flag_base + t, p.epoch);
     }
   }
@@ -887,10 +933,10 @@ void launch_coop(const void* kernel, size_t smem, int& bps, Params& p, uint64_t 
      "cbm_kernel cooperative launch");
 }
 
-template <int V, int U, int D, bool NORM, int SC>
+template <int V, int U, int D, bool NORM, int SC, int H = 1>
 void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
   static int bps = -1;  // per template instance
-  launch_coop(reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SC>),
+  launch_coop(reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SC, H>),
               kWarpsPerCta * sizeof(WarpSmem<V, U, D>), bps, p, tickets, slabs, h, s);
 }
 
@@ -908,6 +954,15 @@ void run_kernel(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl
   else if (!scl) launch_one<V, U, D, true, 0>(p, tickets, slabs, h, s);
   else if (h->info.order_faithful) launch_one<V, U, D, true, 1>(p, tickets, slabs, h, s);
   else launch_one<V, U, D, true, 2>(p, tickets, slabs, h, s);
+}
+
+// Narrow X in the default mode: H deltas per warp instruction (V = 4, U = 1).
+template <int H>
+void run_groups(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl,
+                DeviceMatrix* h, cudaStream_t s) {
+  if (!norm) launch_one<4, 1, 8, false, 0, H>(p, tickets, slabs, h, s);
+  else if (!scl) launch_one<4, 1, 8, true, 0, H>(p, tickets, slabs, h, s);
+  else launch_one<4, 1, 8, true, 2, H>(p, tickets, slabs, h, s);
 }
 
 template <typename T>
@@ -1164,7 +1219,17 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     U = std::min<uint32_t>(U, uint32_t(h->opt.max_segments));
   // (narrower slabs that fit X in L2 were measured slower on cfg[2]/cfg[3]:
   // the extra per-ticket work outweighs the L2 misses they remove)
-  const uint32_t n_slabs = (d + 32 * V * U - 1) / (32 * V * U);
+  // narrow X in the default mode: H lane groups of 32/H lanes, one delta each
+  // per warp instruction (d <= 64, rows 16-byte aligned)
+  uint32_t H = 1;
+#ifndef CBM_NO_LANE_GROUPS
+  if (!L.order_faithful && h->opt.kernel == 0 && d >= 4 && d <= 64 && d % 4 == 0 &&
+      ldin % 4 == 0 && ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(xin) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(y) & 15) == 0)
+    H = d <= 32 ? 4 : 2;
+#endif
+  const uint32_t lanes_v = (H > 1 ? 4u : V) * (32 / H) * (H > 1 ? 1u : U);  // floats per slab
+  const uint32_t n_slabs = (d + lanes_v - 1) / lanes_v;
   if (++ws.epoch == 0) {  // wrapped: re-zero the flags
     ck(cudaMemsetAsync(ws.flags, 0, ws.flags_cap * sizeof(uint32_t), s), "flags memset");
     ws.epoch = 1;
@@ -1210,7 +1275,10 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   }
   p.faithful = L.order_faithful ? 1u : 0u;
   p.ldx32 = uint32_t(ldin);
-  if (d == 1) {  // spmv: lanes over deltas
+  if (H > 1) {
+    if (H == 2) run_groups<2>(p, tickets, n_slabs, norm, scl, h, s);
+    else run_groups<4>(p, tickets, n_slabs, norm, scl, h, s);
+  } else if (d == 1) {  // spmv: lanes over deltas
     if (!norm) launch_spmv<false, 0>(p, tickets, h, s);
     else if (!scl) launch_spmv<true, 0>(p, tickets, h, s);
     else if (L.order_faithful) launch_spmv<true, 1>(p, tickets, h, s);
