@@ -243,6 +243,19 @@ template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+// Copies of one ring slot at the matrix's column edge: out-of-range segments
+// copy nothing (and point at a valid address). Not inlined, so the common
+// full-width path stays a straight line instead of being if-converted.
+template <int V, int U, uint32_t kSeg>
+__device__ __noinline__ void edge_copies(float* slot, const float* src, const float* any,
+                                         uint32_t imask, bool on) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool ok = on && ((imask >> u) & 1u);
+    cp_async_z<V>(slot + u * 32 * V, ok ? src + u * kSeg : any, ok);
+  }
+}
+
 // Wait until at most n (<= N) of the most recently committed groups are pending.
 template <int N>
 __device__ __forceinline__ void cp_wait_upto(uint32_t n) {
@@ -480,7 +493,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
           const uint32_t sz = on ? uint32_t(V * 4) : 0u;
 #pragma unroll
           for (int u = 0; u < U; ++u) cp_async_n<V>(&sm.ring[s0 + b][u][lane * V], src + u * kSeg, sz);
-        } else {  // the matrix edge: out-of-range segments copy nothing
+        } else if constexpr (U == 1 && H == 1) {  // the matrix edge: a real call keeps
+          // the one-segment hot path unpredicated (A/B: cfg[2] 921 -> 838 us; with
+          // lane groups the call costs more than it saves, cfg[0] 20.5 -> 22.5 us)
+          edge_copies<V, U, kSeg>(&sm.ring[s0 + b][0][lane * V], src, p.x, imask, on);
+        } else {  // (inline for U > 1: a call there costs more than the predication)
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const bool ok = on && ((imask >> u) & 1u);
