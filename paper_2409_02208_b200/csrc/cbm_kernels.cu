@@ -323,6 +323,32 @@ __device__ __forceinline__ typename Vec<V>::T fma_sign(typename Vec<V>::T acc,
 }
 
 constexpr int kWarpsPerCta = 4;
+// Ring geometry (measured defaults; overridable for A/B builds, `make alt`):
+// D slots per warp ring by segments per ticket, B slots per ring group.
+#ifndef CBM_D_U4
+#define CBM_D_U4 4
+#endif
+#ifndef CBM_D_U2
+#define CBM_D_U2 8
+#endif
+#ifndef CBM_D_U1
+#define CBM_D_U1 16
+#endif
+#ifndef CBM_B_U4
+#define CBM_B_U4 2
+#endif
+#ifndef CBM_B_U2
+#define CBM_B_U2 4
+#endif
+#ifndef CBM_B_U1
+#define CBM_B_U1 8
+#endif
+#ifndef CBM_D_H2  // lane groups of 16 lanes (d <= 64)
+#define CBM_D_H2 16
+#endif
+#ifndef CBM_B_H2
+#define CBM_B_H2 8
+#endif
 constexpr uint32_t kRecWin = 64;  // ticket records staged per warp (two groups of 32)
 
 // One ticket's record (3 x 16 bytes), as stored in the warp's region of the
@@ -378,7 +404,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
   // deltas per ring group: copies are issued, committed and awaited B at a
   // time (a group never spans two tickets; its unused slots stay idle)
-  constexpr int B = D >= 8 ? 4 : 2;
+  constexpr int B = H == 4 ? 4 : (H == 2 ? CBM_B_H2 : (U == 4 ? CBM_B_U4 : (U == 2 ? CBM_B_U2 : CBM_B_U1)));
+  static_assert(D % B == 0, "whole ring groups");
   constexpr int G = D / B;  // groups in flight
   constexpr uint32_t kGroup = uint32_t(B) * H;  // deltas per ring group
   static_assert(32 % kGroup == 0, "a ring group never spans two index windows");
@@ -977,9 +1004,10 @@ void run_kernel(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl
 template <int H>
 void run_groups(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl,
                 DeviceMatrix* h, cudaStream_t s) {
-  if (!norm) launch_one<4, 1, 8, false, 0, H>(p, tickets, slabs, h, s);
-  else if (!scl) launch_one<4, 1, 8, true, 0, H>(p, tickets, slabs, h, s);
-  else launch_one<4, 1, 8, true, 2, H>(p, tickets, slabs, h, s);
+  constexpr int D = H == 2 ? CBM_D_H2 : 8;
+  if (!norm) launch_one<4, 1, D, false, 0, H>(p, tickets, slabs, h, s);
+  else if (!scl) launch_one<4, 1, D, true, 0, H>(p, tickets, slabs, h, s);
+  else launch_one<4, 1, D, true, 2, H>(p, tickets, slabs, h, s);
 }
 
 template <typename T>
@@ -1301,9 +1329,9 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     else if (L.order_faithful) launch_spmv<true, 1>(p, tickets, h, s);
     else launch_spmv<true, 2>(p, tickets, h, s);
   } else if (V == 4) {
-    if (U == 4) run_kernel<4, 4, 4>(p, tickets, n_slabs, norm, scl, h, s);
-    else if (U == 2) run_kernel<4, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
-    else run_kernel<4, 1, 8>(p, tickets, n_slabs, norm, scl, h, s);
+    if (U == 4) run_kernel<4, 4, CBM_D_U4>(p, tickets, n_slabs, norm, scl, h, s);
+    else if (U == 2) run_kernel<4, 2, CBM_D_U2>(p, tickets, n_slabs, norm, scl, h, s);
+    else run_kernel<4, 1, CBM_D_U1>(p, tickets, n_slabs, norm, scl, h, s);
   } else if (V == 2) {
     if (U == 4) run_kernel<2, 4, 8>(p, tickets, n_slabs, norm, scl, h, s);
     else if (U == 2) run_kernel<2, 2, 8>(p, tickets, n_slabs, norm, scl, h, s);
