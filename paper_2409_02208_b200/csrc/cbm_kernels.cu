@@ -361,21 +361,35 @@ struct alignas(16) TRec {
   uint32_t item, slab, srow, nw;
 };
 
+// Record window per warp for the multiply kernel (a power of two <= kRecWin).
+#ifndef CBM_RECWIN_U4
+#define CBM_RECWIN_U4 64
+#endif
+#ifdef CBM_MINB_U4  // A/B: __launch_bounds__ min blocks for 4-segment kernels
+#define CBM_LAUNCH_BOUNDS(U) __launch_bounds__(kWarpsPerCta * 32, (U) == 4 ? CBM_MINB_U4 : 1)
+#else
+#define CBM_LAUNCH_BOUNDS(U) __launch_bounds__(kWarpsPerCta * 32)
+#endif
+template <int U>
+constexpr uint32_t rec_window() { return U == 4 ? CBM_RECWIN_U4 : kRecWin; }
+
 template <int V, int U, int D>
 struct alignas(16) WarpSmem {
-  float ring[D][U][32 * V];  // slot s, segment u, lane l: [s][u][l*V, l*V+V)
-  TRec rec[kRecWin];         // warp-sequence tickets [g, g+64), slot i & 63
+  float ring[D][U][32 * V];      // slot s, segment u, lane l: [s][u][l*V, l*V+V)
+  TRec rec[rec_window<U>()];     // warp-sequence tickets [g, g+RW), slot i & (RW-1)
 };
 
-// Stage the records of warp-sequence tickets [i0, i0+32). Regions are padded
-// (zero records past a warp's count, 64 more after the last region), so the
-// loads need no bound: one dependent hop from the kernel start to the records.
-template <class SM>
+// Stage the records of warp-sequence tickets [i0, i0+RW/2) into a window of
+// RW records. Regions are padded (zero records past a warp's count, 64 more
+// after the last region), so the loads need no bound: one dependent hop from
+// the kernel start to the records.
+template <uint32_t RW = kRecWin, class SM>
 __device__ __forceinline__ void stage_recs(const Params& p, SM& sm, uint32_t w, uint32_t i0) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t i = i0 + uint32_t(lane);
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane >= RW / 2) return;
+  const uint32_t i = i0 + lane;
   const uint4* src = p.trec + 3 * ((size_t)w * p.wstride + i);
-  uint4* dst = reinterpret_cast<uint4*>(&sm.rec[i & (kRecWin - 1)]);
+  uint4* dst = reinterpret_cast<uint4*>(&sm.rec[i & (RW - 1)]);
   const uint4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
   dst[0] = a;
   dst[1] = b;
@@ -392,7 +406,7 @@ __device__ __forceinline__ void stage_recs(const Params& p, SM& sm, uint32_t w, 
 //   are combined once per ticket by a fixed shuffle tree (summation order
 //   changes; integer sums stay exact).
 template <int V, int U, int D, bool NORM, int SC, int H = 1>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) {
+__global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
   using W = Vec<V>;
   using T4 = typename W::T;
   static_assert(H == 1 || (U == 1 && SC != 1), "lane groups: one segment, default mode");
@@ -411,6 +425,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   static_assert(32 % kGroup == 0, "a ring group never spans two index windows");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
+  constexpr uint32_t RW = rec_window<U>();  // staged records (two halves)
+  constexpr uint32_t kHalf = RW / 2;
   const uint32_t hl = uint32_t(lane) / kLanes;          // lane group
   const uint32_t jv = (uint32_t(lane) % kLanes) * V;    // column offset in a segment
   using SM = WarpSmem<V, U, D>;
@@ -425,12 +441,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   const unsigned long long t_start = p.trace ? globaltimer() : 0ull;
   prefetch_x(p, w);
   uint32_t g = 0;  // staged records cover warp-sequence tickets [g, g + 64)
-  stage_recs(p, sm, w, 0);
-  stage_recs(p, sm, w, 32);
+  stage_recs<RW>(p, sm, w, 0);
+  stage_recs<RW>(p, sm, w, kHalf);
   __syncwarp();
   const uint32_t n_w = sm.rec[0].nw;  // this warp's tickets (increasing ticket order)
   if (n_w == 0) return;
-  auto R = [&](uint32_t i) -> const TRec& { return sm.rec[i & (kRecWin - 1)]; };
+  auto R = [&](uint32_t i) -> const TRec& { return sm.rec[i & (RW - 1)]; };
   // 32 column words (and values) of a delta block: lane j holds delta k0 + j
   struct Wd {
     uint32_t c;
@@ -446,7 +462,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   };
   // first block of ticket i (empty past the end / outside the staged records)
   auto window = [&](uint32_t i) -> Wd {
-    if (i >= n_w || i >= g + kRecWin) return Wd{0u, 0.0f};
+    if (i >= n_w || i >= g + RW) return Wd{0u, 0.0f};
     const TRec& r = R(i);
     return fetch(r.beg, r.end);
   };
@@ -482,7 +498,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
         ii = n_w;
         return;
       }
-      if (ii + 3 >= g + kRecWin && ii + 3 < n_w) {
+      if (ii + 3 >= g + RW && ii + 3 < n_w) {
         iblocked = true;  // resume after the record window slides
         return;
       }
@@ -575,10 +591,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
   uint32_t cseq = 0;  // deltas consumed
 #pragma unroll 1
   for (uint32_t ci = 0; ci < n_w; ++ci) {
-    if (ci - g == 32) {  // slide the record window by one group
+    if (ci - g == kHalf) {  // slide the record window by one half
       __syncwarp();
-      stage_recs(p, sm, w, g + kRecWin);
-      g += 32;
+      stage_recs<RW>(p, sm, w, g + RW);
+      g += kHalf;
       __syncwarp();
       if (iblocked) {
         iblocked = false;
@@ -586,7 +602,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_kernel(const Params p) 
         refill();
       }
     }
-    const uint32_t k_ci = ci & (kRecWin - 1);
+    const uint32_t k_ci = ci & (RW - 1);
     const TRec r = sm.rec[k_ci];
     const uint32_t slab = r.slab, t = r.item;
     const uint32_t col = slab * kSlab + jv;
