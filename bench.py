@@ -301,7 +301,14 @@ def run_ours(args, wl):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic_for(wl.name),
                 "b_alg_bytes": b_alg_local, "kernel": "cbm_kernel",
-                "peak_source": peak_src}
+                "peak_source": peak_src,
+                # what actually bounds the gather: X rows moved L2 -> SM per step
+                # (one row per summed delta) against the measured gather rate of
+                # profiles/r01_ubench_gather.txt
+                "l2_gather": {"bytes": int(info["nnz_effective"]) * d_local * 4,
+                              "achieved_tbps": int(info["nnz_effective"]) * d_local * 4
+                              / (ms * 1e-3) / 1e12 if ms > 0 else 0.0,
+                              "measured_peak_tbps": 15.7}}
 
     gpu_csr = None
     if not args.no_csr_comparator:
