@@ -442,10 +442,13 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
   prefetch_x(p, w);
   uint32_t g = 0;  // staged records cover warp-sequence tickets [g, g + 64)
   stage_recs<RW>(p, sm, w, 0);
-  stage_recs<RW>(p, sm, w, kHalf);
   __syncwarp();
   const uint32_t n_w = sm.rec[0].nw;  // this warp's tickets (increasing ticket order)
   if (n_w == 0) return;
+  if (n_w > kHalf) {  // (most warps of small matrices fit one half: less start-up traffic)
+    stage_recs<RW>(p, sm, w, kHalf);
+    __syncwarp();
+  }
   auto R = [&](uint32_t i) -> const TRec& { return sm.rec[i & (RW - 1)]; };
   // 32 column words (and values) of a delta block: lane j holds delta k0 + j
   struct Wd {
@@ -875,7 +878,10 @@ const DeviceMatrix::Schedule& schedule_for(DeviceMatrix* h, uint32_t warps, uint
   const Layout& L = h->info;
   const uint32_t n = L.n_items;
   const uint64_t total = uint64_t(n) * slabs;
-  constexpr float kTicket = 4.0f;  // epilogue / record overhead in delta-equivalents
+#ifndef CBM_TICKET_COST
+#define CBM_TICKET_COST 4.0f
+#endif
+  constexpr float kTicket = CBM_TICKET_COST;  // epilogue / record overhead in delta-equivalents
   std::vector<uint32_t> owner(total);
   std::vector<uint32_t> count(size_t(warps) + 1, 0);
   std::vector<float> fin(n);

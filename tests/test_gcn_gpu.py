@@ -87,3 +87,18 @@ def test_gcn_sharded_nccl_world1_bitwise():
         dist.destroy_process_group()
     assert_bitwise(got, want, "sharded gcn")
     assert_bitwise(got, O.oracle_gcn_forward(oracle_arrays(c), x, w0, w1), "vs oracle")
+
+
+@pytest.mark.parametrize("hid", [24, 48])
+def test_gcn_narrow_hidden_default_mode(hid):
+    """Default mode with a narrow hidden layer: the ReLU-fused Â product runs
+    with lane groups (several deltas per warp instruction); 1e-5 normwise."""
+    a = P.generate_graph("community", [3000, 300, 0.7, 2e-4], 151)
+    c = P.build_cbm_normalized(a, 0, threads=8)
+    x = P.generate_dense("normal", 3000, 40, 152)
+    w0 = P.generate_dense("glorot", 40, hid, 153)
+    w1 = P.generate_dense("glorot", hid, 7, 154)
+    want = O.oracle_gcn_forward(oracle_arrays(c), x, w0, w1)
+    got = P.DeviceCbm(c).gcn_forward(_t(x), _t(w0), _t(w1)).cpu().numpy()
+    err = np.abs(got - want).max() / np.abs(want).max()
+    assert err <= 1e-5
