@@ -113,6 +113,44 @@ int main() {
     printf("stamp kernel A: CTA start spread %.2f us; B first CTA - A last CTA = %.2f us\n",
            (a1 - a0) / 1e3, (double)(b0 - a1) / 1e3);
   }
+  // launch through a 1-node CUDA graph (kernel node params updated per call)
+  {
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    empty_k<<<740, 128, 0, st>>>(out);
+    cudaStreamEndCapture(st, &g);
+    cudaGraphInstantiate(&ge, g, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float tot = 0;
+    for (int r = 0; r < 53; ++r) {
+      fill<<<148 * 8, 512, 0, st>>>(buf, n, float(r));
+      cudaEventRecord(a, st);
+      cudaGraphLaunch(ge, st);
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (r >= 3) tot += ms;
+    }
+    printf("after fill, 1-node graph launch (grid 740): %.2f us\n", tot / 50 * 1e3);
+    tot = 0;
+    for (int r = 0; r < 53; ++r) {
+      fill<<<148 * 8, 512, 0, st>>>(buf, n, float(r));
+      cudaEventRecord(a, st);
+      empty_k<<<740, 128, 0, st>>>(out);
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (r >= 3) tot += ms;
+    }
+    printf("after fill, plain launch on a non-blocking stream (grid 740): %.2f us\n", tot / 50 * 1e3);
+  }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
   return 0;
