@@ -37,7 +37,7 @@
 #include <vector>
 #include <string>
 
-#include "device.hpp"
+#include "cuda_common.hpp"
 
 namespace cbmb {
 
@@ -46,12 +46,6 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kThreads = 256;  // 8 warps per CTA
 
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    const int code = (e == cudaErrorMemoryAllocation) ? CBM_B200_ENOMEM : CBM_B200_ECUDA;
-    throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e), code);
-  }
-}
 
 // ---------------------------------------------------------------- vectors
 template <int V>
@@ -349,17 +343,7 @@ constexpr int kWarpsPerCta = 4;
 #ifndef CBM_B_H2
 #define CBM_B_H2 8
 #endif
-constexpr uint32_t kRecWin = 64;  // ticket records staged per warp (two groups of 32)
 
-// One ticket's record (3 x 16 bytes), as stored in the warp's region of the
-// ticket stream and staged in shared memory: the item's layout record, the
-// ticket's item and column slab, the row scale, and (first record of a region
-// only) the warp's ticket count.
-struct alignas(16) TRec {
-  uint32_t beg, end, rowk, ppos;
-  uint32_t psrc, first, cnt, slot;
-  uint32_t item, slab, srow, nw;
-};
 
 // Record window per warp for the multiply kernel (a power of two <= kRecWin).
 #ifndef CBM_RECWIN_U4
@@ -836,122 +820,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_spmv_kernel(const Param
   }
 }
 
-// Gathers each warp's ticket records into its region of the ticket stream.
-__global__ void build_ticket_stream(const uint4* __restrict__ rec, const float* __restrict__ srow,
-                                    const uint32_t* __restrict__ list,
-                                    const uint32_t* __restrict__ wstart, uint32_t n_items,
-                                    uint32_t warps, uint32_t stride, uint64_t n_rec,
-                                    TRec* __restrict__ out) {
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n_rec;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    TRec r{};
-    const uint64_t w = k / stride, i = k - w * stride;
-    if (w < warps) {
-      const uint32_t lo = wstart[w], n = wstart[w + 1] - lo;
-      if (i < n) {
-        const uint32_t T = list[lo + i];
-        const uint32_t sl = T / n_items, t = T - sl * n_items;
-        const uint4 a = rec[2 * (size_t)t], b = rec[2 * (size_t)t + 1];
-        r = TRec{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w,
-                 t, sl, srow ? __float_as_uint(srow[t]) : 0u, 0u};
-      }
-      if (i == 0) r.nw = n;
-    }
-    out[k] = r;
-  }
-}
-
-// Static list schedule of the tickets over the resident warps (cbm_kernel).
-// Tickets are taken in order and each goes to the warp that an estimated
-// clock frees first (ties: lowest warp), starting no earlier than its
-// parent / partial producers are estimated to finish; cost ~ per-ticket
-// overhead + deltas + partial rows + parent row. Every warp's list is
-// increasing, which is all the deadlock argument needs (the smallest
-// unfinished ticket is always being worked on). Balancing by work instead of
-// round-robin by count removes the tail where warps holding several 32-delta
-// chunks finish long after the rest.
-const DeviceMatrix::Schedule& schedule_for(DeviceMatrix* h, uint32_t warps, uint32_t slabs,
-                                           cudaStream_t s) {
-  const uint64_t key = (uint64_t(warps) << 32) | slabs;
-  auto it = h->schedules.find(key);
-  if (it != h->schedules.end()) return it->second;
-  const Layout& L = h->info;
-  const uint32_t n = L.n_items;
-  const uint64_t total = uint64_t(n) * slabs;
-#ifndef CBM_TICKET_COST
-#define CBM_TICKET_COST 4.0f
-#endif
-  constexpr float kTicket = CBM_TICKET_COST;  // epilogue / record overhead in delta-equivalents
-  std::vector<uint32_t> owner(total);
-  std::vector<uint32_t> count(size_t(warps) + 1, 0);
-  std::vector<float> fin(n);
-  using Slot = std::pair<float, uint32_t>;
-  std::vector<Slot> heap;
-  heap.reserve(warps);
-  for (uint32_t w = 0; w < warps; ++w) heap.emplace_back(0.0f, w);
-  auto later = [](const Slot& a, const Slot& b) { return a > b; };  // min-heap
-  std::make_heap(heap.begin(), heap.end(), later);
-  for (uint32_t sl = 0; sl < slabs; ++sl) {
-    for (uint32_t t = 0; t < n; ++t) {
-      std::pop_heap(heap.begin(), heap.end(), later);
-      Slot& top = heap.back();
-      const uint32_t* dp = &h->item_dep[size_t(t) * 3];
-      float start = top.first;
-      float cost = kTicket + float(L.item_beg[t + 1] - L.item_beg[t]) + float(dp[2]);
-      if (dp[0] != kNoItem) {
-        start = std::max(start, fin[dp[0]]);
-        cost += 1.0f;
-      }
-      for (uint32_t j = 0; j < dp[2]; ++j) start = std::max(start, fin[dp[1] + j]);
-      fin[t] = start + cost;
-      top.first = fin[t];
-      owner[uint64_t(sl) * n + t] = top.second;
-      ++count[top.second + 1];
-      std::push_heap(heap.begin(), heap.end(), later);
-    }
-  }
-  uint32_t most = 0;
-  for (uint32_t w = 0; w < warps; ++w) {
-    most = std::max(most, count[w + 1]);
-    count[w + 1] += count[w];
-  }
-  std::vector<uint32_t> list(total);
-  {
-    std::vector<uint32_t> pos(count.begin(), count.end() - 1);
-    for (uint64_t T = 0; T < total; ++T) list[pos[owner[T]]++] = uint32_t(T);
-  }
-  // the ticket stream: warp w's records at [w * stride, w * stride + count_w),
-  // zero records after them and 64 more after the last region
-  DeviceMatrix::Schedule sc;
-  sc.wstride = std::max<uint32_t>(32, (most + 31) & ~31u);
-  const uint64_t n_rec = uint64_t(warps) * sc.wstride + kRecWin;
-  uint32_t *d_list = nullptr, *d_start = nullptr;
-  try {
-    ck(cudaMalloc(&sc.trec, n_rec * sizeof(TRec)), "schedule");
-    ck(cudaMalloc(&d_list, std::max<uint64_t>(total, 1) * sizeof(uint32_t)), "schedule");
-    ck(cudaMalloc(&d_start, count.size() * sizeof(uint32_t)), "schedule");
-    ck(cudaMemcpyAsync(d_list, list.data(), total * sizeof(uint32_t), cudaMemcpyHostToDevice, s),
-       "schedule upload");
-    ck(cudaMemcpyAsync(d_start, count.data(), count.size() * sizeof(uint32_t),
-                       cudaMemcpyHostToDevice, s),
-       "schedule upload");
-    const int grid = int(std::min<uint64_t>((n_rec + 255) / 256, uint64_t(h->num_sms) * 32));
-    build_ticket_stream<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(h->rec), h->srow,
-                                             d_list, d_start, L.n_items, warps, sc.wstride,
-                                             n_rec, reinterpret_cast<TRec*>(sc.trec));
-    ck(cudaGetLastError(), "schedule build");
-    ck(cudaStreamSynchronize(s), "schedule build");  // the host vectors go out of scope
-  } catch (...) {
-    if (sc.trec) cudaFree(sc.trec);
-    cudaFree(d_list);
-    cudaFree(d_start);
-    throw;
-  }
-  cudaFree(d_list);
-  cudaFree(d_start);
-  return h->schedules.emplace(key, sc).first->second;
-}
-
 // xs[c, :] = row_scale[c] (*) x[c, :] — the bit-identical products of the
 // normalized stage 1 (fl(+-s*x) = +-fl(s*x)), formed once per call.
 __global__ void prescale_kernel(const float* __restrict__ x, long long ldx,
@@ -1032,191 +900,8 @@ void run_groups(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl
   else launch_one<4, 1, D, true, 2, H>(p, tickets, slabs, h, s);
 }
 
-template <typename T>
-void grow(T*& ptr, uint64_t& cap, uint64_t need, const char* what) {
-  if (need <= cap) return;
-  if (ptr) ck(cudaFree(ptr), "cudaFree");
-  ptr = nullptr;
-  cap = 0;
-  ck(cudaMalloc(&ptr, std::max<uint64_t>(need, 1) * sizeof(T)), what);
-  cap = need;
-}
 
 }  // namespace
-
-namespace {
-// dense_matmul (dense.cpp:31-49) with the reference's exact arithmetic:
-// c[i,q] = sum over ascending j with a[i,j] != 0 of fl(a[i,j] * b[j,q]),
-// each product rounded before the add, starting from +0. A CTA computes a
-// 32-row x 128-column tile; b is staged through shared memory 32 rows of j at
-// a time; the zero test is warp-uniform (a warp shares its row).
-constexpr int kGemmRows = 32, kGemmCols = 128, kGemmK = 32;
-__global__ void __launch_bounds__(256) ordered_gemm_kernel(const float* __restrict__ a,
-                                                           const float* __restrict__ b,
-                                                           float* __restrict__ c, uint32_t m,
-                                                           uint32_t k, uint32_t n) {
-  __shared__ float bs[kGemmK][kGemmCols];
-  __shared__ float as[kGemmRows][kGemmK + 1];
-  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 lanes x 8 warps
-  const uint32_t row0 = blockIdx.y * kGemmRows, col0 = blockIdx.x * kGemmCols;
-  float acc[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[r][q] = 0.0f;
-  for (uint32_t j0 = 0; j0 < k; j0 += kGemmK) {
-    __syncthreads();
-    for (uint32_t e = threadIdx.x; e < kGemmK * kGemmCols; e += 256) {
-      const uint32_t jj = e / kGemmCols, cc = e % kGemmCols;
-      bs[jj][cc] = (j0 + jj < k && col0 + cc < n) ? b[(size_t)(j0 + jj) * n + col0 + cc] : 0.0f;
-    }
-    for (uint32_t e = threadIdx.x; e < kGemmRows * kGemmK; e += 256) {
-      const uint32_t rr = e / kGemmK, jj = e % kGemmK;
-      as[rr][jj] = (row0 + rr < m && j0 + jj < k) ? a[(size_t)(row0 + rr) * k + j0 + jj] : 0.0f;
-    }
-    __syncthreads();
-    const uint32_t jn = min(uint32_t(kGemmK), k - j0);
-    for (uint32_t jj = 0; jj < jn; ++jj) {
-      float bv[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) bv[q] = bs[jj][tx + 32 * q];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const float av = as[ty + 8 * r][jj];
-        if (av != 0.0f) {  // dense.cpp:42 skips zero lhs entries
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[r][q] = __fadd_rn(acc[r][q], __fmul_rn(av, bv[q]));
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const uint32_t i = row0 + ty + 8 * r;
-    if (i >= m) continue;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t cc = col0 + tx + 32 * q;
-      if (cc < n) c[(size_t)i * n + cc] = acc[r][q];
-    }
-  }
-}
-}  // namespace
-
-void device_dense_matmul(const float* a, uint32_t m, uint32_t k, const float* b, uint32_t n,
-                         float* c, void* stream) {
-  if (m == 0 || n == 0) return;
-  const dim3 grid((n + kGemmCols - 1) / kGemmCols, (m + kGemmRows - 1) / kGemmRows);
-  ordered_gemm_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, b, c, m, k, n);
-  ck(cudaGetLastError(), "ordered_gemm launch");
-}
-
-// gcn_forward (gcn.cpp:22-33): X W0 -> A_hat . -> relu -> A_hat . -> . W1, the
-// ReLU fused into the first product's epilogue. Device pointers throughout.
-void device_gcn_forward(DeviceMatrix* h, const float* x, uint32_t n, uint32_t f,
-                        const float* w0, uint32_t hid, const float* w1, uint32_t classes,
-                        float* out, void* stream) {
-  ck(cudaSetDevice(h->device), "cudaSetDevice");
-  const uint32_t hp = (hid + 3) & ~3u;
-  auto& ws = h->ws[stream];
-  grow(ws.gcn_h, ws.gcn_h_cap, uint64_t(n) * hp * 2, "gcn workspace");
-  float* h0 = ws.gcn_h;
-  float* h1 = ws.gcn_h + uint64_t(n) * hp;
-  uint32_t launches = 0;
-  device_dense_matmul(x, n, f, w0, hid, h0, stream);  // packed n x hid
-  ++launches;
-  device_spmm(h, h0, hid, hid, h1, hid, stream, /*relu=*/true);
-  launches += h->last_launches;
-  device_spmm(h, h1, hid, hid, h0, hid, stream, /*relu=*/false);
-  launches += h->last_launches;
-  device_dense_matmul(h0, n, hid, w1, classes, out, stream);
-  h->last_launches = launches + 1;
-}
-
-DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& opt) {
-  // validate + plan on the host first: malformed input is EINVAL, never a CUDA error
-  const uint32_t gain = opt.flatten_gain < 0 ? 16u : uint32_t(opt.flatten_gain);
-  // resident warps for the auto split: ~20 per SM (the multiply's occupancy);
-  // without a device the upload fails after validation anyway
-  int sms = 148, cur = 0;
-  if (cudaGetDevice(&cur) == cudaSuccess &&
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount,
-                             opt.device >= 0 ? opt.device : cur) != cudaSuccess)
-    sms = 148;
-  cudaGetLastError();  // a failed probe must not leak into later error checks
-  Layout L = plan_layout(v, opt.order_faithful != 0, opt.split_threshold, opt.chunk, gain,
-                         uint32_t(sms) * 20);
-  auto* h = new DeviceMatrix;
-  try {
-    int dev = opt.device;
-    if (dev < 0) ck(cudaGetDevice(&dev), "cudaGetDevice");
-    ck(cudaSetDevice(dev), "cudaSetDevice");
-    h->device = dev;
-    h->opt = opt;
-    ck(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev), "attr");
-    ck(cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, dev), "attr");
-    auto put = [&](auto*& dst, const auto& vec, const char* what) {
-      using E = typename std::remove_reference_t<decltype(vec)>::value_type;
-      const size_t bytes = std::max<size_t>(vec.size(), 1) * sizeof(E);
-      ck(cudaMalloc(&dst, bytes), what);
-      if (!vec.empty()) ck(cudaMemcpy(dst, vec.data(), vec.size() * sizeof(E),
-                                      cudaMemcpyHostToDevice), what);
-      h->device_bytes += vec.size() * sizeof(E);
-    };
-    put(h->dcol, L.dcol, "upload dcol");
-    put(h->rec, L.rec, "upload rec");
-    if (L.normalized) {
-      put(h->srow, L.srow, "upload srow");
-      put(h->scale, L.scale, "upload scale");
-      // the signed delta values in dcol order (bit-identical to the CBM's
-      // values: +-row_scale[col], validated by plan_layout)
-      std::vector<float> dval(L.dcol.size());
-      for (size_t k = 0; k < dval.size(); ++k) {
-        const float sc = L.scale[L.dcol[k] & 0x7FFFFFFFu];
-        dval[k] = (L.dcol[k] >> 31) ? -sc : sc;
-      }
-      put(h->dval, dval, "upload dval");
-    }
-    int coop = 0;
-    ck(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev), "attr");
-    if (!coop) throw cuda_error("device lacks cooperative launch", CBM_B200_ECUDA);
-    // keep only sizes on the host
-    L.dcol = {};
-    h->item_dep.resize(size_t(L.n_items) * 3);  // for the ticket schedule
-    for (uint32_t t = 0; t < L.n_items; ++t) {
-      h->item_dep[size_t(t) * 3] = L.rec[size_t(t) * 8 + 3];
-      h->item_dep[size_t(t) * 3 + 1] = L.rec[size_t(t) * 8 + 5];
-      h->item_dep[size_t(t) * 3 + 2] = L.rec[size_t(t) * 8 + 6];
-    }
-    L.rec = {};  // item_beg and item_dep stay: they drive the ticket schedule
-    L.srow = {};
-    L.scale = {};
-    h->info = std::move(L);
-  } catch (...) {
-    device_free(h);
-    throw;
-  }
-  return h;
-}
-
-void device_free(DeviceMatrix* h) {
-  if (!h) return;
-  cudaSetDevice(h->device);
-  if (h->s_in) {
-    cudaStreamDestroy(h->s_in);
-    cudaStreamDestroy(h->s_out);
-    for (auto e : h->ev) cudaEventDestroy(e);
-  }
-  for (auto& kv : h->schedules) cudaFree(kv.second.trec);
-  for (auto& kv : h->ws)
-    for (void* p : {(void*)kv.second.flags, (void*)kv.second.partial, (void*)kv.second.interior,
-                    (void*)kv.second.xs, (void*)kv.second.gcn_h})
-      if (p) cudaFree(p);
-  for (void* p : {(void*)h->dcol, (void*)h->dval, (void*)h->rec, (void*)h->srow, (void*)h->scale,
-                  (void*)h->xstage, (void*)h->ystage})
-    if (p) cudaFree(p);
-  delete h;
-}
 
 namespace {
 uint32_t pick_vec(uint32_t d, const float* x, int64_t ldx, const float* y, int64_t ldy) {
@@ -1226,22 +911,6 @@ uint32_t pick_vec(uint32_t d, const float* x, int64_t ldx, const float* y, int64
   return 1;
 }
 }  // namespace
-
-void device_reserve(DeviceMatrix* h, uint64_t d, void* stream) {
-  const Layout& L = h->info;
-  const uint64_t dpad = (d + 3) & ~uint64_t(3);
-  const uint64_t slabs = (d + 31) / 32;  // worst case (V = 1)
-  ck(cudaSetDevice(h->device), "cudaSetDevice");
-  auto& ws = h->ws[stream];
-  if (uint64_t(L.n_items) * slabs > ws.flags_cap) {
-    grow(ws.flags, ws.flags_cap, uint64_t(L.n_items) * slabs, "workspace flags");
-    ck(cudaMemset(ws.flags, 0, ws.flags_cap * sizeof(uint32_t)), "flags memset");
-    ws.epoch = 0;
-  }
-  grow(ws.partial, ws.partial_cap, uint64_t(L.n_chunk_items) * dpad, "workspace partial");
-  if (L.normalized) grow(ws.interior, ws.interior_cap, uint64_t(L.n_interior) * dpad,
-                         "workspace interior");
-}
 
 void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
                  int64_t ldy, void* stream, bool relu) {
@@ -1378,82 +1047,6 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
       std::fclose(f);
     }
   }
-}
-
-// Host-buffer entry point. Columns are independent (kernels.cpp:27-62), so X
-// and Y move in column chunks on three streams: H2D of chunk k+1 and D2H of
-// chunk k-1 run while chunk k multiplies, and the two copy directions overlap
-// on the full-duplex PCIe link. One chunk when the operand is small.
-void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
-                      int64_t ldy, void* stream, bool wait) {
-  const Layout& L = h->info;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  ck(cudaSetDevice(h->device), "cudaSetDevice");
-  const uint32_t dpad = (d + 3) & ~3u;
-  grow(h->xstage, h->xstage_cap, uint64_t(L.n_cols) * dpad, "staging X");
-  grow(h->ystage, h->ystage_cap, uint64_t(L.n_rows) * dpad, "staging Y");
-  if (!h->s_in) {
-    ck(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking), "stream");
-    ck(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking), "stream");
-    for (auto& e : h->ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-  }
-  const uint64_t bytes = (uint64_t(L.n_cols) + L.n_rows) * d * sizeof(float);
-  // Column chunks (16-byte aligned): the first chunk's H2D and the last
-  // chunk's D2H cannot overlap anything, so those two are narrow (d/8) and
-  // the middle is cut in three (tools/probe_e2e.py: uniform x4 1109 us,
-  // x8 1151 us on cfg[1]; rows narrower than 64 floats slow the 2D copies).
-  std::vector<std::pair<uint32_t, uint32_t>> parts;  // (first column, width)
-  auto r4 = [](uint32_t v) { return (v + 3) & ~3u; };
-  uint32_t chunks = 1;
-  if (bytes >= (8u << 20) && d >= 128) chunks = d >= 256 ? 5 : 2;
-  if (const char* e = std::getenv("CBM_B200_HOST_CHUNKS"))  // dev tool: uniform chunks
-    chunks = std::max<uint32_t>(1, std::min<uint32_t>({kHostChunks, uint32_t(std::atoi(e)), d}));
-  if (chunks == 5 && !std::getenv("CBM_B200_HOST_CHUNKS")) {  // d >= 256
-    const uint32_t edge = r4(d / 8), rest = d - 2 * edge, mid = r4((rest + 2) / 3);
-    uint32_t c0 = 0;
-    const uint32_t m3 = (rest - 2 * mid) & ~3u;  // every chunk starts 16-byte aligned
-    for (uint32_t w : {edge, mid, mid, m3, d - edge - 2 * mid - m3}) {
-      parts.emplace_back(c0, w);
-      c0 += w;
-    }
-  } else {
-    const uint32_t cw = r4((d + chunks - 1) / chunks);
-    for (uint32_t c0 = 0; c0 < d; c0 += cw) parts.emplace_back(c0, std::min(cw, d - c0));
-  }
-  // ev[0]: caller's prior work on s; ev[1+k]: X chunk k landed; ev[1+C+k]: Y chunk k ready
-  ck(cudaEventRecord(h->ev[0], s), "event");
-  ck(cudaStreamWaitEvent(h->s_in, h->ev[0], 0), "wait");
-  ck(cudaStreamWaitEvent(h->s_out, h->ev[0], 0), "wait");
-  for (size_t k = 0; k < parts.size(); ++k) {
-    const auto [c0, w] = parts[k];
-    ck(cudaMemcpy2DAsync(h->xstage + c0, dpad * sizeof(float), x + c0, ldx * sizeof(float),
-                         w * sizeof(float), L.n_cols, cudaMemcpyHostToDevice, h->s_in),
-       "H2D X");
-    ck(cudaEventRecord(h->ev[1 + k], h->s_in), "event");
-  }
-  uint32_t launches = 0;
-  for (size_t k = 0; k < parts.size(); ++k) {
-    const auto [c0, w] = parts[k];
-    ck(cudaStreamWaitEvent(s, h->ev[1 + k], 0), "wait");
-    device_spmm(h, h->xstage + c0, dpad, w, h->ystage + c0, dpad, stream, false);
-    launches += h->last_launches;
-    ck(cudaEventRecord(h->ev[1 + kHostChunks + k], s), "event");
-    ck(cudaStreamWaitEvent(h->s_out, h->ev[1 + kHostChunks + k], 0), "wait");
-    ck(cudaMemcpy2DAsync(y + c0, ldy * sizeof(float), h->ystage + c0, dpad * sizeof(float),
-                         w * sizeof(float), L.n_rows, cudaMemcpyDeviceToHost, h->s_out),
-       "D2H Y");
-  }
-  h->last_launches = launches;  // kernels launched by this call (one per chunk)
-  // the caller's stream resumes after the last copy-out
-  ck(cudaEventRecord(h->ev[0], h->s_out), "event");
-  ck(cudaStreamWaitEvent(s, h->ev[0], 0), "wait");
-  if (wait) device_spmm_host_wait(h, stream);
-}
-
-void device_spmm_host_wait(DeviceMatrix* h, void* stream) {
-  ck(cudaSetDevice(h->device), "cudaSetDevice");
-  ck(cudaStreamSynchronize(h->s_out), "spmm_host synchronize");
-  ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "spmm_host synchronize");
 }
 
 }  // namespace cbmb

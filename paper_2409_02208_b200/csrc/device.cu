@@ -1,0 +1,191 @@
+// The device operator's host side: upload (validation, layout, device
+// arrays), workspace reservation, release, and the host-buffer entry point
+// (column chunks of X and Y overlapped with the multiply on copy streams).
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "cuda_common.hpp"
+
+namespace cbmb {
+
+DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& opt) {
+  // validate + plan on the host first: malformed input is EINVAL, never a CUDA error
+  const uint32_t gain = opt.flatten_gain < 0 ? 16u : uint32_t(opt.flatten_gain);
+  // resident warps for the auto split: ~20 per SM (the multiply's occupancy);
+  // without a device the upload fails after validation anyway
+  int sms = 148, cur = 0;
+  if (cudaGetDevice(&cur) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount,
+                             opt.device >= 0 ? opt.device : cur) != cudaSuccess)
+    sms = 148;
+  cudaGetLastError();  // a failed probe must not leak into later error checks
+  Layout L = plan_layout(v, opt.order_faithful != 0, opt.split_threshold, opt.chunk, gain,
+                         uint32_t(sms) * 20);
+  auto* h = new DeviceMatrix;
+  try {
+    int dev = opt.device;
+    if (dev < 0) ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+    h->device = dev;
+    h->opt = opt;
+    ck(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    ck(cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, dev), "attr");
+    auto put = [&](auto*& dst, const auto& vec, const char* what) {
+      using E = typename std::remove_reference_t<decltype(vec)>::value_type;
+      const size_t bytes = std::max<size_t>(vec.size(), 1) * sizeof(E);
+      ck(cudaMalloc(&dst, bytes), what);
+      if (!vec.empty()) ck(cudaMemcpy(dst, vec.data(), vec.size() * sizeof(E),
+                                      cudaMemcpyHostToDevice), what);
+      h->device_bytes += vec.size() * sizeof(E);
+    };
+    put(h->dcol, L.dcol, "upload dcol");
+    put(h->rec, L.rec, "upload rec");
+    if (L.normalized) {
+      put(h->srow, L.srow, "upload srow");
+      put(h->scale, L.scale, "upload scale");
+      // the signed delta values in dcol order (bit-identical to the CBM's
+      // values: +-row_scale[col], validated by plan_layout)
+      std::vector<float> dval(L.dcol.size());
+      for (size_t k = 0; k < dval.size(); ++k) {
+        const float sc = L.scale[L.dcol[k] & 0x7FFFFFFFu];
+        dval[k] = (L.dcol[k] >> 31) ? -sc : sc;
+      }
+      put(h->dval, dval, "upload dval");
+    }
+    int coop = 0;
+    ck(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev), "attr");
+    if (!coop) throw cuda_error("device lacks cooperative launch", CBM_B200_ECUDA);
+    // keep only sizes on the host
+    L.dcol = {};
+    h->item_dep.resize(size_t(L.n_items) * 3);  // for the ticket schedule
+    for (uint32_t t = 0; t < L.n_items; ++t) {
+      h->item_dep[size_t(t) * 3] = L.rec[size_t(t) * 8 + 3];
+      h->item_dep[size_t(t) * 3 + 1] = L.rec[size_t(t) * 8 + 5];
+      h->item_dep[size_t(t) * 3 + 2] = L.rec[size_t(t) * 8 + 6];
+    }
+    L.rec = {};  // item_beg and item_dep stay: they drive the ticket schedule
+    L.srow = {};
+    L.scale = {};
+    h->info = std::move(L);
+  } catch (...) {
+    device_free(h);
+    throw;
+  }
+  return h;
+}
+
+void device_free(DeviceMatrix* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->s_in) {
+    cudaStreamDestroy(h->s_in);
+    cudaStreamDestroy(h->s_out);
+    for (auto e : h->ev) cudaEventDestroy(e);
+  }
+  for (auto& kv : h->schedules) cudaFree(kv.second.trec);
+  for (auto& kv : h->ws)
+    for (void* p : {(void*)kv.second.flags, (void*)kv.second.partial, (void*)kv.second.interior,
+                    (void*)kv.second.xs, (void*)kv.second.gcn_h})
+      if (p) cudaFree(p);
+  for (void* p : {(void*)h->dcol, (void*)h->dval, (void*)h->rec, (void*)h->srow, (void*)h->scale,
+                  (void*)h->xstage, (void*)h->ystage})
+    if (p) cudaFree(p);
+  delete h;
+}
+
+void device_reserve(DeviceMatrix* h, uint64_t d, void* stream) {
+  const Layout& L = h->info;
+  const uint64_t dpad = (d + 3) & ~uint64_t(3);
+  const uint64_t slabs = (d + 31) / 32;  // worst case (V = 1)
+  ck(cudaSetDevice(h->device), "cudaSetDevice");
+  auto& ws = h->ws[stream];
+  if (uint64_t(L.n_items) * slabs > ws.flags_cap) {
+    grow(ws.flags, ws.flags_cap, uint64_t(L.n_items) * slabs, "workspace flags");
+    ck(cudaMemset(ws.flags, 0, ws.flags_cap * sizeof(uint32_t)), "flags memset");
+    ws.epoch = 0;
+  }
+  grow(ws.partial, ws.partial_cap, uint64_t(L.n_chunk_items) * dpad, "workspace partial");
+  if (L.normalized) grow(ws.interior, ws.interior_cap, uint64_t(L.n_interior) * dpad,
+                         "workspace interior");
+}
+
+// Host-buffer entry point. Columns are independent (kernels.cpp:27-62), so X
+// and Y move in column chunks on three streams: H2D of chunk k+1 and D2H of
+// chunk k-1 run while chunk k multiplies, and the two copy directions overlap
+// on the full-duplex PCIe link. One chunk when the operand is small.
+void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
+                      int64_t ldy, void* stream, bool wait) {
+  const Layout& L = h->info;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ck(cudaSetDevice(h->device), "cudaSetDevice");
+  const uint32_t dpad = (d + 3) & ~3u;
+  grow(h->xstage, h->xstage_cap, uint64_t(L.n_cols) * dpad, "staging X");
+  grow(h->ystage, h->ystage_cap, uint64_t(L.n_rows) * dpad, "staging Y");
+  if (!h->s_in) {
+    ck(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking), "stream");
+    for (auto& e : h->ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
+  const uint64_t bytes = (uint64_t(L.n_cols) + L.n_rows) * d * sizeof(float);
+  // Column chunks (16-byte aligned): the first chunk's H2D and the last
+  // chunk's D2H cannot overlap anything, so those two are narrow (d/8) and
+  // the middle is cut in three (tools/probe_e2e.py: uniform x4 1109 us,
+  // x8 1151 us on cfg[1]; rows narrower than 64 floats slow the 2D copies).
+  std::vector<std::pair<uint32_t, uint32_t>> parts;  // (first column, width)
+  auto r4 = [](uint32_t v) { return (v + 3) & ~3u; };
+  uint32_t chunks = 1;
+  if (bytes >= (8u << 20) && d >= 128) chunks = d >= 256 ? 5 : 2;
+  if (const char* e = std::getenv("CBM_B200_HOST_CHUNKS"))  // dev tool: uniform chunks
+    chunks = std::max<uint32_t>(1, std::min<uint32_t>({kHostChunks, uint32_t(std::atoi(e)), d}));
+  if (chunks == 5 && !std::getenv("CBM_B200_HOST_CHUNKS")) {  // d >= 256
+    const uint32_t edge = r4(d / 8), rest = d - 2 * edge, mid = r4((rest + 2) / 3);
+    uint32_t c0 = 0;
+    const uint32_t m3 = (rest - 2 * mid) & ~3u;  // every chunk starts 16-byte aligned
+    for (uint32_t w : {edge, mid, mid, m3, d - edge - 2 * mid - m3}) {
+      parts.emplace_back(c0, w);
+      c0 += w;
+    }
+  } else {
+    const uint32_t cw = r4((d + chunks - 1) / chunks);
+    for (uint32_t c0 = 0; c0 < d; c0 += cw) parts.emplace_back(c0, std::min(cw, d - c0));
+  }
+  // ev[0]: caller's prior work on s; ev[1+k]: X chunk k landed; ev[1+C+k]: Y chunk k ready
+  ck(cudaEventRecord(h->ev[0], s), "event");
+  ck(cudaStreamWaitEvent(h->s_in, h->ev[0], 0), "wait");
+  ck(cudaStreamWaitEvent(h->s_out, h->ev[0], 0), "wait");
+  for (size_t k = 0; k < parts.size(); ++k) {
+    const auto [c0, w] = parts[k];
+    ck(cudaMemcpy2DAsync(h->xstage + c0, dpad * sizeof(float), x + c0, ldx * sizeof(float),
+                         w * sizeof(float), L.n_cols, cudaMemcpyHostToDevice, h->s_in),
+       "H2D X");
+    ck(cudaEventRecord(h->ev[1 + k], h->s_in), "event");
+  }
+  uint32_t launches = 0;
+  for (size_t k = 0; k < parts.size(); ++k) {
+    const auto [c0, w] = parts[k];
+    ck(cudaStreamWaitEvent(s, h->ev[1 + k], 0), "wait");
+    device_spmm(h, h->xstage + c0, dpad, w, h->ystage + c0, dpad, stream, false);
+    launches += h->last_launches;
+    ck(cudaEventRecord(h->ev[1 + kHostChunks + k], s), "event");
+    ck(cudaStreamWaitEvent(h->s_out, h->ev[1 + kHostChunks + k], 0), "wait");
+    ck(cudaMemcpy2DAsync(y + c0, ldy * sizeof(float), h->ystage + c0, dpad * sizeof(float),
+                         w * sizeof(float), L.n_rows, cudaMemcpyDeviceToHost, h->s_out),
+       "D2H Y");
+  }
+  h->last_launches = launches;  // kernels launched by this call (one per chunk)
+  // the caller's stream resumes after the last copy-out
+  ck(cudaEventRecord(h->ev[0], h->s_out), "event");
+  ck(cudaStreamWaitEvent(s, h->ev[0], 0), "wait");
+  if (wait) device_spmm_host_wait(h, stream);
+}
+
+void device_spmm_host_wait(DeviceMatrix* h, void* stream) {
+  ck(cudaSetDevice(h->device), "cudaSetDevice");
+  ck(cudaStreamSynchronize(h->s_out), "spmm_host synchronize");
+  ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "spmm_host synchronize");
+}
+
+}  // namespace cbmb
