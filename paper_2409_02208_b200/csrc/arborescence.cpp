@@ -58,8 +58,9 @@ struct Heaps {
     lazy[n] = 0;
   }
   uint8_t rk(uint32_t n) const { return n == kNil ? 0 : rank[n]; }
-  // iterative leftist merge along the right spines
-  uint32_t merge(uint32_t a, uint32_t b) {
+  // iterative leftist merge along the right spines (scratch: the spine)
+  uint32_t merge(uint32_t a, uint32_t b) { return merge_with(a, b, spine); }
+  uint32_t merge_with(uint32_t a, uint32_t b, std::vector<uint32_t>& spine) {
     if (a == kNil) return b;
     if (b == kNil) return a;
     spine.clear();
@@ -105,7 +106,9 @@ struct Dsu {
 
 }  // namespace
 
-std::vector<uint32_t> min_arborescence_heap(const EdgeLists& e, uint32_t m, uint32_t* n_rounds) {
+std::vector<uint32_t> min_arborescence_heap(const EdgeLists& e, uint32_t m, uint32_t* n_rounds,
+                                            int threads) {
+  if (threads < 1) threads = 1;
   const uint64_t E = e.src.size();
   if (E >= 0xFFFFFFFFull) throw logic_error("arborescence: too many candidate edges");
   for (uint32_t x = 0; x < m; ++x)
@@ -113,8 +116,10 @@ std::vector<uint32_t> min_arborescence_heap(const EdgeLists& e, uint32_t m, uint
       throw logic_error("arborescence: row " + std::to_string(x) + " has no virtual edge");
   if (m == 0) return {};
   std::vector<uint32_t> odst(E);
-  for (uint32_t x = 0; x < m; ++x)
-    for (uint64_t k = e.ptr[x]; k < e.ptr[x + 1]; ++k) odst[k] = x + 1;
+  parallel_for_chunks(m, threads, [&](size_t lo, size_t hi, int) {
+    for (size_t x = lo; x < hi; ++x)
+      for (uint64_t k = e.ptr[x]; k < e.ptr[x + 1]; ++k) odst[k] = uint32_t(x + 1);
+  });
 
   Heaps H;
   H.key.resize(E);
@@ -133,21 +138,22 @@ std::vector<uint32_t> min_arborescence_heap(const EdgeLists& e, uint32_t m, uint
   Dsu dsu;
   dsu.p.resize(cap);
   std::iota(dsu.p.begin(), dsu.p.end(), 0u);
-  // initial heaps: balanced pairwise merging of each row's in-edges
-  {
-    std::vector<uint32_t> q;
-    for (uint32_t x = 0; x < m; ++x) {
+  // initial heaps: balanced pairwise merging of each row's in-edges (rows
+  // own disjoint edge nodes, so they build in parallel)
+  parallel_for_chunks(m, threads, [&](size_t lo, size_t hi, int) {
+    std::vector<uint32_t> q, spine;
+    for (size_t x = lo; x < hi; ++x) {
       q.clear();
       for (uint64_t k = e.ptr[x]; k < e.ptr[x + 1]; ++k) q.push_back(uint32_t(k));
       while (q.size() > 1) {
         size_t o = 0;
-        for (size_t i = 0; i + 1 < q.size(); i += 2) q[o++] = H.merge(q[i], q[i + 1]);
+        for (size_t i = 0; i + 1 < q.size(); i += 2) q[o++] = H.merge_with(q[i], q[i + 1], spine);
         if (q.size() & 1) q[o++] = q.back();
         q.resize(o);
       }
       heap[x + 1] = q[0];
     }
-  }
+  });
   // super-node bookkeeping for the expansion: members and their cycle edges
   std::vector<uint32_t> mem_ptr{0}, mem_node, mem_edge;
 

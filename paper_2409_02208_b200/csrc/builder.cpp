@@ -193,6 +193,7 @@ EdgeLists candidate_edges(const Csr& a, uint64_t alpha, int threads) {
           for (uint32_t y : cand) {
             const uint64_t ny = a.row_nnz(y);
             const uint64_t t = need(ny);
+            if (t > nx) continue;  // size filter: ov <= nx < t, (*) cannot hold
             const uint32_t* ry = a.row(y);
             uint64_t ov = 0;
             for (uint64_t k = 0; k < ny; ++k) {
@@ -517,7 +518,7 @@ HostCbm build_cbm(const Csr& a, uint64_t alpha, int threads, int algo) {
   c.candidate_edges = e.src.size();
   const auto t1 = Clock::now();
   c.parent = algo == 1 ? min_arborescence(e, a.n_rows, threads, &c.rounds)
-                       : min_arborescence_heap(e, a.n_rows, &c.rounds);
+                       : min_arborescence_heap(e, a.n_rows, &c.rounds, threads);
   EdgeLists().ptr.swap(e.ptr);
   std::vector<uint32_t>().swap(e.src);
   std::vector<uint32_t>().swap(e.w);

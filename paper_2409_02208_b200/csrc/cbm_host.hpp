@@ -86,7 +86,8 @@ EdgeLists candidate_edges(const Csr& a, uint64_t alpha, int threads);
 std::vector<uint32_t> min_arborescence(const EdgeLists& e, uint32_t m, int threads,
                                        uint32_t* rounds);
 // Same arborescence with mergeable heaps, O(E log E) (arborescence.cpp).
-std::vector<uint32_t> min_arborescence_heap(const EdgeLists& e, uint32_t m, uint32_t* rounds);
+std::vector<uint32_t> min_arborescence_heap(const EdgeLists& e, uint32_t m, uint32_t* rounds,
+                                            int threads = 1);
 
 // ---- parallel helper (the reference's parallel_chunks, parallel.hpp:13-32)
 template <typename Fn>
