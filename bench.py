@@ -58,6 +58,12 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # dev-only plumbing check of the N-rank code path on a one-GPU box:
+    # BENCH_DEV_SHARE_GPU=1 puts every rank on cuda:0 with gloo collectives
+    # (no data-path collective exists, so ranks never wait on each other's
+    # kernels; numbers from such a run are not bench values)
+    if os.environ.get("BENCH_DEV_SHARE_GPU") == "1":
+        local = 0
     return rank, world, local
 
 
@@ -202,7 +208,10 @@ def run_ours(args, wl):
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("BENCH_DEV_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         dist = None
         torch.cuda.set_device(local)
@@ -282,7 +291,8 @@ def run_ours(args, wl):
         if dist:
             dist.barrier()
 
-    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64,
+                     device="cpu" if os.environ.get("BENCH_DEV_SHARE_GPU") == "1" else dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, e2e_ms = float(t[0]), float(t[1])
