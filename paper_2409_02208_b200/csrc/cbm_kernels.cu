@@ -354,8 +354,16 @@ constexpr int kWarpsPerCta = 4;
 #else
 #define CBM_LAUNCH_BOUNDS(U) __launch_bounds__(kWarpsPerCta * 32)
 #endif
+#ifndef CBM_RECWIN_U2
+#define CBM_RECWIN_U2 64
+#endif
+#ifndef CBM_RECWIN_U1
+#define CBM_RECWIN_U1 64
+#endif
 template <int U>
-constexpr uint32_t rec_window() { return U == 4 ? CBM_RECWIN_U4 : kRecWin; }
+constexpr uint32_t rec_window() {
+  return U == 4 ? CBM_RECWIN_U4 : (U == 2 ? CBM_RECWIN_U2 : CBM_RECWIN_U1);
+}
 
 template <int V, int U, int D>
 struct alignas(16) WarpSmem {
