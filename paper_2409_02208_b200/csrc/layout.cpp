@@ -200,6 +200,9 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
     }
   }
   L.nnz_effective = eptr[m];
+  if (L.nnz_effective >= 0xFFFFFFFFull)  // dcol offsets are 32-bit on the device
+    throw invalid_argument("upload: more than 2^32-1 deltas after flattening "
+                           "(upload with flatten_gain = 0)");
 
   // ROW items: by depth, ascending row id inside a level (stable counting sort)
   uint32_t max_depth = 0;
