@@ -138,6 +138,14 @@ typedef struct cbm_b200_options {
   int32_t prefetch;          /* 1: bulk-prefetch a contiguous X that fits in
                                 half of L2 before gathering; 0 (default): off
                                 (measured neutral on cfg[0]/cfg[1]) */
+  int32_t tile;              /* default mode only: tiled path: one
+                                CTA per (row block, column slab) with the block's
+                                re-used X rows staged in shared memory. -1 auto
+                                (used when most deltas hit staged rows and each
+                                staged row is re-used enough), 0 off, 1 force */
+  uint32_t tile_rows;        /* rows per tile block (0 = auto, 64..512) */
+  uint32_t tile_stage;       /* staged X rows per block (0 = auto, 640) */
+  int32_t tile_vec;          /* floats per lane of a tile slab: 0 auto, 1, 2, 4 */
 } cbm_b200_options;
 
 void cbm_b200_default_options(cbm_b200_options* opt);
@@ -231,6 +239,12 @@ typedef struct cbm_b200_info {
   uint32_t launches_per_call;/* kernels launched by the last spmm call */
   int32_t is_normalized;
   int32_t order_faithful;
+  int32_t tile_active;       /* multiplies with d >= 32 take the tiled path */
+  uint32_t tile_blocks;      /* row blocks of the tiled layout (0: not planned) */
+  uint32_t tile_max_rows, tile_max_staged, tile_cut_rows;
+  uint64_t tile_deltas;      /* entries the tiled kernel sums (cut rows flattened) */
+  uint64_t tile_staged_deltas; /* of which read from the shared-memory tile */
+  uint64_t tile_staged_rows;   /* staged X rows over all blocks */
 } cbm_b200_info;
 int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* out);
 

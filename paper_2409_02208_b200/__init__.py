@@ -75,7 +75,8 @@ class _Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("order_faithful", C.c_int32),
                 ("split_threshold", C.c_uint32), ("chunk", C.c_uint32), ("prescale", C.c_int32),
                 ("kernel", C.c_int32), ("max_segments", C.c_int32),
-                ("flatten_gain", C.c_int32), ("prefetch", C.c_int32)]
+                ("flatten_gain", C.c_int32), ("prefetch", C.c_int32), ("tile", C.c_int32),
+                ("tile_rows", C.c_uint32), ("tile_stage", C.c_uint32), ("tile_vec", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -85,7 +86,11 @@ class _Info(C.Structure):
                 ("n_items", C.c_uint32), ("n_chunk_items", C.c_uint32),
                 ("max_row_deltas", C.c_uint32), ("device_bytes", C.c_uint64),
                 ("launches_per_call", C.c_uint32), ("is_normalized", C.c_int32),
-                ("order_faithful", C.c_int32)]
+                ("order_faithful", C.c_int32), ("tile_active", C.c_int32),
+                ("tile_blocks", C.c_uint32), ("tile_max_rows", C.c_uint32),
+                ("tile_max_staged", C.c_uint32), ("tile_cut_rows", C.c_uint32),
+                ("tile_deltas", C.c_uint64), ("tile_staged_deltas", C.c_uint64),
+                ("tile_staged_rows", C.c_uint64)]
 
 
 class _Stats(C.Structure):
@@ -413,7 +418,8 @@ class DeviceCbm:
     def __init__(self, c: CbmMatrix, device: int | None = None, order_faithful: bool = False,
                  split_threshold: int = 0, chunk: int = 0, prescale: int = -1,
                  kernel: str = "auto", max_segments: int = 0, flatten_gain: int = -1,
-                 prefetch: bool = False):
+                 prefetch: bool = False, tile: int = -1, tile_rows: int = 0,
+                 tile_stage: int = 0, tile_vec: int = 0):
         opt = _Options()
         _lib.cbm_b200_default_options(C.byref(opt))
         opt.device = -1 if device is None else int(device)
@@ -427,6 +433,10 @@ class DeviceCbm:
         opt.max_segments = max_segments
         opt.flatten_gain = flatten_gain
         opt.prefetch = int(prefetch)
+        opt.tile = int(tile)
+        opt.tile_rows = tile_rows
+        opt.tile_stage = tile_stage
+        opt.tile_vec = tile_vec
         self._h = _vp()
         view = c._view()
         _check(_lib.cbm_b200_upload(C.byref(view), C.byref(opt), C.byref(self._h)))

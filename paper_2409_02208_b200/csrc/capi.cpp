@@ -200,6 +200,10 @@ void cbm_b200_default_options(cbm_b200_options* o) {
   o->max_segments = 0;
   o->flatten_gain = -1;
   o->prefetch = 0;
+  o->tile = -1;
+  o->tile_rows = 0;
+  o->tile_stage = 0;
+  o->tile_vec = 0;
 }
 
 int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
@@ -212,6 +216,9 @@ int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
     if (opt) o = *opt;
     need(o.kernel == 0 || o.kernel == 1, "upload: options.kernel must be 0 (auto) or 1 (scalar)");
     need(o.max_segments >= 0 && o.max_segments <= 4, "upload: options.max_segments must be 0..4");
+    need(o.tile >= -1 && o.tile <= 1, "upload: options.tile must be -1, 0 or 1");
+    need(o.tile_vec == 0 || o.tile_vec == 1 || o.tile_vec == 2 || o.tile_vec == 4,
+         "upload: options.tile_vec must be 0, 1, 2 or 4");
     auto* h = new cbm_b200_matrix{nullptr};
     try {
       h->d = cbmb::device_upload(*c, o);
@@ -395,6 +402,15 @@ int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* o) {
     o->launches_per_call = h->d->last_launches;
     o->is_normalized = L.normalized ? 1 : 0;
     o->order_faithful = L.order_faithful ? 1 : 0;
+    const auto& T = h->d->tile;
+    o->tile_active = h->d->tile_on ? 1 : 0;
+    o->tile_blocks = T.n_blocks;
+    o->tile_max_rows = T.max_rows;
+    o->tile_max_staged = T.max_staged;
+    o->tile_cut_rows = T.n_cut;
+    o->tile_deltas = T.n_deltas;
+    o->tile_staged_deltas = T.n_staged_deltas;
+    o->tile_staged_rows = T.n_staged_cols;
   });
 }
 

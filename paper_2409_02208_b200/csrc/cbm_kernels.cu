@@ -931,6 +931,14 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   device_reserve(h, d, stream);
   auto& ws = h->ws[stream];
   const uint32_t dpad = (d + 3) & ~3u;
+  // tiled path (tile_kernel.cu): community-structured matrices, d >= 32
+  if (h->tile_on && d >= 32) {
+    if (const uint32_t tv = tile_pick_vec(h, d, x, ldx, y, ldy)) {
+      tile_spmm(h, tv, x, ldx, d, y, ldy, ws.tinterior, dpad, relu, s);
+      h->last_launches = 1;
+      return;
+    }
+  }
   bool prescale = false;
   if (L.normalized) {
     if (h->opt.prescale > 0) prescale = true;

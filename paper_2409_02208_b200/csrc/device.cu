@@ -55,6 +55,26 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       }
       put(h->dval, dval, "upload dval");
     }
+    // tiled path (default mode): planned here, kept only when it pays
+    if (!L.order_faithful && opt.tile != 0 && v.n_rows > 0) {
+      TileLayout T = plan_tiles(v, opt.tile_rows, opt.tile_stage, uint32_t(h->num_sms));
+      const double frac = T.n_deltas ? double(T.n_staged_deltas) / double(T.n_deltas) : 0.0;
+      const double reuse = T.n_staged_cols ? double(T.n_staged_deltas) / double(T.n_staged_cols) : 0.0;
+      h->tile_on = opt.tile == 1 || (frac >= kTileMinStagedFrac && reuse >= kTileMinReuse);
+      if (h->tile_on) {
+        put(h->tdcol, T.dcol, "upload tile dcol");
+        if (L.normalized) put(h->tdval, T.dval, "upload tile dval");
+        put(h->trow, T.row, "upload tile rows");
+        put(h->tblock, T.block, "upload tile blocks");
+        put(h->tstage, T.stage, "upload tile stage");
+      }
+      T.dcol = {};
+      T.dval = {};
+      T.row = {};
+      T.block = {};
+      T.stage = {};
+      h->tile = std::move(T);
+    }
     int coop = 0;
     ck(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev), "attr");
     if (!coop) throw cuda_error("device lacks cooperative launch", CBM_B200_ECUDA);
@@ -90,8 +110,11 @@ void device_free(DeviceMatrix* h) {
     for (void* p : {(void*)kv.second.flags, (void*)kv.second.partial, (void*)kv.second.interior,
                     (void*)kv.second.xs, (void*)kv.second.gcn_h})
       if (p) cudaFree(p);
+  for (auto& kv : h->ws)
+    if (kv.second.tinterior) cudaFree(kv.second.tinterior);
   for (void* p : {(void*)h->dcol, (void*)h->dval, (void*)h->rec, (void*)h->srow, (void*)h->scale,
-                  (void*)h->xstage, (void*)h->ystage})
+                  (void*)h->xstage, (void*)h->ystage, (void*)h->tdcol, (void*)h->tdval,
+                  (void*)h->trow, (void*)h->tblock, (void*)h->tstage})
     if (p) cudaFree(p);
   delete h;
 }
@@ -110,6 +133,8 @@ void device_reserve(DeviceMatrix* h, uint64_t d, void* stream) {
   grow(ws.partial, ws.partial_cap, uint64_t(L.n_chunk_items) * dpad, "workspace partial");
   if (L.normalized) grow(ws.interior, ws.interior_cap, uint64_t(L.n_interior) * dpad,
                          "workspace interior");
+  if (h->tile_on) grow(ws.tinterior, ws.tinterior_cap, uint64_t(h->tile.n_interior) * dpad,
+                       "workspace tile interior");
 }
 
 // Host-buffer entry point. Columns are independent (kernels.cpp:27-62), so X

@@ -13,6 +13,7 @@
 
 #include "errors.hpp"
 #include "layout.hpp"
+#include "tile_layout.hpp"
 
 namespace cbmb {
 
@@ -31,6 +32,14 @@ struct DeviceMatrix {
   float* srow = nullptr;
   float* scale = nullptr;
   uint64_t device_bytes = 0;
+  // tiled path (tile_layout.hpp): sizes in `tile` (host vectors released)
+  bool tile_on = false;
+  TileLayout tile;
+  uint32_t* tdcol = nullptr;
+  float* tdval = nullptr;
+  uint32_t* trow = nullptr;
+  uint32_t* tblock = nullptr;
+  uint32_t* tstage = nullptr;
   // per-call workspace, one per stream (concurrent calls on distinct streams
   // never share flags or scratch); grown on demand, or by cbm_b200_reserve
   struct Workspace {
@@ -40,6 +49,8 @@ struct DeviceMatrix {
     uint64_t partial_cap = 0;    // floats
     float* interior = nullptr;
     uint64_t interior_cap = 0;
+    float* tinterior = nullptr;  // tiled path: unscaled rows with children
+    uint64_t tinterior_cap = 0;
     float* xs = nullptr;         // pre-scaled operand (normalized, prescale on)
     uint64_t xs_cap = 0;
     float* gcn_h = nullptr;      // GCN hidden activations (2 x n x hid)
@@ -82,5 +93,10 @@ void device_gcn_forward(DeviceMatrix* h, const float* x, uint32_t n, uint32_t f,
 void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
                       int64_t ldy, void* stream, bool wait = true);
 void device_spmm_host_wait(DeviceMatrix* h, void* stream);
+// tiled path (tile_kernel.cu): slab vector width for a call (0 = not usable)
+uint32_t tile_pick_vec(const DeviceMatrix* h, uint32_t d, const float* x, int64_t ldx,
+                       const float* y, int64_t ldy);
+void tile_spmm(DeviceMatrix* h, uint32_t V, const float* x, int64_t ldx, uint32_t d, float* y,
+               int64_t ldy, float* interior, uint32_t dpad, bool relu, cudaStream_t s);
 
 }  // namespace cbmb

@@ -31,7 +31,14 @@ def lane_groups(d):
     return 4 <= d <= 64 and d % 4 == 0
 
 
+def tiled(info, d):
+    """The default mode's tiled path (d >= 32) sums staged deltas, then cold
+    deltas, then the parent: order changed, integer sums unchanged."""
+    return bool(info["tile_active"]) and d >= 32
+
+
 def gpu_spmm(c, x, dev, **opt):
+    opt.setdefault("tile", 0)  # the streaming kernel; tests/test_tile_gpu.py covers tile=1/-1
     d = P.DeviceCbm(c, **opt)
     xt = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(dev)
     y = d.spmm(xt)
@@ -57,6 +64,7 @@ def test_golden_fixture_bitwise(name, faithful, dev):
         got, d = gpu_spmm(c, g["x"], dev, order_faithful=faithful)
         info = d.info()
     split = info["n_chunk_items"] > 0 or info["n_flattened"] > 0
+    split = split or (not faithful and kind != "spmv" and tiled(info, g["x"].shape[1]))
     integer = np.array_equal(g["x"], np.round(g["x"]))
     fused = c.is_normalized and not faithful  # default mode: fma(x, +-s_c, acc)
     grouped = not faithful and kind != "spmv" and lane_groups(g["x"].shape[1])
@@ -135,7 +143,7 @@ def test_random_suite_bitwise(normalized, kernel, dev):
         info = h.info()
         # default mode: spmv (d = 1) sums a row's deltas lane-parallel
         if (info["n_flattened"] or info["n_chunk_items"] or normalized or x.shape[1] == 1
-                or lane_groups(x.shape[1])):
+                or lane_groups(x.shape[1]) or tiled(info, x.shape[1])):
             assert normwise_err(got, want) <= TOL, f"case {k}"
         else:
             assert_bitwise(got, want, f"default case {k}")
