@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order-faithful", action="store_true")
     ap.add_argument("--kernel", default="auto", choices=["auto", "scalar"])
+    ap.add_argument("--tile", type=int, default=-1, choices=[-1, 0, 1],
+                    help="tiled path: -1 auto (community-structured matrices), 0 off, 1 force")
     ap.add_argument("--no-csr-comparator", action="store_true",
                     help="skip timing the uncompressed (CSR) matrix with the same kernel")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
@@ -224,7 +226,8 @@ def run_ours(args, wl):
     c = wl.build(a, args.threads)
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
-    op = P.DeviceCbm(c, device=local, order_faithful=args.order_faithful, kernel=args.kernel)
+    op = P.DeviceCbm(c, device=local, order_faithful=args.order_faithful, kernel=args.kernel,
+                     tile=args.tile)
     torch.cuda.synchronize()
     t_upload = time.perf_counter() - t0
     info = op.info()
@@ -308,17 +311,33 @@ def run_ours(args, wl):
     peak, peak_src = peaks()
     b_alg_local = b_alg_bytes(info["nnz_delta"], a.n_rows, a.n_cols, d_local, wl.normalized)
     achieved = b_alg_local / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    tiled = bool(info["tile_active"]) and d_local >= 32
+    if tiled:
+        # tiled path: staged X rows come through L2 once per (block, slab) unit,
+        # cold deltas gather their rows from L2, staged deltas read shared memory
+        l2_bytes = (int(info["tile_staged_rows"]) + int(info["tile_deltas"])
+                    - int(info["tile_staged_deltas"])) * d_local * 4
+        smem_bytes = int(info["tile_staged_deltas"]) * d_local * 4
+    else:
+        l2_bytes = int(info["nnz_effective"]) * d_local * 4
+        smem_bytes = 0
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic_for(wl.name),
-                "b_alg_bytes": b_alg_local, "kernel": "cbm_kernel",
+                "b_alg_bytes": b_alg_local, "kernel": "tile_kernel" if tiled else "cbm_kernel",
                 "peak_source": peak_src,
                 # what actually bounds the gather: X rows moved L2 -> SM per step
                 # (one row per summed delta) against the measured gather rate of
                 # profiles/r01_ubench_gather.txt
-                "l2_gather": {"bytes": int(info["nnz_effective"]) * d_local * 4,
-                              "achieved_tbps": int(info["nnz_effective"]) * d_local * 4
-                              / (ms * 1e-3) / 1e12 if ms > 0 else 0.0,
+                "l2_gather": {"bytes": l2_bytes,
+                              "achieved_tbps": l2_bytes / (ms * 1e-3) / 1e12 if ms > 0 else 0.0,
                               "measured_peak_tbps": 15.7}}
+    if tiled:
+        roofline["smem_gather"] = {
+            "bytes": smem_bytes,
+            "achieved_tbps": smem_bytes / (ms * 1e-3) / 1e12 if ms > 0 else 0.0,
+            "staged_fraction": int(info["tile_staged_deltas"]) / max(1, int(info["tile_deltas"])),
+            "blocks": int(info["tile_blocks"]),
+            "note": "staged deltas read the shared-memory X tile (128 B/clk/SM LSU limit)"}
 
     gpu_csr = None
     if not args.no_csr_comparator:
@@ -386,6 +405,7 @@ def run_ours(args, wl):
                       "alpha": wl.alpha, "normalized": wl.normalized,
                       "parallelism": f"column-shard x{world}",
                       "order_faithful": bool(args.order_faithful), "kernel": args.kernel,
+                      "tile": args.tile,
                       "l2": "flushed (256 MiB write) before every timed step",
                       "levels": info["n_levels"], "chunk_items": info["n_chunk_items"],
                       "actual_ops_per_step": int(sum(P.count_scalar_ops(c)) * d_local),

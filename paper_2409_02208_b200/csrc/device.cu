@@ -57,7 +57,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
     }
     // tiled path (default mode): planned here, kept only when it pays
     if (!L.order_faithful && opt.tile != 0 && v.n_rows > 0) {
-      TileLayout T = plan_tiles(v, opt.tile_rows, opt.tile_stage, uint32_t(h->num_sms));
+      TileLayout T = plan_tiles(v, opt.tile_rows, opt.tile_stage, uint32_t(h->num_sms), gain);
       const double frac = T.n_deltas ? double(T.n_staged_deltas) / double(T.n_deltas) : 0.0;
       const double reuse = T.n_staged_cols ? double(T.n_staged_deltas) / double(T.n_staged_cols) : 0.0;
       h->tile_on = opt.tile == 1 || (frac >= kTileMinStagedFrac && reuse >= kTileMinReuse);

@@ -16,6 +16,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "cuda_common.hpp"
 
@@ -44,7 +47,14 @@ struct TileParams {
   float* interior;  // unscaled rows with children, stride dpad
   uint32_t dpad, d, n_slabs, relu;
   uint32_t max_staged, max_rows;
+  unsigned long long* trace;  // dev tool (CBM_B200_TILE_TRACE): 4 x u64 per unit, else null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
@@ -103,6 +113,38 @@ __device__ __forceinline__ void load_idx(const uint32_t* q, uint32_t (&e)[D]) {
   }
 }
 
+// acc +-= the staged rows of entries [k0, k1) (a multiple of 8 long): 16
+// entries per step (two index vectors, 2*D tile reads in flight per lane)
+template <int H, bool SMEM, bool NEG>
+__device__ __forceinline__ void staged_run(const uint32_t* ix, uint32_t k0, uint32_t k1,
+                                           const float* xl, uint32_t g, float4& acc) {
+  constexpr int D = 8 / H;
+  constexpr uint32_t kW = 128u / H;
+  uint32_t k = k0;
+#pragma unroll 1
+  for (; k + 16 <= k1; k += 16) {
+    uint32_t e[D], f[D];
+    load_idx<D, SMEM>(ix + k + g * D, e);
+    load_idx<D, SMEM>(ix + k + 8 + g * D, f);
+    float4 v[2 * D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) v[q] = *reinterpret_cast<const float4*>(xl + e[q] * kW);
+#pragma unroll
+    for (int q = 0; q < D; ++q) v[D + q] = *reinterpret_cast<const float4*>(xl + f[q] * kW);
+#pragma unroll
+    for (int q = 0; q < 2 * D; ++q) acc = NEG ? f4sub(acc, v[q]) : f4add(acc, v[q]);
+  }
+  if (k < k1) {
+    uint32_t e[D];
+    load_idx<D, SMEM>(ix + k + g * D, e);
+    float4 v[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) v[q] = *reinterpret_cast<const float4*>(xl + e[q] * kW);
+#pragma unroll
+    for (int q = 0; q < D; ++q) acc = NEG ? f4sub(acc, v[q]) : f4add(acc, v[q]);
+  }
+}
+
 // One row's delta sum for this lane's group (H lane groups of 32/H lanes x 4
 // floats; group g takes deltas g*D .. g*D+D-1 of every 8). Indices come from
 // `ix` (shared-memory buffer, or global memory for rows longer than a buffer).
@@ -132,26 +174,8 @@ __device__ __forceinline__ float4 row_sum(const TileParams& p, const uint32_t* i
       cv[q] = __ldg(reinterpret_cast<const float4*>(p.x + (long long)(ce[q] & kLocalMask) * p.ldx + col));
   }
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
-  for (uint32_t k = 0; k < npos; k += 8) {
-    uint32_t e[D];
-    load_idx<D, SMEM>(ix + k + g * D, e);
-    float4 v[D];
-#pragma unroll
-    for (int q = 0; q < D; ++q) v[q] = *reinterpret_cast<const float4*>(xl + e[q] * kW);
-#pragma unroll
-    for (int q = 0; q < D; ++q) acc = f4add(acc, v[q]);
-  }
-#pragma unroll 1
-  for (uint32_t k = npos; k < nsk; k += 8) {
-    uint32_t e[D];
-    load_idx<D, SMEM>(ix + k + g * D, e);
-    float4 v[D];
-#pragma unroll
-    for (int q = 0; q < D; ++q) v[q] = *reinterpret_cast<const float4*>(xl + e[q] * kW);
-#pragma unroll
-    for (int q = 0; q < D; ++q) acc = f4sub(acc, v[q]);
-  }
+  staged_run<H, SMEM, false>(ix, 0, npos, xl, g, acc);
+  staged_run<H, SMEM, true>(ix, npos, nsk, xl, g, acc);
 #pragma unroll
   for (int q = 0; q < CPG; ++q) {
     const uint32_t c = g + uint32_t(H * q);
@@ -206,6 +230,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) tile_kernel(const Til
   float* ssc = reinterpret_cast<float*>(idxbuf + kWarps * 2 * kIdxCap);  // staged scales
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t col0 = slab * kW;
+  const unsigned long long t0 = p.trace ? gtimer() : 0ull;
 
   // ---- stage: row records, flags, the staged X rows (+ a zero row at nst)
   for (uint32_t i = tid; i < 2 * nrows; i += NT) cp_async16(recs + i, p.rows + 2ull * row0 + i, 16);
@@ -246,6 +271,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) tile_kernel(const Til
     __syncthreads();
   }
 
+  const unsigned long long t1 = p.trace ? gtimer() : 0ull;
   const uint32_t g = uint32_t(lane) / LG, gl = uint32_t(lane) % LG;
   const uint32_t colu = col0 + gl * 4;
   const bool act = colu < p.d;
@@ -317,6 +343,18 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) tile_kernel(const Til
     b ^= 1u;
   }
   cp_wait<0>();
+  if (p.trace) {
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+      unsigned long long* o = p.trace + 4 * (size_t)unit;
+      o[0] = sm;
+      o[1] = t0;
+      o[2] = t1;
+      o[3] = gtimer();
+    }
+  }
 }
 
 #ifndef CBM_TILE_THREADS
@@ -392,6 +430,13 @@ void tile_spmm(DeviceMatrix* h, uint32_t W, const float* x, int64_t ldx, uint32_
   if (units >= 0x7FFFFFFFull) throw invalid_argument("spmm: too many tile units");
   const size_t smem = tile_smem_bytes(h, W);
   const bool norm = h->info.normalized;
+  // dev tool: CBM_B200_TILE_TRACE=<file> appends (sm, start, staged, end) per unit
+  const char* trace_path = std::getenv("CBM_B200_TILE_TRACE");
+  p.trace = nullptr;
+  if (trace_path) {
+    ck(cudaMalloc(&p.trace, units * 32), "trace");
+    ck(cudaMemsetAsync(p.trace, 0, units * 32, s), "trace");
+  }
   if (W == 128) norm ? launch_tile<1, true>(p, uint32_t(units), smem, s)
                      : launch_tile<1, false>(p, uint32_t(units), smem, s);
   else if (W == 64) norm ? launch_tile<2, true>(p, uint32_t(units), smem, s)
@@ -399,6 +444,19 @@ void tile_spmm(DeviceMatrix* h, uint32_t W, const float* x, int64_t ldx, uint32_
   else norm ? launch_tile<4, true>(p, uint32_t(units), smem, s)
             : launch_tile<4, false>(p, uint32_t(units), smem, s);
   ck(cudaGetLastError(), "tile_kernel launch");
+  if (p.trace) {
+    std::vector<unsigned long long> t(units * 4);
+    ck(cudaStreamSynchronize(s), "trace");
+    ck(cudaMemcpy(t.data(), p.trace, units * 32, cudaMemcpyDeviceToHost), "trace");
+    cudaFree(p.trace);
+    if (FILE* f = std::fopen(trace_path, "a")) {
+      std::fprintf(f, "call units=%llu W=%u\n", (unsigned long long)units, W);
+      for (uint64_t u = 0; u < units; ++u)
+        std::fprintf(f, "%llu %llu %llu %llu %llu\n", (unsigned long long)u, t[4 * u], t[4 * u + 1],
+                     t[4 * u + 2], t[4 * u + 3]);
+      std::fclose(f);
+    }
+  }
 }
 
 }  // namespace cbmb

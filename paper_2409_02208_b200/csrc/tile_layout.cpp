@@ -11,38 +11,10 @@ namespace {
 constexpr uint32_t kVirt = 0xFFFFFFFFu;
 constexpr uint32_t kSign = 0x80000000u;
 
-// full row of x: the root's delta row (all +1), then every delta on the path
-// root -> x applied in turn (reconstruct_rows, builder.cpp:452-490)
-std::vector<uint32_t> full_row(const cbm_b200_cbm_view& v, uint32_t x) {
-  std::vector<uint32_t> path;
-  for (uint32_t y = x; y != kVirt; y = v.parent[y]) path.push_back(y);
-  std::vector<uint32_t> cur, nxt;
-  for (size_t i = path.size(); i-- > 0;) {
-    const uint32_t y = path[i];
-    nxt.clear();
-    uint64_t k = v.row_ptr[y];
-    const uint64_t ke = v.row_ptr[y + 1];
-    size_t a = 0;
-    while (a < cur.size() || k < ke) {  // (parent + plus) - minus, ascending
-      if (k == ke || (a < cur.size() && cur[a] < v.col_idx[k])) {
-        nxt.push_back(cur[a++]);
-      } else if (a == cur.size() || v.col_idx[k] < cur[a]) {
-        if (v.values[k] > 0.0f) nxt.push_back(v.col_idx[k]);
-        ++k;
-      } else {
-        if (v.values[k] > 0.0f) nxt.push_back(cur[a]);
-        ++a;
-        ++k;
-      }
-    }
-    cur.swap(nxt);
-  }
-  return cur;
-}
 }  // namespace
 
 TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t stage_cap,
-                      uint32_t num_sms) {
+                      uint32_t num_sms, uint32_t flatten_gain) {
   const uint32_t m = v.n_rows;
   const bool norm = v.is_normalized != 0;
   TileLayout T;
@@ -75,16 +47,33 @@ TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t st
   for (size_t h = 0; h < bfs.size(); ++h)
     for (uint32_t k = kp[bfs[h]]; k < kp[bfs[h] + 1]; ++k) bfs.push_back(kids[k]);
 
+  // rows whose delta row saves fewer than flatten_gain entries over their full
+  // row are summed directly (cut from their parent, as plan_layout does)
+  std::vector<uint8_t> cut(m, 0);
+  if (flatten_gain > 0) {
+    std::vector<uint64_t> nA(m, 0);
+    for (uint32_t x : bfs) {
+      uint64_t plus = 0, minus = 0;
+      for (uint64_t k = v.row_ptr[x]; k < v.row_ptr[x + 1]; ++k)
+        (v.values[k] < 0.0f ? minus : plus) += 1;
+      const uint32_t p = v.parent[x];
+      nA[x] = p == kVirt ? plus : nA[p] + plus - minus;
+      if (p != kVirt && nA[x] < plus + minus + flatten_gain) {
+        cut[x] = 1;
+        ++T.n_flat;
+      }
+    }
+  }
   // split trees bigger than rows_cap: children with the largest open subtrees
   // are cut off (each becomes the root of its own piece)
   std::vector<uint32_t> open(m, 1);
-  std::vector<uint8_t> cut(m, 0);
   std::vector<std::pair<uint32_t, uint32_t>> ch;
   for (size_t i = m; i-- > 0;) {
     const uint32_t x = bfs[i];
     uint64_t sz = 1;
     ch.clear();
     for (uint32_t k = kp[x]; k < kp[x + 1]; ++k) {
+      if (cut[kids[k]]) continue;
       sz += open[kids[k]];
       ch.emplace_back(open[kids[k]], kids[k]);
     }
@@ -153,11 +142,44 @@ TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t st
       if (interior) slot[x] = T.n_interior++;
     }
 
+  // full rows of the cut rows, parents first (reconstruct_rows, builder.cpp:452-490),
+  // materialised only along the paths that lead to a cut row
+  std::vector<uint8_t> need(cut.begin(), cut.end());
+  for (size_t i = m; i-- > 0;) {
+    const uint32_t x = bfs[i];
+    if (need[x] && v.parent[x] != kVirt) need[v.parent[x]] = 1;
+  }
+  std::vector<std::vector<uint32_t>> full(m);
+  for (uint32_t x : bfs) {
+    if (!need[x]) continue;
+    const uint32_t p = v.parent[x];
+    static const std::vector<uint32_t> kEmpty;
+    const std::vector<uint32_t>& base = p == kVirt ? kEmpty : full[p];
+    std::vector<uint32_t>& out = full[x];
+    uint64_t k = v.row_ptr[x];
+    const uint64_t ke = v.row_ptr[x + 1];
+    size_t a = 0;
+    while (a < base.size() || k < ke) {  // (parent + plus) - minus, ascending
+      if (k == ke || (a < base.size() && base[a] < v.col_idx[k])) {
+        out.push_back(base[a++]);
+      } else if (a == base.size() || v.col_idx[k] < base[a]) {
+        if (v.values[k] > 0.0f) out.push_back(v.col_idx[k]);
+        ++k;
+      } else {
+        if (v.values[k] > 0.0f) out.push_back(base[a]);
+        ++a;
+        ++k;
+      }
+    }
+  }
+  for (uint32_t x = 0; x < m; ++x)
+    if (!cut[x]) std::vector<uint32_t>().swap(full[x]);  // keep the cut rows only
+
   // effective delta rows: the CBM's (column | sign), or the full row for cut rows
   auto row_entries = [&](uint32_t x, std::vector<uint32_t>& out) {
     out.clear();
     if (cut[x]) {
-      for (uint32_t c : full_row(v, x)) out.push_back(c);
+      out.assign(full[x].begin(), full[x].end());
     } else {
       for (uint64_t k = v.row_ptr[x]; k < v.row_ptr[x + 1]; ++k)
         out.push_back(v.col_idx[k] | (v.values[k] < 0.0f ? kSign : 0u));
@@ -171,7 +193,7 @@ TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t st
   for (uint32_t b = 0; b < nb; ++b)
     for (uint32_t i = bptr[b]; i < bptr[b + 1]; ++i) {
       const uint32_t x = brows[i];
-      work[b] += 8 + (cut[x] ? 64 : v.row_ptr[x + 1] - v.row_ptr[x]);
+      work[b] += 8 + (cut[x] ? full[x].size() : v.row_ptr[x + 1] - v.row_ptr[x]);
     }
   std::stable_sort(order.begin(), order.end(),
                    [&](uint32_t a, uint32_t c) { return work[a] > work[c]; });

@@ -33,7 +33,7 @@ inline constexpr double kTileMinStagedFrac = 0.6;
 inline constexpr double kTileMinReuse = 8.0;
 
 struct TileLayout {
-  uint32_t n_blocks = 0, max_rows = 0, max_staged = 0, n_interior = 0, n_cut = 0;
+  uint32_t n_blocks = 0, max_rows = 0, max_staged = 0, n_interior = 0, n_cut = 0, n_flat = 0;
   uint32_t row_cap = 0, stage_cap = 0;
   uint64_t n_deltas = 0, n_staged_deltas = 0, n_staged_cols = 0, n_entries = 0;
   // per block: row0, nrows, st0, nst (tile rows [row0, row0+nrows), staged
@@ -51,8 +51,9 @@ struct TileLayout {
 };
 
 // rows_cap: rows per block (0 = auto); stage_cap: staged columns per block
-// (0 = auto, 640). The view must already be validated (plan_layout).
+// (0 = auto, 640); flatten_gain: as plan_layout (rows saving fewer entries are
+// summed from their full row). The view must already be validated (plan_layout).
 TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t stage_cap,
-                      uint32_t num_sms);
+                      uint32_t num_sms, uint32_t flatten_gain);
 
 }  // namespace cbmb
