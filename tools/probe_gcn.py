@@ -45,8 +45,8 @@ def main():
         h2 = op.spmm(h1)
         t_g1 = ev_time(lambda: P.dense_matmul(h2, w1))
         t_all = ev_time(lambda: op.gcn_forward(x, w0, w1))
-        gf0 = 2 * n * f * hid / t_g0 / 1e6
-        gf1 = 2 * n * hid * classes / t_g1 / 1e6
+        gf0 = 2 * n * f * hid / t_g0 / 1e3
+        gf1 = 2 * n * hid * classes / t_g1 / 1e3
         print(f"{name} faithful={faithful}: X.W0 {t_g0:8.1f} us ({gf0 / 1e3:.1f} TFLOP/s)  "
               f"relu(A.) {t_s1:8.1f} us  A. {t_s2:8.1f} us  .W1 {t_g1:8.1f} us ({gf1 / 1e3:.1f} TFLOP/s)  "
               f"gcn_forward {t_all:8.1f} us", flush=True)
