@@ -144,7 +144,7 @@ typedef struct cbm_b200_options {
                                 (used when most deltas hit staged rows and each
                                 staged row is re-used enough), 0 off, 1 force */
   uint32_t tile_rows;        /* rows per tile block (0 = auto, 64..512) */
-  uint32_t tile_stage;       /* staged X rows per block (0 = auto, 640) */
+  uint32_t tile_stage;       /* staged X rows per block (0 = auto, 600) */
   int32_t tile_vec;          /* floats per lane of a tile slab: 0 auto, 1, 2, 4 */
 } cbm_b200_options;
 

@@ -29,7 +29,7 @@ namespace {
 constexpr uint32_t kLocalMask = 0x7FFFFFFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 #ifndef CBM_TILE_IDXCAP
-#define CBM_TILE_IDXCAP 256
+#define CBM_TILE_IDXCAP 224
 #endif
 constexpr uint32_t kIdxCap = CBM_TILE_IDXCAP;  // row indices per buffer (two per warp)
 
@@ -115,6 +115,9 @@ __device__ __forceinline__ void load_idx(const uint32_t* q, uint32_t (&e)[D]) {
 
 // acc +-= the staged rows of entries [k0, k1) (a multiple of 8 long): 16
 // entries per step (two index vectors, 2*D tile reads in flight per lane)
+#ifndef CBM_TILE_STEP
+#define CBM_TILE_STEP 8
+#endif
 template <int H, bool SMEM, bool NEG>
 __device__ __forceinline__ void staged_run(const uint32_t* ix, uint32_t k0, uint32_t k1,
                                            const float* xl, uint32_t g, float4& acc) {
@@ -122,7 +125,7 @@ __device__ __forceinline__ void staged_run(const uint32_t* ix, uint32_t k0, uint
   constexpr uint32_t kW = 128u / H;
   uint32_t k = k0;
 #pragma unroll 1
-  for (; k + 16 <= k1; k += 16) {
+  for (; CBM_TILE_STEP == 16 && k + 16 <= k1; k += 16) {
     uint32_t e[D], f[D];
     load_idx<D, SMEM>(ix + k + g * D, e);
     load_idx<D, SMEM>(ix + k + 8 + g * D, f);
@@ -134,7 +137,8 @@ __device__ __forceinline__ void staged_run(const uint32_t* ix, uint32_t k0, uint
 #pragma unroll
     for (int q = 0; q < 2 * D; ++q) acc = NEG ? f4sub(acc, v[q]) : f4add(acc, v[q]);
   }
-  if (k < k1) {
+#pragma unroll 1
+  for (; k < k1; k += 8) {
     uint32_t e[D];
     load_idx<D, SMEM>(ix + k + g * D, e);
     float4 v[D];
@@ -154,7 +158,10 @@ __device__ __forceinline__ float4 row_sum(const TileParams& p, const uint32_t* i
                                           const float* xl, uint32_t g, bool act, long long col) {
   constexpr int D = 8 / H;
   constexpr uint32_t kW = 128u / H;  // floats per slab
-  constexpr int CPG = 8;             // cold deltas per group per batch
+#ifndef CBM_TILE_CPG
+#define CBM_TILE_CPG 4
+#endif
+  constexpr int CPG = CBM_TILE_CPG;  // cold deltas per group per batch
   const int lane = threadIdx.x & 31;
   // first batch of cold deltas: group g takes entries g, g+H, ... (loads in
   // flight during the staged loop)
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) tile_kernel(const Til
 }
 
 #ifndef CBM_TILE_THREADS
-#define CBM_TILE_THREADS 512
+#define CBM_TILE_THREADS 768
 #endif
 
 template <int H, bool NORM>

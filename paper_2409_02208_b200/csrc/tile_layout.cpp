@@ -24,7 +24,7 @@ TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t st
     rows_cap = 64;
     while (rows_cap < 512 && rows_cap < want) rows_cap *= 2;
   }
-  if (stage_cap == 0) stage_cap = 640;
+  if (stage_cap == 0) stage_cap = 600;
   rows_cap = std::max<uint32_t>(rows_cap, 1);
   T.row_cap = rows_cap;
   T.stage_cap = stage_cap;

@@ -51,7 +51,7 @@ struct TileLayout {
 };
 
 // rows_cap: rows per block (0 = auto); stage_cap: staged columns per block
-// (0 = auto, 640); flatten_gain: as plan_layout (rows saving fewer entries are
+// (0 = auto, 600); flatten_gain: as plan_layout (rows saving fewer entries are
 // summed from their full row). The view must already be validated (plan_layout).
 TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t stage_cap,
                       uint32_t num_sms, uint32_t flatten_gain);
