@@ -209,6 +209,28 @@ int cbm_b200_spmv(cbm_b200_matrix* h, const float* v, int64_t v_rows, int64_t v_
 int cbm_b200_dense_matmul(const float* a, int64_t m, int64_t k, const float* b, int64_t n,
                           float* c, void* stream);
 
+/* Fused all-gather + GEMM of the multi-GPU GCN: C = [A_0 | A_1 |
+ * ... | A_{P-1}] B, where A_p is m x part_k[p] row-major (leading dimension
+ * part_k[p]) and may be ANOTHER device's buffer mapped with cbm_b200_ipc_open,
+ * so the tiles of the all-gathered operand are read over NVLink inside the
+ * GEMM; C (m x n, leading dimension ldc) is written to every outs[o] (peer
+ * buffers too), which fuses the result's gather. 1..8 parts and outputs.
+ * ordered = 1: the reference's dense_matmul arithmetic over the concatenated
+ * A (ascending k, zero lhs skipped, no FMA: bit-identical); 0: FFMA (part
+ * widths multiples of 4). B is sum(part_k) x n packed. Async on `stream`. */
+int cbm_b200_gemm_parts(const float* const* a_parts, const int64_t* part_k, int32_t n_parts,
+                        int64_t m, const float* b, int64_t n, float* const* outs, int32_t n_outs,
+                        int64_t ldc, int32_t ordered, void* stream);
+
+/* CUDA IPC between the ranks of one node: export the allocation holding dptr
+ * as a 64-byte handle plus dptr's byte offset inside it, map a peer's handle
+ * (device = the caller's GPU, -1 = current; add the offset to the returned
+ * base), unmap. A process cannot map its own handle. */
+#define CBM_B200_IPC_HANDLE_BYTES 64
+int cbm_b200_ipc_handle(const void* dptr, unsigned char* handle64, uint64_t* offset);
+int cbm_b200_ipc_open(const unsigned char* handle64, int32_t device, void** dptr);
+int cbm_b200_ipc_close(void* dptr);
+
 /* Two-layer GCN inference out = A_hat relu(A_hat (X W0)) W1 (gcn_forward,
  * gcn.hpp:27-29, gcn.cpp:22-33) with a normalized uploaded adjacency: the two
  * GEMMs above, the ReLU fused into the first CBM product's epilogue. X is

@@ -32,7 +32,7 @@ __all__ = [
     "CsrBinaryMatrix", "CbmMatrix", "DeviceCbm", "build_cbm", "build_cbm_normalized",
     "count_scalar_ops", "generate_graph", "generate_dense", "CbmError", "FormatError",
     "load_cbm", "save_cbm", "dense_matmul", "csr_operator", "VIRTUAL_PARENT",
-    "library_path",
+    "library_path", "gemm_parts", "ipc_handle", "ipc_open", "ipc_close",
 ]
 
 VIRTUAL_PARENT = 0xFFFFFFFF
@@ -129,6 +129,11 @@ _sig = {
     "cbm_b200_get_info": (C.c_int, [_vp, C.POINTER(_Info)]),
     "cbm_b200_dense_matmul": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp]),
     "cbm_b200_gcn_forward": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "cbm_b200_gemm_parts": (C.c_int, [C.POINTER(_vp), C.POINTER(_i64), _i32, _i64, _vp, _i64,
+                                      C.POINTER(_vp), _i32, _i64, _i32, _vp]),
+    "cbm_b200_ipc_handle": (C.c_int, [_vp, C.c_char_p, C.POINTER(_u64)]),
+    "cbm_b200_ipc_open": (C.c_int, [C.c_char_p, _i32, C.POINTER(_vp)]),
+    "cbm_b200_ipc_close": (C.c_int, [_vp]),
     "cbm_b200_gen_graph": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), _i32, _u64,
                                      C.POINTER(_vp)]),
     "cbm_b200_csr_get": (C.c_int, [_vp, C.POINTER(_CsrView)]),
@@ -402,6 +407,50 @@ def dense_matmul(a, b, stream=None):
     _check(_lib.cbm_b200_dense_matmul(a.data_ptr(), a.shape[0], a.shape[1], b.data_ptr(),
                                       b.shape[1], c.data_ptr(), s))
     return c
+
+
+def _ptr(t):
+    return t if isinstance(t, int) else t.data_ptr()
+
+
+def gemm_parts(parts, part_k, m, b, outs, ldc, ordered=True, stream=None):
+    """C = [A_0 | ... | A_{P-1}] . B written to every buffer of `outs`
+    (cbm_b200_gemm_parts: the fused all-gather + GEMM of the multi-GPU GCN).
+    `parts` / `outs` are CUDA tensors or raw device pointers (e.g. peer
+    buffers from ipc_open); A_p is m x part_k[p] row-major, B is a CUDA
+    tensor sum(part_k) x n, C has leading dimension ldc (floats)."""
+    b = b.contiguous()
+    n = b.shape[1]
+    if b.shape[0] != sum(part_k):
+        raise ValueError("dense_matmul: inner dimensions differ")
+    pa = (_vp * len(parts))(*[_ptr(t) for t in parts])
+    pk = (_i64 * len(part_k))(*[int(k) for k in part_k])
+    po = (_vp * len(outs))(*[_ptr(t) for t in outs])
+    _check(_lib.cbm_b200_gemm_parts(pa, pk, len(parts), m, b.data_ptr(), n, po, len(outs), ldc,
+                                    int(ordered), DeviceCbm._stream(stream)))
+
+
+def ipc_handle(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding CUDA tensor `t`,
+    byte offset of `t` inside that allocation)."""
+    buf = C.create_string_buffer(64)
+    off = _u64()
+    _check(_lib.cbm_b200_ipc_handle(_ptr(t), buf, C.byref(off)))
+    return buf.raw, int(off.value)
+
+
+def ipc_open(handle, device: int = -1) -> int:
+    """Map a peer's buffer from ipc_handle's (handle, offset); returns the
+    device pointer of the peer's tensor (base + offset). Unmap the base with
+    ipc_close(ptr - offset)."""
+    raw, off = handle
+    p = _vp()
+    _check(_lib.cbm_b200_ipc_open(C.create_string_buffer(raw, 64), device, C.byref(p)))
+    return int(p.value) + int(off)
+
+
+def ipc_close(base_ptr: int):
+    _check(_lib.cbm_b200_ipc_close(base_ptr))
 
 
 # ---------------------------------------------------------------------------

@@ -365,6 +365,52 @@ int cbm_b200_dense_matmul(const float* a, int64_t m, int64_t k, const float* b, 
   });
 }
 
+int cbm_b200_gemm_parts(const float* const* a_parts, const int64_t* part_k, int32_t n_parts,
+                        int64_t m, const float* b, int64_t n, float* const* outs, int32_t n_outs,
+                        int64_t ldc, int32_t ordered, void* stream) {
+  return guard([&] {
+    need(a_parts && part_k && outs && n_parts >= 1 && n_parts <= int32_t(cbmb::kMaxParts) &&
+             n_outs >= 1 && n_outs <= int32_t(cbmb::kMaxParts),
+         "gemm_parts: 1..8 parts and outputs");
+    need(m >= 0 && n >= 0 && ldc >= n && m < (int64_t(1) << 31) && n < (int64_t(1) << 31),
+         "gemm_parts: bad shape");
+    uint32_t pk[cbmb::kMaxParts];
+    int64_t k = 0;
+    for (int32_t p = 0; p < n_parts; ++p) {
+      need(part_k[p] >= 0 && (a_parts[p] || part_k[p] * m == 0), "gemm_parts: bad part");
+      if (!ordered) need(part_k[p] % 4 == 0 || p == n_parts - 1,
+                         "gemm_parts: part widths must be multiples of 4 (column_slab)");
+      pk[p] = uint32_t(part_k[p]);
+      k += part_k[p];
+    }
+    need(k < (int64_t(1) << 31) && (b || k * n == 0), "gemm_parts: bad shape");
+    for (int32_t o = 0; o < n_outs; ++o) need(outs[o] || m * n == 0, "gemm_parts: null output");
+    cbmb::device_gemm_parts(a_parts, pk, uint32_t(n_parts), uint32_t(m), b, uint32_t(n), outs,
+                            uint32_t(n_outs), uint32_t(ldc), ordered != 0, stream);
+  });
+}
+
+int cbm_b200_ipc_handle(const void* dptr, unsigned char* handle64, uint64_t* offset) {
+  return guard([&] {
+    need(dptr && handle64 && offset, "ipc: null argument");
+    cbmb::ipc_handle(dptr, handle64, offset);
+  });
+}
+
+int cbm_b200_ipc_open(const unsigned char* handle64, int32_t device, void** dptr) {
+  return guard([&] {
+    need(handle64 && dptr, "ipc: null argument");
+    *dptr = cbmb::ipc_open(handle64, device);
+  });
+}
+
+int cbm_b200_ipc_close(void* dptr) {
+  return guard([&] {
+    need(dptr != nullptr, "ipc: null argument");
+    cbmb::ipc_close(dptr);
+  });
+}
+
 int cbm_b200_gcn_forward(cbm_b200_matrix* h, const float* x, int64_t n, int64_t f,
                          const float* w0, int64_t hid, const float* w1, int64_t classes,
                          float* out, void* stream) {

@@ -84,6 +84,17 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
                  int64_t ldy, void* stream, bool relu = false);
 void device_dense_matmul(const float* a, uint32_t m, uint32_t k, const float* b, uint32_t n,
                          float* c, void* stream);
+void device_fast_matmul(const float* a, uint32_t m, uint32_t k, const float* b, uint32_t n,
+                        float* c, void* stream);
+// C = [A_0 | ... | A_{P-1}] B written to every outs[o] (leading dimension ldc);
+// A_p is m x part_k[p] row-major and may live on another device (CUDA IPC).
+inline constexpr uint32_t kMaxParts = 8;
+void device_gemm_parts(const float* const* a_parts, const uint32_t* part_k, uint32_t n_parts,
+                       uint32_t m, const float* b, uint32_t n, float* const* outs,
+                       uint32_t n_outs, uint32_t ldc, bool ordered, void* stream);
+void ipc_handle(const void* dptr, unsigned char* out64, uint64_t* offset);
+void* ipc_open(const unsigned char* in64, int device);
+void ipc_close(void* dptr);
 void device_gcn_forward(DeviceMatrix* h, const float* x, uint32_t n, uint32_t f,
                         const float* w0, uint32_t hid, const float* w1, uint32_t classes,
                         float* out, void* stream);

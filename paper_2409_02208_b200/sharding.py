@@ -25,6 +25,11 @@ def all_slabs(d: int, world: int) -> list[tuple[int, int]]:
     return [column_slab(d, world, r) for r in range(world)]
 
 
+def row_block(n: int, world: int, rank: int) -> tuple[int, int]:
+    """[r0, r1) rows of `rank` for the fused gather-GEMM (balanced, contiguous)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
 class _DeviceCompute:
     """The product's compute for one rank: the reference-exact GEMM and the
     CBM multiply (ReLU fused into the epilogue) on this rank's GPU."""
@@ -38,6 +43,49 @@ class _DeviceCompute:
 
     def spmm(self, x, relu=False):
         return self.op.spmm(x.contiguous(), relu=relu)
+
+    def gather_gemm(self, z, hslabs, w1, rank, group, ordered):
+        """out = [Z_0 | ... | Z_{N-1}] . W1 on every rank, fused: rank r's GEMM
+        reads the rows [r0, r1) of every peer's Z slab over NVLink (CUDA IPC)
+        and writes its output rows into every rank's output buffer
+        (cbm_b200_gemm_parts). No staging copy of the gathered Z exists."""
+        import torch
+        import torch.distributed as dist
+        from . import gemm_parts, ipc_close, ipc_handle, ipc_open
+        world = len(hslabs)
+        n, classes = z.shape[0], w1.shape[1]
+        z = z.contiguous()
+        out = torch.empty((n, classes), dtype=torch.float32, device=z.device)
+        widths = [hi - lo for lo, hi in hslabs]
+        if world == 1:
+            gemm_parts([z], widths, n, w1, [out], classes, ordered)
+            return out
+        torch.cuda.synchronize(z.device)  # Z complete before peers read it
+        mine = (ipc_handle(z), ipc_handle(out))
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        dev = z.device.index
+        maps = []  # (peer base pointer to unmap)
+        zp, op = [], []
+        for s_, (hz, ho) in enumerate(handles):
+            if s_ == rank:
+                zp.append(z.data_ptr())
+                op.append(out.data_ptr())
+                continue
+            pz, po = ipc_open(hz, dev), ipc_open(ho, dev)
+            maps += [pz - hz[1], po - ho[1]]
+            zp.append(pz)
+            op.append(po)
+        r0, r1 = row_block(n, world, rank)
+        parts = [p + r0 * w * 4 for p, w in zip(zp, widths)]
+        outs = [p + r0 * classes * 4 for p in op]
+        dist.barrier(group=group)  # every rank has mapped every buffer
+        gemm_parts(parts, widths, r1 - r0, w1, outs, classes, ordered)
+        torch.cuda.synchronize(z.device)
+        dist.barrier(group=group)  # every rank's rows have landed in `out`
+        for p in maps:
+            ipc_close(p)
+        return out
 
 
 def _gather_columns(local, slabs, rank, group):
@@ -56,7 +104,7 @@ def _gather_columns(local, slabs, rank, group):
     return full
 
 
-def gcn_forward_sharded(op, x, w0, w1, group=None, compute=None):
+def gcn_forward_sharded(op, x, w0, w1, group=None, compute=None, fused=False):
     """gcn_forward (gcn.cpp:22-33) over the ranks of `group`, bit-identical to
     one GPU.
 
@@ -69,6 +117,12 @@ def gcn_forward_sharded(op, x, w0, w1, group=None, compute=None):
     Z . W1[:, cslab] in the reference's ascending order and a small second
     all-gather assembles the n x classes output on every rank. `x`, `w0`,
     `w1` are replicated on every rank (torch tensors on the rank's device).
+
+    fused=True replaces both all-gathers and the last GEMM with one kernel per
+    rank (compute.gather_gemm): rank r computes the output rows
+    row_block(n, world, r) reading every peer's Z slab in place over NVLink and
+    storing its rows into every rank's output; the ascending-k order over the
+    concatenated slabs is the reference's, so the result is the same bits.
     """
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -82,6 +136,9 @@ def gcn_forward_sharded(op, x, w0, w1, group=None, compute=None):
     t = cm.matmul(x, w0[:, lo:hi].contiguous())
     h = cm.spmm(t, relu=True)
     z = cm.spmm(h)
+    if fused:
+        ordered = bool(op.info()["order_faithful"]) if op is not None else True
+        return cm.gather_gemm(z, hslabs, w1, rank, group, ordered)
     z_full = _gather_columns(z, hslabs, rank, group)
     cslabs = all_slabs(classes, world)
     clo, chi = cslabs[rank]

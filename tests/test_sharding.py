@@ -96,6 +96,22 @@ class _OracleCompute:
     def matmul(self, a, b):
         return torch.from_numpy(O.oracle_dense_matmul(a.numpy(), b.contiguous().numpy()))
 
+    def gather_gemm(self, z, hslabs, w1, rank, group, ordered):
+        """CPU stand-in for the fused peer-memory gather-GEMM: the peers' Z
+        slabs are fetched with a gloo all-gather (the device reads them in
+        place over NVLink), rank r computes its row block, the blocks are
+        gathered back (the device stores them into every rank's output)."""
+        from paper_2409_02208_b200.sharding import row_block
+        world = len(hslabs)
+        slabs = [None] * world
+        dist.all_gather_object(slabs, z.numpy(), group=group)
+        r0, r1 = row_block(z.shape[0], world, rank)
+        zr = np.ascontiguousarray(np.concatenate([sl[r0:r1] for sl in slabs], axis=1))
+        mine = O.oracle_dense_matmul(zr, w1.contiguous().numpy())
+        blocks = [None] * world
+        dist.all_gather_object(blocks, mine, group=group)
+        return torch.from_numpy(np.ascontiguousarray(np.concatenate(blocks, axis=0)))
+
     def spmm(self, x, relu=False):
         y = O.oracle_spmm(self.arrays, np.ascontiguousarray(x.numpy()))
         if relu:
@@ -112,25 +128,29 @@ def _gcn_inputs():
     return c, x, w0, w1
 
 
-def _gcn_worker(rank, world, port, out):
+def _gcn_worker(rank, world, port, out, fused=False):
     from paper_2409_02208_b200.sharding import gcn_forward_sharded
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     c, x, w0, w1 = _gcn_inputs()
     got = gcn_forward_sharded(None, torch.from_numpy(x), torch.from_numpy(w0),
-                              torch.from_numpy(w1), compute=_OracleCompute(oracle_arrays(c)))
+                              torch.from_numpy(w1), compute=_OracleCompute(oracle_arrays(c)),
+                              fused=fused)
     out.put((rank, got.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_gloo_world2_sharded_gcn_bitwise():
+@pytest.mark.parametrize("fused", [False, True])
+def test_gloo_world2_sharded_gcn_bitwise(fused):
     """Hidden-column shards + all-gather (gcn_forward_sharded) on 2 gloo ranks:
-    both ranks hold the single-device gcn_forward output bit for bit."""
+    both ranks hold the single-device gcn_forward output bit for bit. fused:
+    the row-block gather-GEMM partition (rank r's rows over the concatenated
+    slabs, ascending k) instead of two all-gathers."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gcn_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gcn_worker, args=(r, 2, port, q, fused)) for r in range(2)]
     for p_ in procs:
         p_.start()
     results = dict(q.get(timeout=240) for _ in range(2))
