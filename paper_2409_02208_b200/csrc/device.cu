@@ -72,7 +72,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       T.dval = {};
       T.row = {};
       T.block = {};
-      T.stage = {};
+      T.stage = {};  // (T.work stays: it sizes the split of the last wave)
       h->tile = std::move(T);
     }
     int coop = 0;

@@ -40,6 +40,7 @@ struct DeviceMatrix {
   uint32_t* trow = nullptr;
   uint32_t* tblock = nullptr;
   uint32_t* tstage = nullptr;
+  std::map<uint64_t, uint32_t> tile_main;  // (W, slabs) -> full-width units of the launch
   // per-call workspace, one per stream (concurrent calls on distinct streams
   // never share flags or scratch); grown on demand, or by cbm_b200_reserve
   struct Workspace {

@@ -21,14 +21,21 @@ struct Parts {
   uint32_t ldc;
 };
 
+template <bool MULTI>
 __device__ __forceinline__ float load_a(const Parts& P, uint32_t row, uint32_t kk) {
+  if constexpr (!MULTI) return __ldg(P.a[0] + (size_t)row * P.koff[1] + kk);
   uint32_t p = 0;
   while (p + 1 < P.n_parts && kk >= P.koff[p + 1]) ++p;
   const uint32_t kp = P.koff[p + 1] - P.koff[p];
   return P.a[p][(size_t)row * kp + (kk - P.koff[p])];
 }
 
+template <bool MULTI>
 __device__ __forceinline__ void store_c(const Parts& P, uint32_t i, uint32_t cc, float v) {
+  if constexpr (!MULTI) {
+    P.out[0][(size_t)i * P.ldc + cc] = v;
+    return;
+  }
   for (uint32_t o = 0; o < P.n_out; ++o) P.out[o][(size_t)i * P.ldc + cc] = v;
 }
 
@@ -38,6 +45,7 @@ __device__ __forceinline__ void store_c(const Parts& P, uint32_t i, uint32_t cc,
 // 32-row x 128-column tile; b is staged through shared memory 32 rows of j at
 // a time; the zero test is warp-uniform (a warp shares its row).
 constexpr int kGemmRows = 32, kGemmCols = 128, kGemmK = 32;
+template <bool MULTI>
 __global__ void __launch_bounds__(256) ordered_gemm_kernel(const Parts P,
                                                            const float* __restrict__ b,
                                                            uint32_t m, uint32_t k, uint32_t n) {
@@ -58,7 +66,7 @@ __global__ void __launch_bounds__(256) ordered_gemm_kernel(const Parts P,
     }
     for (uint32_t e = threadIdx.x; e < kGemmRows * kGemmK; e += 256) {
       const uint32_t rr = e / kGemmK, jj = e % kGemmK;
-      as[rr][jj] = (row0 + rr < m && j0 + jj < k) ? load_a(P, row0 + rr, j0 + jj) : 0.0f;
+      as[rr][jj] = (row0 + rr < m && j0 + jj < k) ? load_a<MULTI>(P, row0 + rr, j0 + jj) : 0.0f;
     }
     __syncthreads();
     const uint32_t jn = min(uint32_t(kGemmK), k - j0);
@@ -83,7 +91,7 @@ __global__ void __launch_bounds__(256) ordered_gemm_kernel(const Parts P,
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint32_t cc = col0 + tx + 32 * q;
-      if (cc < n) store_c(P, i, cc, acc[r][q]);
+      if (cc < n) store_c<MULTI>(P, i, cc, acc[r][q]);
     }
   }
 }
@@ -94,6 +102,7 @@ __global__ void __launch_bounds__(256) ordered_gemm_kernel(const Parts P,
 // contributes fma(0, b, acc) = acc like dense.cpp:42's skip. Part widths are
 // multiples of 4 (column_slab), so a 4-wide k group never straddles two parts.
 constexpr int kFB = 128, kFK = 8;
+template <bool MULTI>
 __global__ void __launch_bounds__(256, 2) fast_gemm_kernel(const Parts P,
                                                            const float* __restrict__ b,
                                                            uint32_t m, uint32_t k, uint32_t n) {
@@ -113,7 +122,7 @@ __global__ void __launch_bounds__(256, 2) fast_gemm_kernel(const Parts P,
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint32_t kk = k0 + ak + i;
-      av[i] = (row0 + ar < m && kk < k) ? load_a(P, row0 + ar, kk) : 0.0f;
+      av[i] = (row0 + ar < m && kk < k) ? load_a<MULTI>(P, row0 + ar, kk) : 0.0f;
       const uint32_t cc = col0 + bc + i;
       bv[i] = (k0 + bk < k && cc < n) ? __ldg(b + (size_t)(k0 + bk) * n + cc) : 0.0f;
     }
@@ -143,7 +152,7 @@ __global__ void __launch_bounds__(256, 2) fast_gemm_kernel(const Parts P,
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const uint32_t cc = col0 + (q < 4 ? tx * 4 + q : 64 + tx * 4 + q - 4);
-      if (cc < n) store_c(P, i, cc, acc[r][q]);
+      if (cc < n) store_c<MULTI>(P, i, cc, acc[r][q]);
     }
   }
 }
@@ -163,12 +172,15 @@ Parts one_part(const float* a, uint32_t k, float* c, uint32_t n) {
 void launch_gemm(const Parts& P, uint32_t m, uint32_t k, const float* b, uint32_t n,
                  bool ordered, cudaStream_t s) {
   if (m == 0 || n == 0) return;
+  const bool multi = P.n_parts > 1 || P.n_out > 1;
   if (ordered) {
     const dim3 grid((n + kGemmCols - 1) / kGemmCols, (m + kGemmRows - 1) / kGemmRows);
-    ordered_gemm_kernel<<<grid, 256, 0, s>>>(P, b, m, k, n);
+    if (multi) ordered_gemm_kernel<true><<<grid, 256, 0, s>>>(P, b, m, k, n);
+    else ordered_gemm_kernel<false><<<grid, 256, 0, s>>>(P, b, m, k, n);
   } else {
     const dim3 grid((n + kFB - 1) / kFB, (m + kFB - 1) / kFB);
-    fast_gemm_kernel<<<grid, 256, 0, s>>>(P, b, m, k, n);
+    if (multi) fast_gemm_kernel<true><<<grid, 256, 0, s>>>(P, b, m, k, n);
+    else fast_gemm_kernel<false><<<grid, 256, 0, s>>>(P, b, m, k, n);
   }
   ck(cudaGetLastError(), "gemm launch");
 }

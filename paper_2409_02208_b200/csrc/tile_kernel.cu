@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <queue>
 #include <vector>
 
 #include "cuda_common.hpp"
@@ -47,6 +48,7 @@ struct TileParams {
   float* interior;  // unscaled rows with children, stride dpad
   uint32_t dpad, d, n_slabs, relu;
   uint32_t max_staged, max_rows;
+  uint32_t n_main;            // full-width units; the rest are split in two
   unsigned long long* trace;  // dev tool (CBM_B200_TILE_TRACE): 4 x u64 per unit, else null
 };
 
@@ -219,14 +221,13 @@ __device__ __forceinline__ float4 row_sum(const TileParams& p, const uint32_t* i
   return acc;
 }
 
+// One (row block, column slab) unit: slab columns [col0, col0 + 128/H).
 template <int H, bool NORM, int NT>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) tile_kernel(const TileParams p) {
+__device__ __forceinline__ void tile_unit(const TileParams& p, uint32_t blk, uint32_t col0,
+                                          unsigned char* smem, uint32_t unit) {
   constexpr uint32_t LG = 32u / H;  // lanes per group
   constexpr uint32_t kW = 4u * LG;  // floats per slab
   constexpr int kWarps = NT / 32;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const uint32_t unit = blockIdx.x;
-  const uint32_t blk = unit / p.n_slabs, slab = unit - blk * p.n_slabs;
   const uint4 B = p.blocks[blk];
   const uint32_t row0 = B.x, nrows = B.y, st0 = B.z, nst = B.w;
   float* xs = reinterpret_cast<float*>(smem);
@@ -236,7 +237,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) tile_kernel(const Til
   uint32_t* idxbuf = counter + 4 + ((p.max_rows & 3u) ? 4u - (p.max_rows & 3u) : 0u);
   float* ssc = reinterpret_cast<float*>(idxbuf + kWarps * 2 * kIdxCap);  // staged scales
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t col0 = slab * kW;
   const unsigned long long t0 = p.trace ? gtimer() : 0ull;
 
   // ---- stage: row records, flags, the staged X rows (+ a zero row at nst)
@@ -364,6 +364,26 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) tile_kernel(const Til
   }
 }
 
+// Units [0, n_main) are (block, slab of 128/H columns), block-major. The
+// remaining (block, slab) pairs of that order are each split into two units of
+// half the width, so the last wave is made of smaller pieces (tile_spmm picks
+// n_main by simulating the dispatch).
+template <int H, bool NORM, int NT>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) tile_kernel(const TileParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t u = blockIdx.x;
+  if constexpr (H < 4) {
+    if (u >= p.n_main) {
+      const uint32_t v = u - p.n_main, w = p.n_main + v / 2;
+      const uint32_t blk = w / p.n_slabs, slab = w - blk * p.n_slabs;
+      tile_unit<2 * H, NORM, NT>(p, blk, slab * (128u / H) + (v & 1u) * (64u / H), smem, u);
+      return;
+    }
+  }
+  const uint32_t blk = u / p.n_slabs, slab = u - blk * p.n_slabs;
+  tile_unit<H, NORM, NT>(p, blk, slab * (128u / H), smem, u);
+}
+
 #ifndef CBM_TILE_THREADS
 #define CBM_TILE_THREADS 768
 #endif
@@ -411,6 +431,54 @@ uint32_t tile_pick_vec(const DeviceMatrix* h, uint32_t d, const float* x, int64_
   return best;
 }
 
+// Full-width units of a launch (tile_kernel): the last (block, slab) pairs are
+// split into two half-width units when that shortens the last wave. The CTA
+// dispatch (one CTA per SM: 24 warps x ~80 registers) is simulated on the
+// blocks' work estimates; a half unit is costed at 0.62 of a full one.
+uint32_t tile_pick_main(DeviceMatrix* h, uint32_t W, uint32_t n_slabs) {
+  const uint64_t key = (uint64_t(W) << 32) | n_slabs;
+  auto it = h->tile_main.find(key);
+  if (it != h->tile_main.end()) return it->second;
+  const auto& wk = h->tile.work;
+  const uint64_t T = uint64_t(wk.size()) * n_slabs;
+  const uint32_t S = uint32_t(std::max(1, h->num_sms));
+  uint64_t best_x = 0;
+  double best = -1.0;
+  if (W > 32 && !std::getenv("CBM_B200_TILE_NOSPLIT")) {
+    const uint64_t cand[] = {0, S / 4, S / 2, S * 3 / 4, S, S * 3 / 2, uint64_t(S) * 2,
+                             uint64_t(S) * 3};
+    for (uint64_t x : cand) {
+      if (x > T) continue;
+      std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+      for (uint32_t i = 0; i < S; ++i) q.push(0.0);
+      auto put = [&](double w) {
+        const double t0 = q.top();
+        q.pop();
+        q.push(t0 + w);
+      };
+      for (uint64_t u = 0; u < T - x; ++u) put(double(wk[u / n_slabs]));
+      for (uint64_t u = T - x; u < T; ++u) {
+        put(0.62 * wk[u / n_slabs]);
+        put(0.62 * wk[u / n_slabs]);
+      }
+      double mk = 0.0;
+      while (!q.empty()) {
+        mk = std::max(mk, q.top());
+        q.pop();
+      }
+      if (best < 0.0 || mk < best * 0.999) {
+        best = mk;
+        best_x = x;
+      }
+    }
+  }
+  if (const char* e = std::getenv("CBM_B200_TILE_SPLIT"))  // test hook: split the last x pairs
+    if (W > 32) best_x = std::min<uint64_t>(T, std::strtoull(e, nullptr, 10));
+  const uint32_t n_main = uint32_t(T - best_x);
+  h->tile_main[key] = n_main;
+  return n_main;
+}
+
 void tile_spmm(DeviceMatrix* h, uint32_t W, const float* x, int64_t ldx, uint32_t d, float* y,
                int64_t ldy, float* interior, uint32_t dpad, bool relu, cudaStream_t s) {
   const auto& t = h->tile;
@@ -432,8 +500,10 @@ void tile_spmm(DeviceMatrix* h, uint32_t W, const float* x, int64_t ldx, uint32_
   p.relu = relu ? 1u : 0u;
   p.max_staged = t.max_staged;
   p.max_rows = t.max_rows;
-  const uint64_t units = uint64_t(t.n_blocks) * p.n_slabs;
-  if (units == 0) return;
+  const uint64_t pairs = uint64_t(t.n_blocks) * p.n_slabs;
+  if (pairs == 0) return;
+  p.n_main = tile_pick_main(h, W, p.n_slabs);
+  const uint64_t units = p.n_main + 2 * (pairs - p.n_main);
   if (units >= 0x7FFFFFFFull) throw invalid_argument("spmm: too many tile units");
   const size_t smem = tile_smem_bytes(h, W);
   const bool norm = h->info.normalized;

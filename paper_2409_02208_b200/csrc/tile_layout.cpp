@@ -269,6 +269,7 @@ TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t st
       T.row.insert(T.row.end(), r, r + 8);
     }
     T.block.insert(T.block.end(), {row0, bptr[b + 1] - bptr[b], st0, uint32_t(cand.size())});
+    T.work.push_back(uint32_t(std::min<uint64_t>(work[b], 0xFFFFFFFFull)));
     T.max_rows = std::max(T.max_rows, bptr[b + 1] - bptr[b]);
     T.max_staged = std::max(T.max_staged, uint32_t(cand.size()));
     for (uint32_t c : touched) {

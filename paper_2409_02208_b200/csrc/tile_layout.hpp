@@ -48,6 +48,7 @@ struct TileLayout {
   std::vector<uint32_t> dcol;   // staged: local index | sign<<31; cold: column | sign<<31
   std::vector<float> dval;      // normalized: signed value +-row_scale[col] per delta
   std::vector<uint32_t> stage;  // staged global columns, per block ascending
+  std::vector<uint32_t> work;   // per block (launch order): estimated work (kept on the host)
 };
 
 // rows_cap: rows per block (0 = auto); stage_cap: staged columns per block

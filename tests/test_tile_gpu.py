@@ -151,3 +151,17 @@ def test_empty_rows_and_identity(dev):
     x = P.generate_dense("normal", 50, 40, 2)
     got, _ = run(eye, x, dev)
     assert_bitwise(got, x, "identity")
+
+
+@pytest.mark.parametrize("split", ["1", "7", "100000"])
+def test_half_width_units(split, dev, monkeypatch):
+    """The last (block, slab) pairs of a launch run as two half-width units
+    (shorter last wave); force 1, 7 or all pairs to split."""
+    monkeypatch.setenv("CBM_B200_TILE_SPLIT", split)
+    a = P.generate_graph("community", [3000, 250, 0.5, 0.003], 7)
+    for normalized in (False, True):
+        c = (P.build_cbm_normalized if normalized else P.build_cbm)(a, 0, threads=8)
+        for d, vec in ((256, 2), (256, 4), (200, 2), (96, 0)):
+            x = P.generate_dense("int", 3000, d, 8, -8, 8)
+            got, _ = run(c, x, dev, tile_vec=vec)
+            check(c, x, got, f"split={split} d={d} vec={vec} norm={normalized}")
