@@ -60,7 +60,14 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       TileLayout T = plan_tiles(v, opt.tile_rows, opt.tile_stage, uint32_t(h->num_sms), gain);
       const double frac = T.n_deltas ? double(T.n_staged_deltas) / double(T.n_deltas) : 0.0;
       const double reuse = T.n_staged_cols ? double(T.n_staged_deltas) / double(T.n_staged_cols) : 0.0;
-      h->tile_on = opt.tile == 1 || (frac >= kTileMinStagedFrac && reuse >= kTileMinReuse);
+      // a row is summed by one warp and a block by one CTA: auto mode also
+      // refuses layouts whose longest row or heaviest block would dominate
+      // the launch (hub rows of power-law graphs)
+      const double per_sm = double(T.n_entries) / double(std::max(1, h->num_sms));
+      const bool balanced = double(T.max_row_entries) <= std::max(4096.0, 0.25 * per_sm) &&
+                            double(T.max_block_entries) <= std::max(65536.0, 2.0 * per_sm);
+      h->tile_on = opt.tile == 1 ||
+                   (frac >= kTileMinStagedFrac && reuse >= kTileMinReuse && balanced);
       if (h->tile_on) {
         put(h->tdcol, T.dcol, "upload tile dcol");
         if (L.normalized) put(h->tdval, T.dval, "upload tile dval");

@@ -225,6 +225,7 @@ TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t st
       T.n_staged_cols += 1;
     }
     const uint32_t row0 = uint32_t(T.row.size() / 8);
+    uint64_t blk_entries = 0;
     for (uint32_t i = bptr[b]; i < bptr[b + 1]; ++i) {
       const uint32_t x = brows[i];
       row_entries(x, ent);
@@ -261,6 +262,8 @@ TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t st
       if (end >= 0xFFFFFFFFull) throw invalid_argument("tiles: more than 2^32-1 deltas");
       for (uint32_t e : ent) T.n_staged_deltas += lidx[e & ~kSign] != kTileNone;
       T.n_entries += ent.size();
+      T.max_row_entries = std::max<uint64_t>(T.max_row_entries, ent.size());
+      blk_entries += ent.size();
       const uint32_t p = v.parent[x];
       const bool has_parent = p != kVirt && !cut[x];
       const uint32_t r[8] = {uint32_t(beg), uint32_t(mpos), uint32_t(mid), uint32_t(end), x,
@@ -270,6 +273,7 @@ TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t st
     }
     T.block.insert(T.block.end(), {row0, bptr[b + 1] - bptr[b], st0, uint32_t(cand.size())});
     T.work.push_back(uint32_t(std::min<uint64_t>(work[b], 0xFFFFFFFFull)));
+    T.max_block_entries = std::max(T.max_block_entries, blk_entries);
     T.max_rows = std::max(T.max_rows, bptr[b + 1] - bptr[b]);
     T.max_staged = std::max(T.max_staged, uint32_t(cand.size()));
     for (uint32_t c : touched) {

@@ -36,6 +36,8 @@ struct TileLayout {
   uint32_t n_blocks = 0, max_rows = 0, max_staged = 0, n_interior = 0, n_cut = 0, n_flat = 0;
   uint32_t row_cap = 0, stage_cap = 0;
   uint64_t n_deltas = 0, n_staged_deltas = 0, n_staged_cols = 0, n_entries = 0;
+  uint64_t max_row_entries = 0;  // longest row (one warp sums a row: no splitting)
+  uint64_t max_block_entries = 0;  // heaviest block (one CTA per block and slab)
   // per block: row0, nrows, st0, nst (tile rows [row0, row0+nrows), staged
   // columns tstage[st0, st0+nst)); blocks ordered by estimated work, largest first
   std::vector<uint32_t> block;
