@@ -841,6 +841,20 @@ __global__ void prescale_kernel(const float* __restrict__ x, long long ldx,
   }
 }
 
+// relu_inplace (dense.cpp:51-54) on a column slab of Y: the binary streaming
+// kernel's children read their parent's row from Y itself, so a fused ReLU
+// would feed them clipped parents; binary multiplies with ReLU clip afterwards.
+__global__ void relu_kernel(float* __restrict__ y, long long ldy, uint32_t rows, uint32_t d) {
+  const uint64_t total = (uint64_t)rows * d;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = uint32_t(i / d), c = uint32_t(i - (uint64_t)r * d);
+    float* q = y + (long long)r * ldy + c;
+    const float v = *q;
+    if (v < 0.0f) *q = 0.0f;
+  }
+}
+
 // Cooperative launch: one full residency wave (all warps co-resident), no
 // more warps than tickets.
 void launch_coop(const void* kernel, size_t smem, int& bps, Params& p, uint64_t tickets,
@@ -1005,7 +1019,10 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   if (tickets >= 0x7FFFFFFFull) throw invalid_argument("spmm: too many work tickets");
   p.total_tickets = uint32_t(tickets);
   p.epoch = ws.epoch;
-  p.relu = relu ? 1u : 0u;
+  // binary streaming kernel: children read parents from Y, so the ReLU runs
+  // after the multiply (relu_kernel below); normalized parents come from scratch
+  const bool relu_after = relu && !L.normalized;
+  p.relu = relu && !relu_after ? 1u : 0u;
   // pull a small, contiguous X into L2 ahead of the gathers
   const uint64_t xbytes = uint64_t(L.n_cols) * d * sizeof(float);
   p.prefetch_bytes = (h->opt.prefetch != 0 && uint64_t(ldin) == d && xbytes >= (1u << 20) &&
@@ -1050,6 +1067,13 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   }
   ck(cudaGetLastError(), "cbm_kernel launch");
   ++h->last_launches;
+  if (relu_after) {
+    const uint64_t total = uint64_t(L.n_rows) * d;
+    const int grid = int(std::min<uint64_t>((total + 255) / 256, uint64_t(h->num_sms) * 16));
+    relu_kernel<<<grid, 256, 0, s>>>(y, ldy, L.n_rows, d);
+    ck(cudaGetLastError(), "relu launch");
+    ++h->last_launches;
+  }
   if (trace) {
     std::vector<unsigned long long> t(trace_n);
     ck(cudaStreamSynchronize(s), "trace");

@@ -440,3 +440,20 @@ def test_lane_groups_narrow_operands(normalized, dev):
                     assert_bitwise(got, want, f"lane groups d={d} {opts}")
                 else:
                     assert normwise_err(got, want) <= TOL, (d, kind, opts)
+
+
+@pytest.mark.parametrize("tile", [0, 1])
+@pytest.mark.parametrize("faithful", [False, True])
+def test_binary_relu_epilogue(tile, faithful, dev):
+    """spmm_ex with CBM_B200_RELU on a BINARY matrix: children must add their
+    parent's unclipped row (relu_inplace, dense.cpp:51-54, applies to the
+    finished product only)."""
+    a = P.generate_graph("community", [2000, 100, 0.5, 0.002], 171)
+    c = P.build_cbm(a, 0, threads=8)
+    x = P.generate_dense("int", 2000, 96, 172, -8, 8)
+    want = O.oracle_spmm(oracle_arrays(c), x)
+    want = np.where(want < 0, np.float32(0), want)
+    h = P.DeviceCbm(c, tile=tile, order_faithful=faithful)
+    y = h.spmm(torch.from_numpy(x).to(dev), relu=True)
+    torch.cuda.synchronize()
+    assert_bitwise(y.cpu().numpy(), want, f"binary relu tile={tile} faithful={faithful}")
