@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -857,15 +858,24 @@ __global__ void relu_kernel(float* __restrict__ y, long long ldy, uint32_t rows,
 
 // Cooperative launch: one full residency wave (all warps co-resident), no
 // more warps than tickets.
-void launch_coop(const void* kernel, size_t smem, int& bps, Params& p, uint64_t tickets,
-                 uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
-  if (bps < 0) {
+// Per (kernel instance, device): the dynamic shared-memory attribute is set
+// and the occupancy queried once on every device the kernel runs on (0 = not
+// yet; the attribute belongs to the device's context).
+constexpr int kMaxDevices = 64;
+using DeviceSlots = std::atomic<int>[kMaxDevices];
+
+void launch_coop(const void* kernel, size_t smem, DeviceSlots& slots, Params& p,
+                 uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
+  if (h->device < 0 || h->device >= kMaxDevices) throw invalid_argument("spmm: device ordinal");
+  int bps = slots[h->device].load(std::memory_order_acquire);
+  if (bps == 0) {
     ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
        "smem attribute");
     int b = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kWarpsPerCta * 32, smem),
        "occupancy");
     bps = std::max(1, b);
+    slots[h->device].store(bps, std::memory_order_release);
   }
   // cooperative launch: one full residency wave, never more warps than tickets
   constexpr uint64_t wpb = kWarpsPerCta;
@@ -891,16 +901,16 @@ void launch_coop(const void* kernel, size_t smem, int& bps, Params& p, uint64_t 
 
 template <int V, int U, int D, bool NORM, int SC, int H = 1>
 void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
-  static int bps = -1;  // per template instance
+  static DeviceSlots slots;  // per template instance and device
   launch_coop(reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SC, H>),
-              kWarpsPerCta * sizeof(WarpSmem<V, U, D>), bps, p, tickets, slabs, h, s);
+              kWarpsPerCta * sizeof(WarpSmem<V, U, D>), slots, p, tickets, slabs, h, s);
 }
 
 template <bool NORM, int SC>
 void launch_spmv(Params& p, uint64_t tickets, DeviceMatrix* h, cudaStream_t s) {
-  static int bps = -1;
+  static DeviceSlots slots;
   launch_coop(reinterpret_cast<const void*>(&cbm_spmv_kernel<NORM, SC>),
-              kWarpsPerCta * sizeof(SpmvSmem), bps, p, tickets, 1, h, s);
+              kWarpsPerCta * sizeof(SpmvSmem), slots, p, tickets, 1, h, s);
 }
 
 template <int V, int U, int D>

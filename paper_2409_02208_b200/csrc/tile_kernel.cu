@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -389,14 +390,16 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) tile_kernel(const Til
 #endif
 
 template <int H, bool NORM>
-void launch_tile(const TileParams& p, uint32_t units, size_t smem, cudaStream_t s) {
+void launch_tile(const TileParams& p, uint32_t units, size_t smem, int device, cudaStream_t s) {
   constexpr int NT = CBM_TILE_THREADS;
-  static bool attr = false;
-  if (!attr) {
+  // the dynamic shared-memory attribute belongs to each device's context
+  static std::atomic<uint64_t> set_on{0};
+  const uint64_t bit = 1ull << (device & 63);
+  if (!(set_on.load(std::memory_order_acquire) & bit)) {
     ck(cudaFuncSetAttribute(tile_kernel<H, NORM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             227 * 1024),
        "tile smem attribute");
-    attr = true;
+    set_on.fetch_or(bit, std::memory_order_acq_rel);
   }
   tile_kernel<H, NORM, NT><<<units, NT, smem, s>>>(p);
 }
@@ -514,12 +517,12 @@ void tile_spmm(DeviceMatrix* h, uint32_t W, const float* x, int64_t ldx, uint32_
     ck(cudaMalloc(&p.trace, units * 32), "trace");
     ck(cudaMemsetAsync(p.trace, 0, units * 32, s), "trace");
   }
-  if (W == 128) norm ? launch_tile<1, true>(p, uint32_t(units), smem, s)
-                     : launch_tile<1, false>(p, uint32_t(units), smem, s);
-  else if (W == 64) norm ? launch_tile<2, true>(p, uint32_t(units), smem, s)
-                         : launch_tile<2, false>(p, uint32_t(units), smem, s);
-  else norm ? launch_tile<4, true>(p, uint32_t(units), smem, s)
-            : launch_tile<4, false>(p, uint32_t(units), smem, s);
+  if (W == 128) norm ? launch_tile<1, true>(p, uint32_t(units), smem, h->device, s)
+                     : launch_tile<1, false>(p, uint32_t(units), smem, h->device, s);
+  else if (W == 64) norm ? launch_tile<2, true>(p, uint32_t(units), smem, h->device, s)
+                         : launch_tile<2, false>(p, uint32_t(units), smem, h->device, s);
+  else norm ? launch_tile<4, true>(p, uint32_t(units), smem, h->device, s)
+            : launch_tile<4, false>(p, uint32_t(units), smem, h->device, s);
   ck(cudaGetLastError(), "tile_kernel launch");
   if (p.trace) {
     std::vector<unsigned long long> t(units * 4);
