@@ -172,7 +172,18 @@ void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, 
   if (bytes >= (8u << 20) && d >= 128) chunks = d >= 256 ? 5 : 2;
   if (const char* e = std::getenv("CBM_B200_HOST_CHUNKS"))  // dev tool: uniform chunks
     chunks = std::max<uint32_t>(1, std::min<uint32_t>({kHostChunks, uint32_t(std::atoi(e)), d}));
-  if (chunks == 5 && !std::getenv("CBM_B200_HOST_CHUNKS")) {  // d >= 256
+  if (const char* e = std::getenv("CBM_B200_HOST_WIDTHS")) {  // dev tool: explicit widths
+    uint32_t c0 = 0;
+    for (const char* q = e; *q && c0 < d;) {
+      const uint32_t w = std::min<uint32_t>(uint32_t(std::strtoul(q, const_cast<char**>(&q), 10)), d - c0);
+      if (w == 0) break;
+      parts.emplace_back(c0, w);
+      c0 += w;
+      if (*q == ',') ++q;
+    }
+    if (c0 < d) parts.emplace_back(c0, d - c0);
+    if (parts.size() > kHostChunks) throw invalid_argument("CBM_B200_HOST_WIDTHS: too many chunks");
+  } else if (chunks == 5 && !std::getenv("CBM_B200_HOST_CHUNKS")) {  // d >= 256
     const uint32_t edge = r4(d / 8), rest = d - 2 * edge, mid = r4((rest + 2) / 3);
     uint32_t c0 = 0;
     const uint32_t m3 = (rest - 2 * mid) & ~3u;  // every chunk starts 16-byte aligned

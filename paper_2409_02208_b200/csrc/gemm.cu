@@ -39,73 +39,22 @@ __device__ __forceinline__ void store_c(const Parts& P, uint32_t i, uint32_t cc,
   for (uint32_t o = 0; o < P.n_out; ++o) P.out[o][(size_t)i * P.ldc + cc] = v;
 }
 
-// dense_matmul (dense.cpp:31-49) with the reference's exact arithmetic:
-// c[i,q] = sum over ascending j with a[i,j] != 0 of fl(a[i,j] * b[j,q]),
-// each product rounded before the add, starting from +0. A CTA computes a
-// 32-row x 128-column tile; b is staged through shared memory 32 rows of j at
-// a time; the zero test is warp-uniform (a warp shares its row).
-constexpr int kGemmRows = 32, kGemmCols = 128, kGemmK = 32;
-template <bool MULTI>
-__global__ void __launch_bounds__(256) ordered_gemm_kernel(const Parts P,
-                                                           const float* __restrict__ b,
-                                                           uint32_t m, uint32_t k, uint32_t n) {
-  __shared__ float bs[kGemmK][kGemmCols];
-  __shared__ float as[kGemmRows][kGemmK + 1];
-  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 lanes x 8 warps
-  const uint32_t row0 = blockIdx.y * kGemmRows, col0 = blockIdx.x * kGemmCols;
-  float acc[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[r][q] = 0.0f;
-  for (uint32_t j0 = 0; j0 < k; j0 += kGemmK) {
-    __syncthreads();
-    for (uint32_t e = threadIdx.x; e < kGemmK * kGemmCols; e += 256) {
-      const uint32_t jj = e / kGemmCols, cc = e % kGemmCols;
-      bs[jj][cc] = (j0 + jj < k && col0 + cc < n) ? b[(size_t)(j0 + jj) * n + col0 + cc] : 0.0f;
-    }
-    for (uint32_t e = threadIdx.x; e < kGemmRows * kGemmK; e += 256) {
-      const uint32_t rr = e / kGemmK, jj = e % kGemmK;
-      as[rr][jj] = (row0 + rr < m && j0 + jj < k) ? load_a<MULTI>(P, row0 + rr, j0 + jj) : 0.0f;
-    }
-    __syncthreads();
-    const uint32_t jn = min(uint32_t(kGemmK), k - j0);
-    for (uint32_t jj = 0; jj < jn; ++jj) {
-      float bv[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) bv[q] = bs[jj][tx + 32 * q];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const float av = as[ty + 8 * r][jj];
-        if (av != 0.0f) {  // dense.cpp:42 skips zero lhs entries
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[r][q] = __fadd_rn(acc[r][q], __fmul_rn(av, bv[q]));
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const uint32_t i = row0 + ty + 8 * r;
-    if (i >= m) continue;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t cc = col0 + tx + 32 * q;
-      if (cc < n) store_c<MULTI>(P, i, cc, acc[r][q]);
-    }
-  }
-}
-
-// Default-mode GEMM of the GCN (within the north_star tolerance, not bit-exact):
-// FFMA, 128 x 128 output tile per CTA, 8 x 8 per thread, k staged 8 at a time
-// (A transposed in shared memory). Finite operands assumed: a zero lhs entry
-// contributes fma(0, b, acc) = acc like dense.cpp:42's skip. Part widths are
-// multiples of 4 (column_slab), so a 4-wide k group never straddles two parts.
+// 128 x 128 output tile per CTA, 8 x 8 per thread, k staged 8 at a time (A
+// transposed in shared memory).
+//   ORDERED: dense_matmul (dense.cpp:31-49) bit for bit. Every entry sums
+//     fl(a*b) in ascending k with separate rounding (FMUL then FADD). The
+//     reference skips zero lhs entries (dense.cpp:42); adding fl(0*b) = +-0
+//     instead leaves the sum unchanged (it starts at +0 and can never become
+//     -0), unless b is not finite, so a k-step whose B rows hold an inf or
+//     NaN takes the per-entry skip (block-uniform branch).
+//   !ORDERED (default-mode GCN, north_star tolerance): FFMA.
+// Part widths are multiples of 4 (column_slab), so a 4-wide k group never
+// straddles two parts.
 constexpr int kFB = 128, kFK = 8;
-template <bool MULTI>
-__global__ void __launch_bounds__(256, 2) fast_gemm_kernel(const Parts P,
-                                                           const float* __restrict__ b,
-                                                           uint32_t m, uint32_t k, uint32_t n) {
+template <bool MULTI, bool ORDERED>
+__global__ void __launch_bounds__(256, 2) tiled_gemm_kernel(const Parts P,
+                                                            const float* __restrict__ b,
+                                                            uint32_t m, uint32_t k, uint32_t n) {
   __shared__ __align__(16) float as[kFK][kFB];
   __shared__ __align__(16) float bs[kFK][kFB];
   const uint32_t t = threadIdx.x, tx = t & 15, ty = t >> 4;
@@ -119,30 +68,50 @@ __global__ void __launch_bounds__(256, 2) fast_gemm_kernel(const Parts P,
   const uint32_t bk = t >> 5, bc = (t & 31) * 4;  // B tile: k bk, cols bc..bc+3
   for (uint32_t k0 = 0; k0 < k; k0 += kFK) {
     float av[4], bv[4];
+    bool nonfinite = false;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint32_t kk = k0 + ak + i;
       av[i] = (row0 + ar < m && kk < k) ? load_a<MULTI>(P, row0 + ar, kk) : 0.0f;
       const uint32_t cc = col0 + bc + i;
       bv[i] = (k0 + bk < k && cc < n) ? __ldg(b + (size_t)(k0 + bk) * n + cc) : 0.0f;
+      nonfinite |= !isfinite(bv[i]);
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i) as[ak + i][ar] = av[i];
     *reinterpret_cast<float4*>(&bs[bk][bc]) = make_float4(bv[0], bv[1], bv[2], bv[3]);
-    __syncthreads();
+    const bool exact_skip = __syncthreads_or(ORDERED && nonfinite) != 0;
+    const uint32_t kn = min(uint32_t(kFK), k - k0);
+    if (!exact_skip) {
 #pragma unroll
-    for (int kk = 0; kk < kFK; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&as[kk][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&as[kk][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&bs[kk][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&bs[kk][64 + tx * 4]);
-      const float ar8[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float br8[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      for (int kk = 0; kk < kFK; ++kk) {
+        if (ORDERED && uint32_t(kk) >= kn) break;  // (zero padding is harmless for FFMA)
+        const float4 a0 = *reinterpret_cast<const float4*>(&as[kk][ty * 4]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&as[kk][64 + ty * 4]);
+        const float4 b0 = *reinterpret_cast<const float4*>(&bs[kk][tx * 4]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&bs[kk][64 + tx * 4]);
+        const float ar8[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float br8[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[r][q] = __fmaf_rn(ar8[r], br8[q], acc[r][q]);
+          for (int q = 0; q < 8; ++q)
+            acc[r][q] = ORDERED ? __fadd_rn(acc[r][q], __fmul_rn(ar8[r], br8[q]))
+                                : __fmaf_rn(ar8[r], br8[q], acc[r][q]);
+      }
+    } else {
+      for (uint32_t kk = 0; kk < kn; ++kk) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float a = as[kk][r < 4 ? ty * 4 + r : 64 + ty * 4 + r - 4];
+          if (a == 0.0f) continue;  // dense.cpp:42
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            acc[r][q] = __fadd_rn(acc[r][q],
+                                  __fmul_rn(a, bs[kk][q < 4 ? tx * 4 + q : 64 + tx * 4 + q - 4]));
+        }
+      }
     }
   }
 #pragma unroll
@@ -173,14 +142,13 @@ void launch_gemm(const Parts& P, uint32_t m, uint32_t k, const float* b, uint32_
                  bool ordered, cudaStream_t s) {
   if (m == 0 || n == 0) return;
   const bool multi = P.n_parts > 1 || P.n_out > 1;
+  const dim3 grid((n + kFB - 1) / kFB, (m + kFB - 1) / kFB);
   if (ordered) {
-    const dim3 grid((n + kGemmCols - 1) / kGemmCols, (m + kGemmRows - 1) / kGemmRows);
-    if (multi) ordered_gemm_kernel<true><<<grid, 256, 0, s>>>(P, b, m, k, n);
-    else ordered_gemm_kernel<false><<<grid, 256, 0, s>>>(P, b, m, k, n);
+    if (multi) tiled_gemm_kernel<true, true><<<grid, 256, 0, s>>>(P, b, m, k, n);
+    else tiled_gemm_kernel<false, true><<<grid, 256, 0, s>>>(P, b, m, k, n);
   } else {
-    const dim3 grid((n + kFB - 1) / kFB, (m + kFB - 1) / kFB);
-    if (multi) fast_gemm_kernel<true><<<grid, 256, 0, s>>>(P, b, m, k, n);
-    else fast_gemm_kernel<false><<<grid, 256, 0, s>>>(P, b, m, k, n);
+    if (multi) tiled_gemm_kernel<true, false><<<grid, 256, 0, s>>>(P, b, m, k, n);
+    else tiled_gemm_kernel<false, false><<<grid, 256, 0, s>>>(P, b, m, k, n);
   }
   ck(cudaGetLastError(), "gemm launch");
 }

@@ -54,6 +54,25 @@ def test_gemm_parts_equals_concatenated_gemm(widths, n):
     assert normwise_err(fast[0].cpu().numpy(), want) <= 1e-5
 
 
+def test_dense_matmul_nonfinite_rhs_and_zero_lhs():
+    """dense.cpp:42 skips zero lhs entries: 0 * inf must not turn into NaN,
+    while a nonzero lhs times inf must (k-steps with a non-finite B row take the
+    per-entry skip)."""
+    rng = np.random.default_rng(5)
+    m, k, n = 300, 37, 70
+    a = rng.standard_normal((m, k)).astype(np.float32)
+    a[rng.random((m, k)) < 0.4] = 0.0
+    a[:, 3] = 0.0
+    b = rng.standard_normal((k, n)).astype(np.float32)
+    b[3, 5] = np.inf
+    b[3, 6] = np.nan
+    b[20, 7] = -np.inf
+    want = O.oracle_dense_matmul(a, b)
+    got = P.dense_matmul(_t(a), _t(b)).cpu().numpy()
+    assert_bitwise(got, want, "nonfinite rhs")
+    assert np.isfinite(got[:, 5]).all() or not np.isfinite(want[:, 5]).all()
+
+
 def _gcn_inputs():
     a = P.generate_graph("community", [3000, 500, 0.8, 1e-4], 91)
     c = P.build_cbm_normalized(a, 0, threads=8)

@@ -55,8 +55,13 @@ def one(name, chunks):
 
 if __name__ == "__main__":
     if len(sys.argv) > 3:
-        one(sys.argv[1], int(sys.argv[3]))
+        one(sys.argv[1], sys.argv[3])
     else:
         for ch in sys.argv[2].split(","):
             env = dict(os.environ, CBM_B200_HOST_CHUNKS=ch)
+            if ch == "0":  # the library's default chunking
+                env.pop("CBM_B200_HOST_CHUNKS")
+            if "/" in ch:  # explicit widths, e.g. 32/96/128/128/96/32
+                env.pop("CBM_B200_HOST_CHUNKS")
+                env["CBM_B200_HOST_WIDTHS"] = ch.replace("/", ",")
             subprocess.run([sys.executable, __file__, sys.argv[1], "", ch], env=env, check=True)
