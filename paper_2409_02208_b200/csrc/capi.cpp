@@ -259,6 +259,7 @@ int cbm_b200_spmm(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_
     need(h != nullptr, "spmm: null handle");
     check_spmm_shapes(h->d->info, x_rows, x_cols, y_rows, y_cols, "spmm");
     need(ldx >= x_cols && ldy >= y_cols, "spmm: leading dimension smaller than the width");
+    need(ldx < (int64_t(1) << 30), "spmm: leading dimension of X must be below 2^30");
     need((x || x_rows * x_cols == 0) && (y || y_rows * y_cols == 0), "spmm: null data");
     std::lock_guard<std::mutex> lk(h->d->mu);
     cbmb::device_spmm(h->d, x, ldx, uint32_t(x_cols), y, ldy, stream);
@@ -273,6 +274,7 @@ int cbm_b200_spmm_ex(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t
     need((flags & ~CBM_B200_RELU) == 0, "spmm: unknown flags");
     check_spmm_shapes(h->d->info, x_rows, x_cols, y_rows, y_cols, "spmm");
     need(ldx >= x_cols && ldy >= y_cols, "spmm: leading dimension smaller than the width");
+    need(ldx < (int64_t(1) << 30), "spmm: leading dimension of X must be below 2^30");
     need((x || x_rows * x_cols == 0) && (y || y_rows * y_cols == 0), "spmm: null data");
     std::lock_guard<std::mutex> lk(h->d->mu);
     cbmb::device_spmm(h->d, x, ldx, uint32_t(x_cols), y, ldy, stream,

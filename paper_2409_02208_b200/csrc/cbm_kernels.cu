@@ -150,7 +150,8 @@ struct Params {
   uint32_t faithful;    // order-faithful mode (spmv: sequential adds)
   uint64_t prefetch_bytes;  // > 0: X is one contiguous block of this size, pulled into L2 first
   unsigned long long* trace;  // dev tool (CBM_B200_TRACE): 4 x u64 per warp, else null
-  uint32_t ldx32;             // ldx in floats (< 2^31): 32x32->64 address multiply
+  uint32_t ldx32;             // ldx in floats (< 2^30): 32x32->64 address multiply
+  uint32_t ldxb;              // ldx in bytes (< 2^32): one IMAD.WIDE per gathered row
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -466,6 +467,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
   // ---- issue cursor: ticket ii, offset iq inside it. win = window of ii,
   // wn1 / wn2 = windows of ii+1 / ii+2 (fetched two tickets ahead)
   uint32_t ii = 0, iq = 0, ibeg = 0, ilen = 0, icol = 0, imask = 0;
+  const char* ixb = reinterpret_cast<const char*>(p.x);  // this ticket's column slab of X row 0
   bool ifull = true;  // warp-uniform: every segment of every lane inside the matrix
   Wd win = window(0), wn1 = window(1), wn2 = window(2), wlong{0u, 0.0f};
   uint32_t iseq = 0;     // ring slots issued (B per group)
@@ -479,6 +481,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
     ibeg = r.beg;
     ilen = r.end - r.beg;
     icol = r.slab * kSlab + jv;
+    ixb = reinterpret_cast<const char*>(p.x + icol);
     imask = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -512,54 +515,60 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
     if (!iblocked && ii < n_w) {
       const uint32_t n = min(kGroup, ilen - iq);
       const uint32_t s0 = iseq & (D - 1);  // a multiple of B
-      // all B column words / values first (no shuffle under a branch), then
-      // B predicated copies: slots past the ticket's end are zero-filled with
+      // all B column words first (no shuffle under a branch), then B
+      // predicated copies: slots past the ticket's end are zero-filled with
       // value 0, so the consumer adds exact zeros there (acc is never -0)
       // slot s0 + b holds deltas b*H + h of the group, lane group h each
+      // (a group never spans two 32-delta windows: iq & 31 is a multiple of
+      // kGroup and 32 % kGroup == 0, so (iq & 31) + b*H + hl < 32)
       uint32_t cwb[B];
-      float vb[B];
+      const uint32_t wl = (iq & 31) + hl;
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        cwb[b] = __shfl_sync(kFull, win.c, (iq + uint32_t(b) * H + hl) & 31);
-        if constexpr (SC != 0 && H == 1) vb[b] = __shfl_sync(kFull, win.v, (iq + b) & 31);
+      for (int b = 0; b < B; ++b) cwb[b] = __shfl_sync(kFull, win.c, wl + uint32_t(b) * H);
+      // the deltas' signed values (the reference's values[k], kernels.cpp:33):
+      // lane (s0 + b) * H + h of the value ring holds delta q = b * H + h of
+      // the group, i.e. q = lane - s0 * H; one shuffle per group, not per delta
+      {
+        const uint32_t q = uint32_t(lane) - s0 * H;
+        float val;
+        if constexpr (SC != 0) {
+          val = __shfl_sync(kFull, win.v, (iq + q) & 31);
+        } else {
+          const uint32_t cv = __shfl_sync(kFull, win.c, (iq + q) & 31);
+          val = __int_as_float(0x3F800000u | (cv & 0x80000000u));
+        }
+        if (q < kGroup) vring = q < n ? val : 0.0f;
       }
+      if (ifull) {  // straight-line copies: one size for all segments, immediate
+        // segment offsets, one IMAD.WIDE per row address (byte pitch < 2^32)
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const bool on = uint32_t(b) * H + hl < n;
-        const uint32_t c = on ? (cwb[b] & 0x7FFFFFFFu) : 0u;
-        const float* src = p.x + (uint64_t)c * p.ldx32 + icol;
-        if (ifull) {  // one size for all segments, immediate segment offsets
+        for (int b = 0; b < B; ++b) {
+          // past the ticket's end the word is another delta of this window or
+          // 0 (fetch): a valid row either way, and nothing is read (size 0)
+          const bool on = uint32_t(b) * H + hl < n;
+          const uint32_t c = cwb[b] & 0x7FFFFFFFu;
+          const float* src = reinterpret_cast<const float*>(ixb + (uint64_t)c * p.ldxb);
           const uint32_t sz = on ? uint32_t(V * 4) : 0u;
 #pragma unroll
           for (int u = 0; u < U; ++u) cp_async_n<V>(&sm.ring[s0 + b][u][lane * V], src + u * kSeg, sz);
-        } else if constexpr (U == 1 && H == 1) {  // the matrix edge: a real call keeps
-          // the one-segment hot path unpredicated (A/B: cfg[2] 921 -> 838 us; with
-          // lane groups the call costs more than it saves, cfg[0] 20.5 -> 22.5 us)
-          edge_copies<V, U, kSeg>(&sm.ring[s0 + b][0][lane * V], src, p.x, imask, on);
-        } else {  // (inline for U > 1: a call there costs more than the predication)
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const bool ok = on && ((imask >> u) & 1u);
-            cp_async_z<V>(&sm.ring[s0 + b][u][lane * V], ok ? src + u * kSeg : p.x, ok);
-          }
         }
-        // the delta's signed value (the reference's values[k], kernels.cpp:33),
-        // held by lane (s0 + b) * H + h of the value ring
-        if constexpr (H == 1) {
-          float val = SC != 0 ? vb[b] : __int_as_float(0x3F800000u | (cwb[b] & 0x80000000u));
-          if (!on) val = 0.0f;
-          if (uint32_t(lane) == s0 + b) vring = val;
-        } else {
-          const uint32_t hh = uint32_t(lane) - (s0 + b) * H;  // < H on the holder lanes
-          const uint32_t q = uint32_t(b) * H + (hh < H ? hh : 0u);
-          float val;
-          if constexpr (SC != 0) {
-            val = __shfl_sync(kFull, win.v, (iq + q) & 31);
-          } else {
-            const uint32_t cv = __shfl_sync(kFull, win.c, (iq + q) & 31);
-            val = __int_as_float(0x3F800000u | (cv & 0x80000000u));
+      } else {
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const bool on = uint32_t(b) * H + hl < n;
+          const uint32_t c = on ? (cwb[b] & 0x7FFFFFFFu) : 0u;
+          const float* src = reinterpret_cast<const float*>(ixb + (uint64_t)c * p.ldxb);
+          if constexpr (U == 1 && H == 1) {  // the matrix edge: a real call keeps
+            // the one-segment hot path unpredicated (A/B: cfg[2] 921 -> 838 us; with
+            // lane groups the call costs more than it saves, cfg[0] 20.5 -> 22.5 us)
+            edge_copies<V, U, kSeg>(&sm.ring[s0 + b][0][lane * V], src, p.x, imask, on);
+          } else {  // (inline for U > 1: a call there costs more than the predication)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const bool ok = on && ((imask >> u) & 1u);
+              cp_async_z<V>(&sm.ring[s0 + b][u][lane * V], ok ? src + u * kSeg : p.x, ok);
+            }
           }
-          if (hh < H) vring = q < n ? val : 0.0f;
         }
       }
       iseq += B;
@@ -1054,6 +1063,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   }
   p.faithful = L.order_faithful ? 1u : 0u;
   p.ldx32 = uint32_t(ldin);
+  p.ldxb = uint32_t(ldin) * 4u;  // ldin < 2^30 (checked at the C ABI)
   if (H > 1) {
     if (H == 2) run_groups<2>(p, tickets, n_slabs, norm, scl, h, s);
     else run_groups<4>(p, tickets, n_slabs, norm, scl, h, s);
