@@ -109,8 +109,13 @@ struct Vec<4> {
 };
 
 // ---------------------------------------------------------------- flags
+// Every lane's row stores, then the warp barrier (memory ordering among the
+// participating lanes), then lane 0's release store at gpu scope, which is
+// cumulative over the stores it has observed: the split-K semaphore pattern
+// (barrier, then one thread's fence.acq_rel + store). No per-lane
+// fence.sc.gpu: that was a second full MEMBAR (+ L1 invalidate) per publish,
+// ~5% of cfg[2]'s stall samples.
 __device__ __forceinline__ void publish(uint32_t* f, uint32_t epoch) {
-  __threadfence();  // each lane's row stores before the flag (gpu scope)
   __syncwarp();
   if ((threadIdx.x & 31) == 0)
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
