@@ -275,6 +275,23 @@ __device__ __forceinline__ typename Vec<V>::T relu_v(typename Vec<V>::T v) {
   else if constexpr (V == 2) return make_float2(relu1(v.x), relu1(v.y));
   else return relu1(v);
 }
+// n consecutive floats from shared memory (16-byte aligned for n >= 4)
+template <int N>
+__device__ __forceinline__ void load_vals(const float* p, float (&o)[N]) {
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+      const float4 a = *reinterpret_cast<const float4*>(p + i);
+      o[i] = a.x; o[i + 1] = a.y; o[i + 2] = a.z; o[i + 3] = a.w;
+    }
+  } else if constexpr (N == 2) {
+    const float2 a = *reinterpret_cast<const float2*>(p);
+    o[0] = a.x; o[1] = a.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) o[i] = p[i];
+  }
+}
 template <int V>
 __device__ __forceinline__ typename Vec<V>::T lds(const float* p) {
   if constexpr (V == 4) return *reinterpret_cast<const float4*>(p);
@@ -376,6 +393,7 @@ template <int V, int U, int D>
 struct alignas(16) WarpSmem {
   float ring[D][U][32 * V];      // slot s, segment u, lane l: [s][u][l*V, l*V+V)
   TRec rec[rec_window<U>()];     // warp-sequence tickets [g, g+RW), slot i & (RW-1)
+  float val[32];                 // signed delta values: lane group h, slot s at [h*D + s]
 };
 
 // Stage the records of warp-sequence tickets [i0, i0+RW/2) into a window of
@@ -478,7 +496,6 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
   uint32_t iseq = 0;     // ring slots issued (B per group)
   uint32_t icommit = 0;  // ring groups committed; the consumer's k-th group is the k-th
   uint32_t cgroup = 0;   // groups consumed
-  float vring = 0.0f;  // lane s: signed value of the delta in ring slot s
   bool iblocked = false;
   auto load_ticket = [&]() {  // cursor fields of ticket ii (window already in win)
     iq = 0;
@@ -531,10 +548,11 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
 #pragma unroll
       for (int b = 0; b < B; ++b) cwb[b] = __shfl_sync(kFull, win.c, wl + uint32_t(b) * H);
       // the deltas' signed values (the reference's values[k], kernels.cpp:33):
-      // lane (s0 + b) * H + h of the value ring holds delta q = b * H + h of
-      // the group, i.e. q = lane - s0 * H; one shuffle per group, not per delta
+      // lane q < kGroup fetches delta q = b * H + h of the group and stores it
+      // at val[h * D + s0 + b], so the consumer reads a group's B values of
+      // its lane group with one or two broadcast LDS
       {
-        const uint32_t q = uint32_t(lane) - s0 * H;
+        const uint32_t q = uint32_t(lane);
         float val;
         if constexpr (SC != 0) {
           val = __shfl_sync(kFull, win.v, (iq + q) & 31);
@@ -542,7 +560,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
           const uint32_t cv = __shfl_sync(kFull, win.c, (iq + q) & 31);
           val = __int_as_float(0x3F800000u | (cv & 0x80000000u));
         }
-        if (q < kGroup) vring = q < n ? val : 0.0f;
+        if (q < kGroup) sm.val[(q % H) * D + s0 + q / H] = q < n ? val : 0.0f;
       }
       if (ifull) {  // straight-line copies: one size for all segments, immediate
         // segment offsets, one IMAD.WIDE per row address (byte pitch < 2^32)
@@ -597,6 +615,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
   if (R(0).end != R(0).beg) load_ticket();
   else next_ticket();
   refill();
+  __syncwarp();  // the first groups' values are in sm.val
 
   uint32_t cseq = 0;  // deltas consumed
 #pragma unroll 1
@@ -610,6 +629,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
         iblocked = false;
         next_ticket();
         refill();
+        __syncwarp();
       }
     }
     const uint32_t k_ci = ci & (RW - 1);
@@ -631,11 +651,12 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
       if (icommit <= cgroup) __trap();
       cp_wait_upto<G - 1>(icommit - 1 - cgroup);
       const uint32_t s0 = cseq & (D - 1);
+      if constexpr (G == 1) __syncwarp();  // (G >= 2: a barrier already follows the issue)
       float sc[B];
+      load_vals<B>(&sm.val[hl * D + s0], sc);  // +-1 or +-s_c
       T4 v[B][U];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        sc[b] = __shfl_sync(kFull, vring, (s0 + b) * H + hl);  // +-1 or +-s_c
 #pragma unroll
         for (int u = 0; u < U; ++u) v[b][u] = lds<V>(&sm.ring[s0 + b][u][lane * V]);
       }

@@ -111,6 +111,11 @@ def test_shape_errors_mirror_reference(dev):
         d.spmv_into(torch.zeros((3, 2), device=dev), torch.zeros((3, 1), device=dev))
     with pytest.raises(ValueError, match="spmv: inner dimensions differ"):
         d.spmv(torch.zeros((4, 1), device=dev))
+    # the gather kernels address X rows with a 32-bit byte pitch (checked
+    # before any device work, so the buffers are never touched)
+    x, y = torch.zeros((3, 2), device=dev), torch.zeros((3, 2), device=dev)
+    rc = P._lib.cbm_b200_spmm(d._h, x.data_ptr(), 3, 2, 1 << 30, y.data_ptr(), 3, 2, 2, None)
+    assert rc == P.EINVAL and b"below 2^30" in P._lib.cbm_b200_last_error()
 
 
 # ------------------------------------------------------------- seeded suites
