@@ -540,26 +540,22 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
       // all B column words first (no shuffle under a branch), then B
       // predicated copies: slots past the ticket's end are zero-filled with
       // value 0, so the consumer adds exact zeros there (acc is never -0)
-      // slot s0 + b holds deltas b*H + h of the group, lane group h each
-      // (a group never spans two 32-delta windows: iq & 31 is a multiple of
-      // kGroup and 32 % kGroup == 0, so (iq & 31) + b*H + hl < 32)
+      // slot s0 + b holds deltas b*H + h of the group, lane group h each.
+      // The window is kept rotated so that lane q holds the group's delta q
+      // (shifted down by kGroup after each group): the shuffles below take
+      // immediate lane indices (H = 1) and the values need no shuffle at all.
       uint32_t cwb[B];
-      const uint32_t wl = (iq & 31) + hl;
 #pragma unroll
-      for (int b = 0; b < B; ++b) cwb[b] = __shfl_sync(kFull, win.c, wl + uint32_t(b) * H);
+      for (int b = 0; b < B; ++b) cwb[b] = __shfl_sync(kFull, win.c, uint32_t(b) * H + hl);
       // the deltas' signed values (the reference's values[k], kernels.cpp:33):
-      // lane q < kGroup fetches delta q = b * H + h of the group and stores it
-      // at val[h * D + s0 + b], so the consumer reads a group's B values of
-      // its lane group with one or two broadcast LDS
+      // lane q < kGroup stores its delta q = b * H + h at val[h * D + s0 + b],
+      // so the consumer reads a group's B values of its lane group with one or
+      // two broadcast LDS
       {
         const uint32_t q = uint32_t(lane);
         float val;
-        if constexpr (SC != 0) {
-          val = __shfl_sync(kFull, win.v, (iq + q) & 31);
-        } else {
-          const uint32_t cv = __shfl_sync(kFull, win.c, (iq + q) & 31);
-          val = __int_as_float(0x3F800000u | (cv & 0x80000000u));
-        }
+        if constexpr (SC != 0) val = win.v;
+        else val = __int_as_float(0x3F800000u | (win.c & 0x80000000u));
         if (q < kGroup) sm.val[(q % H) * D + s0 + q / H] = q < n ? val : 0.0f;
       }
       if (ifull) {  // straight-line copies: one size for all segments, immediate
@@ -567,7 +563,8 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
 #pragma unroll
         for (int b = 0; b < B; ++b) {
           // past the ticket's end the word is another delta of this window or
-          // 0 (fetch): a valid row either way, and nothing is read (size 0)
+          // 0 (fetch, or a lane the rotation left in place): a valid row either
+          // way, and nothing is read (size 0)
           const bool on = uint32_t(b) * H + hl < n;
           const uint32_t c = cwb[b] & 0x7FFFFFFFu;
           const float* src = reinterpret_cast<const float*>(ixb + (uint64_t)c * p.ldxb);
@@ -601,6 +598,9 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
       } else if ((iq & 31) == 0) {  // next 32-delta block of a long ticket
         win = wlong;
         wlong = fetch(ibeg + iq + 32, ibeg + ilen);
+      } else {  // rotate: the next group's deltas to lanes 0 .. kGroup-1
+        win.c = __shfl_down_sync(kFull, win.c, kGroup);
+        if constexpr (SC != 0) win.v = __shfl_down_sync(kFull, win.v, kGroup);
       }
       cp_commit();  // only real groups are committed: group k is the consumer's k-th
       ++icommit;
