@@ -462,3 +462,24 @@ def test_binary_relu_epilogue(tile, faithful, dev):
     y = h.spmm(torch.from_numpy(x).to(dev), relu=True)
     torch.cuda.synchronize()
     assert_bitwise(y.cpu().numpy(), want, f"binary relu tile={tile} faithful={faithful}")
+
+
+@pytest.mark.parametrize("faithful", [False, True])
+@pytest.mark.parametrize("normalized", [False, True])
+def test_hub_heavy_clique_overlay(normalized, faithful, dev):
+    """cfg[2]-shaped (Zipf clique overlay) at 1/40 scale: hub rows of thousands
+    of deltas walk many 32-delta index windows (rotated per ring group; in the
+    order-faithful mode unsplit), at every kernel variant's width."""
+    a = P.generate_graph("clique_overlay", [6000, 30000, 2, 10, 1.1], 0xC0F60000 + 77)
+    c = (P.build_cbm_normalized if normalized else P.build_cbm)(a, 8)
+    assert np.diff(c.row_ptr).max() > 256
+    arrays = oracle_arrays(c)
+    for d in (1, 48, 64, 128, 200, 256, 512):
+        kind = "int" if not normalized else "normal"
+        x = P.generate_dense(kind, a.n_cols, d, 0xC0F61000 + d, -8, 8)
+        want = O.oracle_spmm(arrays, x)
+        got, _ = gpu_spmm(c, x, dev, order_faithful=faithful)
+        if faithful or not normalized:
+            assert_bitwise(got, want, f"clique overlay d={d} faithful={faithful}")
+        else:
+            assert normwise_err(got, want) <= TOL, d
