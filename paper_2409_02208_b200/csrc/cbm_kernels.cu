@@ -373,13 +373,13 @@ constexpr int kWarpsPerCta = 4;
 #ifndef CBM_RECWIN_U4
 #define CBM_RECWIN_U4 64
 #endif
-// 4-segment kernels: 5 CTAs per SM (<= 96 registers; shared memory allows 5 at
-// 45.5 KB per CTA). Unbounded, the normalized variants took 97 registers and
-// dropped to 4 CTAs (16 warps) per SM.
-#ifndef CBM_MINB_U4
-#define CBM_MINB_U4 5
+// 5 CTAs per SM (<= 96 registers): shared memory allows 5 at 45.5 KB per CTA.
+// Unbounded, the 4-segment normalized variants took 97 registers and the
+// one-segment ones 110, both dropping to 4 CTAs (16 warps) per SM.
+#ifndef CBM_MINB
+#define CBM_MINB 5
 #endif
-#define CBM_LAUNCH_BOUNDS(U) __launch_bounds__(kWarpsPerCta * 32, (U) == 4 ? CBM_MINB_U4 : 1)
+#define CBM_LAUNCH_BOUNDS(U) __launch_bounds__(kWarpsPerCta * 32, CBM_MINB)
 #ifndef CBM_RECWIN_U2
 #define CBM_RECWIN_U2 64
 #endif
