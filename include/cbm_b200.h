@@ -161,8 +161,9 @@ void cbm_b200_free(cbm_b200_matrix* h);
 /* Y = A X on device memory (spmm_into, kernels.hpp:36-39, kernels.cpp:105-123).
  * X is x_rows x x_cols row-major with leading dimension ldx (floats); Y is
  * y_rows x y_cols with leading dimension ldy; Y is fully overwritten. A column
- * slab of a wider matrix is passed as (base + c0, ldx = full width). Async on
- * `stream` (a cudaStream_t; NULL = legacy default stream). */
+ * slab of a wider matrix is passed as (base + c0, ldx = full width); ldx must
+ * be below 2^30 (EINVAL otherwise). Async on `stream` (a cudaStream_t; NULL =
+ * legacy default stream). */
 int cbm_b200_spmm(cbm_b200_matrix* h, const float* x, int64_t x_rows, int64_t x_cols,
                   int64_t ldx, float* y, int64_t y_rows, int64_t y_cols, int64_t ldy,
                   void* stream);
