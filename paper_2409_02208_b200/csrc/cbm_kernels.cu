@@ -391,11 +391,11 @@ constexpr uint32_t rec_window() {
   return U == 4 ? CBM_RECWIN_U4 : (U == 2 ? CBM_RECWIN_U2 : CBM_RECWIN_U1);
 }
 
-template <int V, int U, int D>
+template <int V, int U, int D, int H = 1>
 struct alignas(16) WarpSmem {
   float ring[D][U][32 * V];      // slot s, segment u, lane l: [s][u][l*V, l*V+V)
   TRec rec[rec_window<U>()];     // warp-sequence tickets [g, g+RW), slot i & (RW-1)
-  float val[32];                 // signed delta values: lane group h, slot s at [h*D + s]
+  float val[D * H > 32 ? D * H : 32];  // signed delta values: lane group h, slot s at [h*D + s]
 };
 
 // Stage the records of warp-sequence tickets [i0, i0+RW/2) into a window of
@@ -429,7 +429,6 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
   using W = Vec<V>;
   using T4 = typename W::T;
   static_assert(H == 1 || (U == 1 && SC != 1), "lane groups: one segment, default mode");
-  static_assert(D * H <= 32, "one value-ring lane per (slot, lane group)");
   constexpr uint32_t kLanes = 32u / H;    // lanes per delta
   constexpr uint32_t kSeg = kLanes * V;   // floats of one segment (one LDGSTS per lane)
   constexpr uint32_t kSlab = kSeg * U;    // floats per ticket
@@ -437,7 +436,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
   // deltas per ring group: copies are issued, committed and awaited B at a
   // time (a group never spans two tickets; its unused slots stay idle)
-  constexpr int B = H == 4 ? 4 : (H == 2 ? CBM_B_H2 : (U == 4 ? CBM_B_U4 : (U == 2 ? CBM_B_U2 : CBM_B_U1)));
+  constexpr int B = H >= 8 ? 32 / H : (H == 4 ? 4 : (H == 2 ? CBM_B_H2 : (U == 4 ? CBM_B_U4 : (U == 2 ? CBM_B_U2 : CBM_B_U1))));
   static_assert(D % B == 0, "whole ring groups");
   constexpr int G = D / B;  // groups in flight
   constexpr uint32_t kGroup = uint32_t(B) * H;  // deltas per ring group
@@ -448,7 +447,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
   constexpr uint32_t kHalf = RW / 2;
   const uint32_t hl = uint32_t(lane) / kLanes;          // lane group
   const uint32_t jv = (uint32_t(lane) % kLanes) * V;    // column offset in a segment
-  using SM = WarpSmem<V, U, D>;
+  using SM = WarpSmem<V, U, D, H>;
   SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
   // warp -> position in the round-robin: CTAs b, b+G, b+2G, ... (G = p.cta_stride,
   // one per SM) share an SM, so consecutive tickets (adjacent rows, similar
@@ -940,7 +939,7 @@ template <int V, int U, int D, bool NORM, int SC, int H = 1>
 void launch_one(Params& p, uint64_t tickets, uint32_t slabs, DeviceMatrix* h, cudaStream_t s) {
   static DeviceSlots slots;  // per template instance and device
   launch_coop(reinterpret_cast<const void*>(&cbm_kernel<V, U, D, NORM, SC, H>),
-              kWarpsPerCta * sizeof(WarpSmem<V, U, D>), slots, p, tickets, slabs, h, s);
+              kWarpsPerCta * sizeof(WarpSmem<V, U, D, H>), slots, p, tickets, slabs, h, s);
 }
 
 template <bool NORM, int SC>
@@ -960,10 +959,12 @@ void run_kernel(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl
 }
 
 // Narrow X in the default mode: H deltas per warp instruction (V = 4, U = 1).
+// H = 8 / 16 (d <= 16 / 8, e.g. the slabs of 4-8 column-sharded ranks): a
+// ring group is a whole 32-delta window (B = 32 / H), two groups in flight.
 template <int H>
 void run_groups(Params& p, uint64_t tickets, uint32_t slabs, bool norm, bool scl,
                 DeviceMatrix* h, cudaStream_t s) {
-  constexpr int D = H == 2 ? CBM_D_H2 : 8;
+  constexpr int D = H == 2 ? CBM_D_H2 : (H == 16 ? 4 : 8);
   if (!norm) launch_one<4, 1, D, false, 0, H>(p, tickets, slabs, h, s);
   else if (!scl) launch_one<4, 1, D, true, 0, H>(p, tickets, slabs, h, s);
   else launch_one<4, 1, D, true, 2, H>(p, tickets, slabs, h, s);
@@ -1039,7 +1040,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   if (!L.order_faithful && h->opt.kernel == 0 && d >= 4 && d <= 64 && d % 4 == 0 &&
       ldin % 4 == 0 && ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(xin) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(y) & 15) == 0)
-    H = d <= 32 ? 4 : 2;
+    H = d <= 8 ? 16 : (d <= 16 ? 8 : (d <= 32 ? 4 : 2));
 #endif
   const uint32_t lanes_v = (H > 1 ? 4u : V) * (32 / H) * (H > 1 ? 1u : U);  // floats per slab
   const uint32_t n_slabs = (d + lanes_v - 1) / lanes_v;
@@ -1094,7 +1095,9 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   p.ldxb = uint32_t(ldin) * 4u;  // ldin < 2^30 (checked at the C ABI)
   if (H > 1) {
     if (H == 2) run_groups<2>(p, tickets, n_slabs, norm, scl, h, s);
-    else run_groups<4>(p, tickets, n_slabs, norm, scl, h, s);
+    else if (H == 4) run_groups<4>(p, tickets, n_slabs, norm, scl, h, s);
+    else if (H == 8) run_groups<8>(p, tickets, n_slabs, norm, scl, h, s);
+    else run_groups<16>(p, tickets, n_slabs, norm, scl, h, s);
   } else if (d == 1) {  // spmv: lanes over deltas
     if (!norm) launch_spmv<false, 0>(p, tickets, h, s);
     else if (!scl) launch_spmv<true, 0>(p, tickets, h, s);

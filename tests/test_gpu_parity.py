@@ -428,14 +428,14 @@ def test_long_runs_of_empty_tickets(sprinkle, dev):
 
 @pytest.mark.parametrize("normalized", [False, True])
 def test_lane_groups_narrow_operands(normalized, dev):
-    """Default mode, 4 <= d <= 64: 2 or 4 deltas per warp instruction, each
+    """Default mode, 4 <= d <= 64: 2, 4, 8 or 16 deltas per warp instruction, each
     lane group summing every H-th delta, combined by a fixed shuffle tree.
     Integer X on the binary matrix stays bit-exact; otherwise 1e-5 normwise;
     long rows chunked and parent chains included."""
     a = P.generate_graph("community", [2500, 100, 0.4, 0.004], 141)
     c = (P.build_cbm_normalized if normalized else P.build_cbm)(a, 0)
     arrays = oracle_arrays(c)
-    for d in (4, 8, 20, 32, 36, 64):
+    for d in (4, 8, 12, 16, 20, 32, 36, 64):  # H = 16, 16, 8, 8, 4, 4, 2, 2
         for kind in ("int", "normal"):
             x = P.generate_dense(kind, 2500, d, 142 + d, -8, 8)
             want = O.oracle_spmm(arrays, x)
