@@ -75,7 +75,10 @@ def main():
     for r in range(rounds):
         for name in names:
             for lib in ("libcbm_b200.so", alt):
-                env = dict(os.environ, CBM_B200_LIB=lib)
+                env = dict(os.environ, CBM_B200_LIB=lib.split(":")[0])
+                if lib != "libcbm_b200.so" and os.environ.get("AB_ALT_ENV"):  # K=V for the B arm
+                    k, v = os.environ["AB_ALT_ENV"].split("=", 1)
+                    env[k] = v
                 out = subprocess.run([sys.executable, __file__, "--one", name, str(d)], env=env,
                                      capture_output=True, text=True, check=True).stdout.strip()
                 res.setdefault((name, lib), []).append(float(out))
