@@ -30,6 +30,74 @@ def row_block(n: int, world: int, rank: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
+def _gather_rows(ptr, data, rows):
+    """Concatenated data[ptr[r]:ptr[r+1]] for r in rows (vectorised)."""
+    import numpy as np
+    ptr = np.asarray(ptr, np.int64)
+    starts = ptr[rows]
+    lens = ptr[rows + 1] - starts
+    total = int(lens.sum())
+    if total == 0:
+        return data[:0]
+    base = np.repeat(starts - (np.cumsum(lens) - lens), lens)
+    return data[base + np.arange(total)]
+
+
+def row_partition(a, c, parts: int):
+    """Row groups of a 2-D (row group x column slab) partition of a BINARY CBM
+    (DESIGN.md §7): contiguous row ranges balanced by delta count. A row whose
+    parent lies in another range is flattened (its deltas become its row of A
+    with a virtual parent, as the tiled path does for cut trees), so a group
+    never waits on another and no collective is needed. Returns
+    [(global row ids, sub-CBM of those rows x all columns)], one per group;
+    Y[rows_g] = sub_g . X. Integer-valued X gives the exact sums of the full
+    multiply; otherwise the flattened rows sum in a different order (within
+    the default mode's tolerance).
+
+    A normalized CBM cannot be cut this way: its delta values are +-row_scale
+    of the COLUMN and the container ties row_scale to square matrices
+    (io.cpp:369-380), so a row subset is not a valid CbmMatrix."""
+    import numpy as np
+    from . import VIRTUAL_PARENT, CbmMatrix
+    if c.is_normalized:
+        raise ValueError("row_partition: binary CBMs only")
+    if parts < 1:
+        raise ValueError("row_partition: parts must be >= 1")
+    if a.n_rows != c.n_rows or a.n_cols != c.n_cols:
+        raise ValueError("row_partition: A and its CBM differ in shape")
+    m = c.n_rows
+    clen = np.diff(c.row_ptr.astype(np.int64))
+    cum = np.cumsum(clen)
+    total = int(cum[-1]) if m else 0
+    cuts = [0] + [int(np.searchsorted(cum, total * k / parts, side="left")) + 1
+                  for k in range(1, parts)] + [m]
+    cuts = np.maximum.accumulate(np.minimum(np.asarray(cuts), m))
+    out = []
+    par_all = c.parent.astype(np.int64)
+    for g in range(parts):
+        lo, hi = int(cuts[g]), int(cuts[g + 1])
+        rows = np.arange(lo, hi, dtype=np.int64)
+        par = par_all[lo:hi]
+        virt = par == VIRTUAL_PARENT
+        inside = ~virt & (par >= lo) & (par < hi)
+        flat = ~virt & ~inside
+        parent = np.where(inside, par - lo, VIRTUAL_PARENT).astype(np.uint32)
+        alen = np.diff(a.row_ptr.astype(np.int64))[lo:hi]
+        lens = np.where(flat, alen, clen[lo:hi])
+        row_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+        row_of = np.repeat(np.arange(hi - lo), lens)
+        fpos = flat[row_of]
+        col_idx = np.empty(int(row_ptr[-1]), np.uint32)
+        values = np.empty(int(row_ptr[-1]), np.float32)
+        col_idx[fpos] = _gather_rows(a.row_ptr, a.col_idx, rows[flat])
+        values[fpos] = 1.0
+        col_idx[~fpos] = _gather_rows(c.row_ptr, c.col_idx, rows[~flat])
+        values[~fpos] = _gather_rows(c.row_ptr, c.values, rows[~flat])
+        out.append((rows, CbmMatrix(hi - lo, c.n_cols, c.alpha, False, parent, row_ptr, col_idx,
+                                    values)))
+    return out
+
+
 class _DeviceCompute:
     """The product's compute for one rank: the reference-exact GEMM and the
     CBM multiply (ReLU fused into the epilogue) on this rank's GPU."""

@@ -161,3 +161,39 @@ def test_gloo_world2_sharded_gcn_bitwise(fused):
     want = O.oracle_gcn_forward(oracle_arrays(c), x, w0, w1)
     for r in range(2):
         assert np.array_equal(results[r].view(np.uint32), want.view(np.uint32)), r
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 7])
+def test_row_partition_reassembles_exactly(parts):
+    """2-D partition row groups (sharding.row_partition): every group's
+    sub-CBM is a valid container, groups cover the rows once, flattened rows
+    keep their exact integer sums, and Y[rows_g] = sub_g . X reassembles the
+    full multiply (oracle on each group, integer X: exact in any order)."""
+    from paper_2409_02208_b200.sharding import row_partition
+    a = P.generate_graph("clique_overlay", [1500, 6000, 2, 8, 1.1], 0xC0F60000 + 91)
+    c = P.build_cbm(a, 4)
+    x = P.generate_dense("int", a.n_cols, 20, 0xC0F61000 + 91, -8, 8)
+    want = O.oracle_spmm(oracle_arrays(c), x)
+    groups = row_partition(a, c, parts)
+    assert len(groups) == parts
+    seen = np.concatenate([rows for rows, _ in groups])
+    assert np.array_equal(seen, np.arange(c.n_rows))
+    got = np.empty_like(want)
+    for rows, sub in groups:
+        assert sub.n_rows == len(rows) and sub.n_cols == c.n_cols
+        par = sub.parent[sub.parent != P.VIRTUAL_PARENT]
+        assert np.all(par < sub.n_rows)  # parents inside the group
+        got[rows] = O.oracle_spmm(oracle_arrays(sub), x)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    # the cut balances the CBM's deltas (up to one row's worth); flattened rows
+    # then add their A rows on top
+    clen = np.diff(c.row_ptr.astype(np.int64))
+    for rows, _ in groups:
+        assert clen[rows].sum() <= c.nnz / parts + clen.max() + 1
+
+
+def test_row_partition_rejects_normalized():
+    from paper_2409_02208_b200.sharding import row_partition
+    a = P.generate_graph("community", [200, 20, 0.5, 0.01], 5)
+    with pytest.raises(ValueError, match="binary CBMs only"):
+        row_partition(a, P.build_cbm_normalized(a, 0), 2)

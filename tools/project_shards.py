@@ -9,6 +9,10 @@ reports the N-GPU whole-job throughput that follows: 2*nnz*d / max_r t_r.
 It is a per-rank measurement, not an N-GPU run: it assumes the ranks do not
 slow each other down, which holds when nothing crosses NVLink.
 
+Binary workloads also get the 2-D partition (sharding.row_partition): N =
+R row groups x C column slabs, each rank timed on its group's sub-CBM at its
+slab width; the best (R, C) per N is reported beside the column-only split.
+
 Usage: python tools/project_shards.py cfg1            (the bench workload)
        python tools/project_shards.py cfg4            (2.45M rows, d = 64/128/256,
                                                        binary and normalized; slow build)
@@ -65,6 +69,50 @@ def sweep(name, a, c, normalized, ds, flush, dev):
                   flush=True)
 
 
+def sweep2d(name, a, c, ds, flush, dev):
+    """N = R x C ranks: row group g of R (sharding.row_partition) x column slab
+    of C; every rank's (sub-CBM, slab width) timed; N-GPU step = max."""
+    from paper_2409_02208_b200.sharding import row_partition
+    nnz = a.nnz
+    groups = {R: [(rows, P.DeviceCbm(sub)) for rows, sub in row_partition(a, c, R)]
+              for R in (2, 4, 8)}
+    for d in ds:
+        x_full = P.generate_dense("normal", a.n_cols, d, 0xC0F61000 + 4)
+        base = None
+        cache = {}
+        for world in (1, 2, 4, 8):
+            best = None
+            for R in (1, 2, 4, 8):
+                if world % R:
+                    continue
+                C = world // R
+                widths = sorted({hi - lo for lo, hi in all_slabs(d, C)}, reverse=True)
+                t_max = 0.0
+                for w in widths:
+                    x = torch.from_numpy(np.ascontiguousarray(x_full[:, :w])).to(dev)
+                    ops = [(None, P.DeviceCbm(c))] if R == 1 else groups[R]
+                    for gi, (rows, op) in enumerate(ops):
+                        key = (R, gi, w)
+                        if key not in cache:
+                            n_out = c.n_rows if rows is None else len(rows)
+                            y = torch.empty((n_out, w), device=dev)
+                            cache[key] = timeit(op, x, y, flush)
+                            del y
+                        t_max = max(t_max, cache[key])
+                    del x
+                if best is None or t_max < best[0]:
+                    best = (t_max, R, C, widths)
+            t_max, R, C, widths = best
+            value = 2.0 * nnz * d / (t_max * 1e-3) / 1e9
+            base = base or value
+            print(json.dumps({"workload": name, "normalized": False, "d": d, "n_gpus": world,
+                              "partition": f"{R} row groups x {C} column slabs",
+                              "slab_widths": widths, "ms_max_rank": t_max,
+                              "projected_gflops": value, "speedup_vs_1": value / base,
+                              "note": "2-D partition; per-rank work timed on one B200; "
+                                      "N-GPU step = max over ranks"}), flush=True)
+
+
 def main():
     dev = torch.device("cuda:0")
     flush = torch.empty(64 << 20, device=dev)
@@ -75,13 +123,22 @@ def main():
         a = wl.graph()
         for normalized in (False, True):
             c = (P.build_cbm_normalized if normalized else P.build_cbm)(a, wl.alpha, threads)
-            sweep("cfg4", a, c, normalized, (64, 128, 256), flush, dev)
+            if "--2d" in sys.argv:
+                if not normalized:
+                    sweep2d("cfg4", a, c, (64, 128, 256), flush, dev)
+            else:
+                sweep("cfg4", a, c, normalized, (64, 128, 256), flush, dev)
             del c
+            if "--2d" in sys.argv:
+                break
     else:
         wl = WORKLOADS[which]
         a = wl.graph()
         c = wl.build(a, threads)
-        sweep(which, a, c, wl.normalized, (wl.d,), flush, dev)
+        if "--2d" in sys.argv:
+            sweep2d(which, a, c, (wl.d,), flush, dev)
+        else:
+            sweep(which, a, c, wl.normalized, (wl.d,), flush, dev)
 
 
 if __name__ == "__main__":
