@@ -76,6 +76,7 @@ def sweep2d(name, a, c, ds, flush, dev):
     nnz = a.nnz
     groups = {R: [(rows, P.DeviceCbm(sub)) for rows, sub in row_partition(a, c, R)]
               for R in (2, 4, 8)}
+    groups[1] = [(None, P.DeviceCbm(c))]
     for d in ds:
         x_full = P.generate_dense("normal", a.n_cols, d, 0xC0F61000 + 4)
         base = None
@@ -90,7 +91,7 @@ def sweep2d(name, a, c, ds, flush, dev):
                 t_max = 0.0
                 for w in widths:
                     x = torch.from_numpy(np.ascontiguousarray(x_full[:, :w])).to(dev)
-                    ops = [(None, P.DeviceCbm(c))] if R == 1 else groups[R]
+                    ops = groups[R]
                     for gi, (rows, op) in enumerate(ops):
                         key = (R, gi, w)
                         if key not in cache:
