@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-csr-comparator", action="store_true",
                     help="skip timing the uncompressed (CSR) matrix with the same kernel")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
+    ap.add_argument("--row-groups", type=int, default=1,
+                    help="2-D partition (binary workloads): N = row groups x column slabs, "
+                         "rank r owns Y[rows of group r // C, slab r % C] (DESIGN.md §7)")
     return ap.parse_args()
 
 
@@ -225,21 +228,30 @@ def run_ours(args, wl):
     t0 = time.perf_counter()
     c = wl.build(a, args.threads)
     t_build = time.perf_counter() - t0
+    from paper_2409_02208_b200.sharding import column_slab, grid_position, row_partition
+    group, slab_rank, n_slabs = grid_position(world, rank, args.row_groups)
+    c_local, n_out = c, a.n_rows
+    if args.row_groups > 1:
+        # this rank's row group (cross-group parents flattened); host-side
+        # construction, outside every timed region like the build itself
+        t0 = time.perf_counter()
+        rows_g, c_local = row_partition(a, c, args.row_groups)[group]
+        n_out = len(rows_g)
+        t_build += time.perf_counter() - t0
     t0 = time.perf_counter()
-    op = P.DeviceCbm(c, device=local, order_faithful=args.order_faithful, kernel=args.kernel,
-                     tile=args.tile)
+    op = P.DeviceCbm(c_local, device=local, order_faithful=args.order_faithful,
+                     kernel=args.kernel, tile=args.tile)
     torch.cuda.synchronize()
     t_upload = time.perf_counter() - t0
     info = op.info()
 
-    from paper_2409_02208_b200.sharding import column_slab
-    lo, hi = column_slab(wl.d, world, rank)
+    lo, hi = column_slab(wl.d, n_slabs, slab_rank)
     d_local = hi - lo
     x_full = wl.operand(a.n_cols)
     x_host = torch.from_numpy(np.ascontiguousarray(x_full[:, lo:hi])).pin_memory()
     del x_full
     x = x_host.to(dev)
-    y = torch.empty((a.n_rows, d_local), dtype=torch.float32, device=dev)
+    y = torch.empty((n_out, d_local), dtype=torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     op.reserve(max(1, d_local))
     stream = torch.cuda.current_stream()
@@ -272,12 +284,12 @@ def run_ours(args, wl):
         launches = op.info()["launches_per_call"] * args.steps if d_local else 0
 
         # e2e: C-ABI host-buffer entry point, pinned host memory
-        y_host = torch.empty((a.n_rows, d_local), dtype=torch.float32).pin_memory()
+        y_host = torch.empty((n_out, d_local), dtype=torch.float32).pin_memory()
         e2e_steps = max(3, min(args.steps, 50))
         for _ in range(2):
             if d_local:
                 op.spmm_host_ptr(x_host.data_ptr(), a.n_cols, d_local, y_host.data_ptr(),
-                                 a.n_rows, d_local, stream)
+                                 n_out, d_local, stream)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
@@ -287,7 +299,7 @@ def run_ours(args, wl):
         for _ in range(e2e_steps):
             if d_local:
                 op.spmm_host_ptr(x_host.data_ptr(), a.n_cols, d_local, y_host.data_ptr(),
-                                 a.n_rows, d_local, stream)
+                                 n_out, d_local, stream)
         ee.record(stream)
         torch.cuda.synchronize()
         e2e_ms = es.elapsed_time(ee) / e2e_steps
@@ -309,7 +321,7 @@ def run_ours(args, wl):
     # With pre-scaling (normalized, dense rows) two kernels run; the step is
     # then attributed to the pair (documented in DESIGN.md).
     peak, peak_src = peaks()
-    b_alg_local = b_alg_bytes(info["nnz_delta"], a.n_rows, a.n_cols, d_local, wl.normalized)
+    b_alg_local = b_alg_bytes(info["nnz_delta"], n_out, a.n_cols, d_local, wl.normalized)
     achieved = b_alg_local / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
     tiled = bool(info["tile_active"]) and d_local >= 32
     if tiled:
@@ -340,7 +352,7 @@ def run_ours(args, wl):
             "note": "staged deltas read the shared-memory X tile (128 B/clk/SM LSU limit)"}
 
     gpu_csr = None
-    if not args.no_csr_comparator:
+    if not args.no_csr_comparator and args.row_groups == 1:
         # same kernel on the uncompressed matrix: the paper's runtime reduction
         # (t_csr - t_cbm) / t_csr, both on this B200
         csr_op = P.DeviceCbm(P.csr_operator(a, wl.normalized), device=local)
@@ -371,7 +383,7 @@ def run_ours(args, wl):
     spmv = None
     if rank == 0:
         v = torch.from_numpy(wl.operand(a.n_cols, 1)).to(dev)
-        u = torch.empty((a.n_rows, 1), dtype=torch.float32, device=dev)
+        u = torch.empty((n_out, 1), dtype=torch.float32, device=dev)
         op.reserve(1)
         for _ in range(3):
             op.spmv_into(v, u, stream)
@@ -403,12 +415,13 @@ def run_ours(args, wl):
            "config": {"workload": wl.name, "note": wl.note, "n": a.n_rows, "nnz": nnz,
                       "nnz_delta": info["nnz_delta"], "d": wl.d, "d_per_rank": d_local,
                       "alpha": wl.alpha, "normalized": wl.normalized,
-                      "parallelism": f"column-shard x{world}",
+                      "parallelism": (f"column-shard x{world}" if args.row_groups == 1 else
+                                      f"{args.row_groups} row groups x {n_slabs} column slabs"),
                       "order_faithful": bool(args.order_faithful), "kernel": args.kernel,
                       "tile": args.tile,
                       "l2": "flushed (256 MiB write) before every timed step",
                       "levels": info["n_levels"], "chunk_items": info["n_chunk_items"],
-                      "actual_ops_per_step": int(sum(P.count_scalar_ops(c)) * d_local),
+                      "actual_ops_per_step": int(sum(P.count_scalar_ops(c_local)) * d_local),
                       "build_s": t_build, "upload_s": t_upload},
            "roofline": roofline,
            "cpu_baseline": cpu,
@@ -416,7 +429,7 @@ def run_ours(args, wl):
            "spmv": spmv,
            "e2e": {"value": e2e_value, "unit": UNIT,
                    "h2d_bytes_per_step": int(a.n_cols * d_local * 4),
-                   "d2h_bytes_per_step": int(a.n_rows * d_local * 4),
+                   "d2h_bytes_per_step": int(n_out * d_local * 4),
                    "entry": "cbm_b200_spmm_host (C ABI, pinned host buffers)"},
            "gpu_launches": int(launches),
            "clocks": sampler.summary()}

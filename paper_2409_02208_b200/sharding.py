@@ -212,3 +212,18 @@ def gcn_forward_sharded(op, x, w0, w1, group=None, compute=None, fused=False):
     clo, chi = cslabs[rank]
     o = cm.matmul(z_full, w1[:, clo:chi].contiguous())
     return _gather_columns(o, cslabs, rank, group)
+
+
+def grid_position(world: int, rank: int, row_groups: int) -> tuple[int, int, int]:
+    """Rank -> (row group, column-slab rank, column slabs) of the 2-D
+    partition N = row_groups x (N / row_groups), row-group major: ranks
+    g*C .. g*C+C-1 share row group g (sharding.row_partition) and split its
+    columns with column_slab(d, C, .). row_groups = 1 is the column-only
+    split. Like the column split it needs no collective: each rank owns the
+    block Y[rows_g, slab]."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("grid_position: bad rank/world")
+    if row_groups < 1 or world % row_groups:
+        raise ValueError("grid_position: row_groups must divide world")
+    slabs = world // row_groups
+    return rank // slabs, rank % slabs, slabs

@@ -483,3 +483,23 @@ def test_hub_heavy_clique_overlay(normalized, faithful, dev):
             assert_bitwise(got, want, f"clique overlay d={d} faithful={faithful}")
         else:
             assert normwise_err(got, want) <= TOL, d
+
+
+@pytest.mark.parametrize("tile", [0, -1])
+def test_2d_partition_blocks_on_device(tile, dev):
+    """bench.py --row-groups: every (row group, column slab) block multiplied
+    on the device from its own sub-CBM (sharding.row_partition, cross-group
+    parents flattened) reassembles the full 1-GPU multiply exactly (integer X,
+    exact in any summation order)."""
+    from paper_2409_02208_b200.sharding import all_slabs, row_partition
+    a = P.generate_graph("clique_overlay", [6000, 30000, 2, 10, 1.1], 0xC0F60000 + 93)
+    c = P.build_cbm(a, 4)
+    x = P.generate_dense("int", a.n_cols, 96, 0xC0F61000 + 93, -8, 8)
+    want = O.oracle_spmm(oracle_arrays(c), x)
+    for groups in (2, 4):
+        got = np.full_like(want, np.nan)
+        for rows, sub in row_partition(a, c, groups):
+            for lo, hi in all_slabs(96, 2):
+                y, _ = gpu_spmm(sub, x[:, lo:hi], dev, tile=tile)
+                got[rows, lo:hi] = y
+        assert_bitwise(got, want, f"{groups} row groups")

@@ -197,3 +197,58 @@ def test_row_partition_rejects_normalized():
     a = P.generate_graph("community", [200, 20, 0.5, 0.01], 5)
     with pytest.raises(ValueError, match="binary CBMs only"):
         row_partition(a, P.build_cbm_normalized(a, 0), 2)
+
+
+@pytest.mark.parametrize("world,row_groups", [(4, 1), (4, 2), (4, 4), (6, 3)])
+def test_grid_position_covers_every_block_once(world, row_groups):
+    from paper_2409_02208_b200.sharding import grid_position
+    pos = [grid_position(world, r, row_groups) for r in range(world)]
+    assert sorted((g, s) for g, s, _ in pos) == [(g, s) for g in range(row_groups)
+                                                for s in range(world // row_groups)]
+    assert all(n == world // row_groups for _, _, n in pos)
+    with pytest.raises(ValueError):
+        grid_position(4, 0, 3)
+
+
+def _grid_worker(rank, world, row_groups, port, out):
+    from paper_2409_02208_b200.sharding import grid_position, row_partition
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = P.generate_graph("clique_overlay", [1500, 6000, 2, 8, 1.1], 0xC0F60000 + 92)
+    c = P.build_cbm(a, 2)
+    x = P.generate_dense("int", a.n_cols, 40, 0xC0F61000 + 92, -8, 8)
+    g, s, n_slabs = grid_position(world, rank, row_groups)
+    rows, sub = row_partition(a, c, row_groups)[g]
+    lo, hi = column_slab(40, n_slabs, s)
+    blk = O.oracle_spmm(oracle_arrays(sub), np.ascontiguousarray(x[:, lo:hi]))
+    pieces = [None] * world
+    dist.all_gather_object(pieces, (rows, lo, hi, blk))
+    if rank == 0:
+        y = np.full((c.n_rows, 40), np.nan, np.float32)
+        for rows_, lo_, hi_, blk_ in pieces:
+            y[rows_, lo_:hi_] = blk_
+        out.put(y)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world4_2d_partition_reassembles_bitwise():
+    """bench.py --row-groups 2 at N = 4 (2 row groups x 2 column slabs), each
+    rank's block from the oracle on its sub-CBM and slab, gathered over gloo:
+    the blocks tile Y exactly once and equal the full multiply bit for bit
+    (integer X)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grid_worker, args=(r, 4, 2, port, q)) for r in range(4)]
+    for p_ in procs:
+        p_.start()
+    y = q.get(timeout=240)
+    for p_ in procs:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    a = P.generate_graph("clique_overlay", [1500, 6000, 2, 8, 1.1], 0xC0F60000 + 92)
+    c = P.build_cbm(a, 2)
+    x = P.generate_dense("int", a.n_cols, 40, 0xC0F61000 + 92, -8, 8)
+    want = O.oracle_spmm(oracle_arrays(c), x)
+    assert np.array_equal(y.view(np.uint32), want.view(np.uint32))
