@@ -53,9 +53,10 @@ def parse():
     ap.add_argument("--no-csr-comparator", action="store_true",
                     help="skip timing the uncompressed (CSR) matrix with the same kernel")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
-    ap.add_argument("--row-groups", type=int, default=1,
+    ap.add_argument("--row-groups", type=int, default=-1,
                     help="2-D partition (binary workloads): N = row groups x column slabs, "
-                         "rank r owns Y[rows of group r // C, slab r % C] (DESIGN.md §7)")
+                         "rank r owns Y[rows of group r // C, slab r % C] (DESIGN.md §7); "
+                         "-1 = auto (sharding.auto_row_groups), 1 = column slabs only")
     return ap.parse_args()
 
 
@@ -228,7 +229,10 @@ def run_ours(args, wl):
     t0 = time.perf_counter()
     c = wl.build(a, args.threads)
     t_build = time.perf_counter() - t0
-    from paper_2409_02208_b200.sharding import column_slab, grid_position, row_partition
+    from paper_2409_02208_b200.sharding import (auto_row_groups, column_slab, grid_position,
+                                                row_partition)
+    if args.row_groups < 0:
+        args.row_groups = 1 if wl.normalized else auto_row_groups(wl.d, world)
     group, slab_rank, n_slabs = grid_position(world, rank, args.row_groups)
     c_local, n_out = c, a.n_rows
     if args.row_groups > 1:

@@ -227,3 +227,16 @@ def grid_position(world: int, rank: int, row_groups: int) -> tuple[int, int, int
         raise ValueError("grid_position: row_groups must divide world")
     slabs = world // row_groups
     return rank // slabs, rank % slabs, slabs
+
+
+def auto_row_groups(d: int, world: int) -> int:
+    """Row groups for N ranks of a binary CBM: keep column slabs >= 128
+    wide (C = the largest divisor of N not above d / 128) and give the rest
+    of N to row groups. Chosen from the per-rank projection
+    (profiles/r01e_project_2d.jsonl): every rank walks its
+    group's whole structure whatever its width, so narrow slabs stop
+    scaling while row groups shrink the structure itself."""
+    if world < 1:
+        raise ValueError("auto_row_groups: world must be >= 1")
+    slabs = max(c for c in range(1, world + 1) if world % c == 0 and c <= max(1, d // 128))
+    return world // slabs

@@ -252,3 +252,12 @@ def test_gloo_world4_2d_partition_reassembles_bitwise():
     x = P.generate_dense("int", a.n_cols, 40, 0xC0F61000 + 92, -8, 8)
     want = O.oracle_spmm(oracle_arrays(c), x)
     assert np.array_equal(y.view(np.uint32), want.view(np.uint32))
+
+
+def test_auto_row_groups_matches_the_projection_choice():
+    """The (R, C) per N that profiles/r01e_project_2d.jsonl measured best."""
+    from paper_2409_02208_b200.sharding import auto_row_groups
+    assert [auto_row_groups(128, n) for n in (1, 2, 4, 8)] == [1, 2, 4, 8]
+    assert [auto_row_groups(64, n) for n in (1, 2, 4, 8)] == [1, 2, 4, 8]
+    assert [auto_row_groups(256, n) for n in (1, 2, 4, 8)] == [1, 1, 2, 4]
+    assert auto_row_groups(512, 6) == 2
