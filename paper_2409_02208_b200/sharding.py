@@ -43,9 +43,37 @@ def _gather_rows(ptr, data, rows):
     return data[base + np.arange(total)]
 
 
+def _balanced_cuts(cost, parts):
+    import numpy as np
+    m = len(cost)
+    cum = np.cumsum(cost)
+    total = int(cum[-1]) if m else 0
+    cuts = [0] + [int(np.searchsorted(cum, total * k / parts, side="left")) + 1
+                  for k in range(1, parts)] + [m]
+    return np.maximum.accumulate(np.minimum(np.asarray(cuts), m))
+
+
+def _group_cost(cuts, par, clen, alen):
+    """Per-row stored length under `cuts`: the deltas, or the A row when the
+    parent lies in another group (flattened)."""
+    import numpy as np
+    from . import VIRTUAL_PARENT
+    group = np.searchsorted(cuts, np.arange(len(par)), side="right") - 1
+    virt = par == VIRTUAL_PARENT
+    pg = np.searchsorted(cuts, np.where(virt, 0, par), side="right") - 1
+    return np.where(~virt & (pg != group), alen, clen)
+
+
+def _max_group(cost, cuts):
+    import numpy as np
+    cum = np.concatenate([[0], np.cumsum(cost)])
+    return int(np.max(cum[cuts[1:]] - cum[cuts[:-1]]))
+
+
 def row_partition(a, c, parts: int):
     """Row groups of a 2-D (row group x column slab) partition of a BINARY CBM
-    (DESIGN.md §7): contiguous row ranges balanced by delta count. A row whose
+    (DESIGN.md §7): contiguous row ranges balanced by stored length (delta
+    count, refined to count flattened rows at their A length). A row whose
     parent lies in another range is flattened (its deltas become its row of A
     with a virtual parent, as the tiled path does for cut trees), so a group
     never waits on another and no collective is needed. Returns
@@ -67,13 +95,19 @@ def row_partition(a, c, parts: int):
         raise ValueError("row_partition: A and its CBM differ in shape")
     m = c.n_rows
     clen = np.diff(c.row_ptr.astype(np.int64))
-    cum = np.cumsum(clen)
-    total = int(cum[-1]) if m else 0
-    cuts = [0] + [int(np.searchsorted(cum, total * k / parts, side="left")) + 1
-                  for k in range(1, parts)] + [m]
-    cuts = np.maximum.accumulate(np.minimum(np.asarray(cuts), m))
-    out = []
+    alen_all = np.diff(a.row_ptr.astype(np.int64))
     par_all = c.parent.astype(np.int64)
+    cuts = _balanced_cuts(clen, parts)
+    # refine: balance the lengths AFTER flattening (a flattened row costs its
+    # A row, not its deltas); keep whichever cut has the lightest heaviest group
+    best = (_max_group(_group_cost(cuts, par_all, clen, alen_all), cuts), cuts)
+    for _ in range(4):
+        cuts = _balanced_cuts(_group_cost(cuts, par_all, clen, alen_all), parts)
+        heavy = _max_group(_group_cost(cuts, par_all, clen, alen_all), cuts)
+        if heavy < best[0]:
+            best = (heavy, cuts)
+    cuts = best[1]
+    out = []
     for g in range(parts):
         lo, hi = int(cuts[g]), int(cuts[g + 1])
         rows = np.arange(lo, hi, dtype=np.int64)
@@ -82,7 +116,7 @@ def row_partition(a, c, parts: int):
         inside = ~virt & (par >= lo) & (par < hi)
         flat = ~virt & ~inside
         parent = np.where(inside, par - lo, VIRTUAL_PARENT).astype(np.uint32)
-        alen = np.diff(a.row_ptr.astype(np.int64))[lo:hi]
+        alen = alen_all[lo:hi]
         lens = np.where(flat, alen, clen[lo:hi])
         row_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
         row_of = np.repeat(np.arange(hi - lo), lens)
