@@ -102,13 +102,15 @@ def sweep2d(name, a, c, ds, flush, dev):
                         t_max = max(t_max, cache[key])
                     del x
                 if best is None or t_max < best[0]:
-                    best = (t_max, R, C, widths)
-            t_max, R, C, widths = best
+                    group_ms = [round(cache[(R, gi, widths[0])], 4) for gi in range(R)]
+                    best = (t_max, R, C, widths, group_ms)
+            t_max, R, C, widths, group_ms = best
             value = 2.0 * nnz * d / (t_max * 1e-3) / 1e9
             base = base or value
             print(json.dumps({"workload": name, "normalized": False, "d": d, "n_gpus": world,
                               "partition": f"{R} row groups x {C} column slabs",
                               "slab_widths": widths, "ms_max_rank": t_max,
+                              "group_ms_widest_slab": group_ms,
                               "projected_gflops": value, "speedup_vs_1": value / base,
                               "note": "2-D partition; per-rank work timed on one B200; "
                                       "N-GPU step = max over ranks"}), flush=True)
