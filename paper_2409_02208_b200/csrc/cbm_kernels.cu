@@ -1092,7 +1092,11 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   }
   p.faithful = L.order_faithful ? 1u : 0u;
   p.ldx32 = uint32_t(ldin);
-  p.ldxb = uint32_t(ldin) * 4u;  // ldin < 2^30 (checked at the C ABI)
+  // every caller (C ABI, host pipeline, GCN, prescale) lands here: the byte
+  // pitch of one gathered row must fit 32 bits
+  if (uint64_t(ldin) >= (uint64_t(1) << 30))
+    throw invalid_argument("spmm: leading dimension of X must be below 2^30");
+  p.ldxb = uint32_t(ldin) * 4u;
   if (H > 1) {
     if (H == 2) run_groups<2>(p, tickets, n_slabs, norm, scl, h, s);
     else if (H == 4) run_groups<4>(p, tickets, n_slabs, norm, scl, h, s);

@@ -57,7 +57,15 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
     }
     // tiled path (default mode): planned here, kept only when it pays
     if (!L.order_faithful && opt.tile != 0 && v.n_rows > 0) {
-      TileLayout T = plan_tiles(v, opt.tile_rows, opt.tile_stage, uint32_t(h->num_sms), gain);
+      TileLayout T;
+      bool planned = true;
+      try {
+        T = plan_tiles(v, opt.tile_rows, opt.tile_stage, uint32_t(h->num_sms), gain);
+      } catch (const inconsistent_rows&) {
+        if (opt.tile == 1) throw;  // forced: EINVAL; auto: the streaming kernel takes it
+        planned = false;
+      }
+      if (planned) {
       const double frac = T.n_deltas ? double(T.n_staged_deltas) / double(T.n_deltas) : 0.0;
       const double reuse = T.n_staged_cols ? double(T.n_staged_deltas) / double(T.n_staged_cols) : 0.0;
       // a row is summed by one warp and a block by one CTA: auto mode also
@@ -81,6 +89,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       T.block = {};
       T.stage = {};  // (T.work stays: it sizes the split of the last wave)
       h->tile = std::move(T);
+      }
     }
     int coop = 0;
     ck(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev), "attr");
@@ -111,6 +120,7 @@ void device_free(DeviceMatrix* h) {
     cudaStreamDestroy(h->s_in);
     cudaStreamDestroy(h->s_out);
     for (auto e : h->ev) cudaEventDestroy(e);
+    cudaEventDestroy(h->ev_done);
   }
   for (auto& kv : h->schedules) cudaFree(kv.second.trec);
   for (auto& kv : h->ws)
@@ -134,7 +144,11 @@ void device_reserve(DeviceMatrix* h, uint64_t d, void* stream) {
   auto& ws = h->ws[stream];
   if (uint64_t(L.n_items) * slabs > ws.flags_cap) {
     grow(ws.flags, ws.flags_cap, uint64_t(L.n_items) * slabs, "workspace flags");
-    ck(cudaMemset(ws.flags, 0, ws.flags_cap * sizeof(uint32_t)), "flags memset");
+    // on the stream the workspace serves (the kernel that spins on these flags
+    // runs there; a legacy-stream memset would not be ordered before it on a
+    // non-blocking or per-thread stream)
+    ck(cudaMemsetAsync(ws.flags, 0, ws.flags_cap * sizeof(uint32_t),
+                       static_cast<cudaStream_t>(stream)), "flags memset");
     ws.epoch = 0;
   }
   grow(ws.partial, ws.partial_cap, uint64_t(L.n_chunk_items) * dpad, "workspace partial");
@@ -160,6 +174,8 @@ void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, 
     ck(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking), "stream");
     for (auto& e : h->ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(h->ev_done, h->s_out), "event");
   }
   const uint64_t bytes = (uint64_t(L.n_cols) + L.n_rows) * d * sizeof(float);
   // Column chunks (16-byte aligned): the first chunk's H2D and the last
@@ -199,6 +215,11 @@ void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, 
   ck(cudaEventRecord(h->ev[0], s), "event");
   ck(cudaStreamWaitEvent(h->s_in, h->ev[0], 0), "wait");
   ck(cudaStreamWaitEvent(h->s_out, h->ev[0], 0), "wait");
+  // xstage/ystage are shared by every caller stream: the previous call's
+  // kernel has read xstage and its copy-out has drained ystage before this
+  // call's copy-in starts (the kernels below wait on the copy-in, so their
+  // ystage writes are ordered after it too)
+  ck(cudaStreamWaitEvent(h->s_in, h->ev_done, 0), "wait");
   for (size_t k = 0; k < parts.size(); ++k) {
     const auto [c0, w] = parts[k];
     ck(cudaMemcpy2DAsync(h->xstage + c0, dpad * sizeof(float), x + c0, ldx * sizeof(float),
@@ -220,8 +241,8 @@ void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, 
   }
   h->last_launches = launches;  // kernels launched by this call (one per chunk)
   // the caller's stream resumes after the last copy-out
-  ck(cudaEventRecord(h->ev[0], h->s_out), "event");
-  ck(cudaStreamWaitEvent(s, h->ev[0], 0), "wait");
+  ck(cudaEventRecord(h->ev_done, h->s_out), "event");
+  ck(cudaStreamWaitEvent(s, h->ev_done, 0), "wait");
   if (wait) device_spmm_host_wait(h, stream);
 }
 

@@ -66,6 +66,9 @@ struct DeviceMatrix {
   // host-API pipeline: copy-in / copy-out streams and chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev[1 + 2 * kHostChunks] = {};
+  // end of the last host call's copy-out: the shared staging buffers are free
+  // again (the next call's copy-in, whatever stream it comes from, waits on it)
+  cudaEvent_t ev_done = nullptr;
   // static ticket -> warp schedules (cbm_kernel), one per (warps, slabs)
   struct Schedule {
     void* trec = nullptr;    // ticket stream: per warp, its records in increasing order

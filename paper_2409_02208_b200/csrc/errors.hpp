@@ -10,6 +10,12 @@ namespace cbmb {
 struct invalid_argument : std::invalid_argument {  // std::invalid_argument in the reference
   using std::invalid_argument::invalid_argument;
 };
+// a delta row that removes a column its parent lacks or adds one it has: the
+// reference multiplies it (deltas + parent) but it has no full-row form, so
+// paths that flatten or cut rows step aside for it
+struct inconsistent_rows : invalid_argument {
+  inconsistent_rows() : invalid_argument("delta rows are inconsistent with their parents' rows") {}
+};
 struct logic_error : std::logic_error {  // std::logic_error in the reference builder
   using std::logic_error::logic_error;
 };

@@ -9,6 +9,55 @@
 
 namespace cbmb {
 
+// Full rows (parent + plus - minus, ascending) of every row, parents first
+// (reconstruct_rows, builder.cpp:452-490): fptr has m+1 offsets. Returns false,
+// without writing past any row, when some delta row is inconsistent with its
+// parent's row (a minus column the parent lacks, a plus column it has).
+bool reconstruct_full_rows(const cbm_b200_cbm_view& v, const std::vector<uint32_t>& bfs,
+                           std::vector<uint64_t>& fptr, std::vector<uint32_t>& fcol) {
+  const uint32_t m = v.n_rows;
+  std::vector<uint64_t> len(m, 0);
+  for (uint32_t x : bfs) {
+    uint64_t plus = 0, minus = 0;
+    for (uint64_t k = v.row_ptr[x]; k < v.row_ptr[x + 1]; ++k)
+      (v.values[k] < 0.0f ? minus : plus) += 1;
+    const uint32_t p = v.parent[x];
+    const uint64_t base = p == kVirtual ? 0 : len[p];
+    if (base + plus < minus || (p == kVirtual && minus)) return false;
+    len[x] = base + plus - minus;
+  }
+  fptr.assign(size_t(m) + 1, 0);
+  for (uint32_t x = 0; x < m; ++x) fptr[x + 1] = fptr[x] + len[x];
+  fcol.resize(fptr[m]);
+  for (uint32_t x : bfs) {
+    uint32_t* out = fcol.data() + fptr[x];
+    uint32_t* const end = out + len[x];
+    const uint32_t p = v.parent[x];
+    uint64_t k = v.row_ptr[x];
+    const uint64_t ke = v.row_ptr[x + 1];
+    const uint32_t* pr = p == kVirtual ? nullptr : fcol.data() + fptr[p];
+    const uint32_t* pe = p == kVirtual ? nullptr : pr + len[p];
+    while (pr < pe || k < ke) {
+      uint32_t c;
+      if (k == ke || (pr < pe && *pr < v.col_idx[k])) {
+        c = *pr++;                              // parent column kept
+      } else if (pr == pe || v.col_idx[k] < *pr) {
+        if (v.values[k] < 0.0f) return false;   // removes a column the parent lacks
+        c = v.col_idx[k++];                     // added column
+      } else {
+        if (v.values[k] > 0.0f) return false;   // adds a column the parent has
+        ++pr;                                   // removed column
+        ++k;
+        continue;
+      }
+      if (out == end) return false;
+      *out++ = c;
+    }
+    if (out != end) return false;
+  }
+  return true;
+}
+
 Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t split_threshold,
                    uint32_t chunk, uint32_t flatten_gain, uint32_t warps_hint) {
   const uint32_t m = v.n_rows;
@@ -106,7 +155,8 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
         for (uint64_t k = v.row_ptr[x]; k < v.row_ptr[x + 1]; ++k)
           (v.values[k] < 0.0f ? minus : plus) += 1;
         const uint32_t p = v.parent[x];
-        nA[x] = p == kVirtual ? plus : nA[p] + plus - minus;
+        const uint64_t base = p == kVirtual ? 0 : nA[p];
+        nA[x] = base + plus >= minus ? base + plus - minus : 0;  // (inconsistent rows: 0)
         const uint64_t dl = plus + minus;
         if (p != kVirtual && nA[x] < dl + flatten_gain) {
           flat[x] = 1;
@@ -117,49 +167,20 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
     L.n_flattened = uint32_t(n_flat);
     std::vector<uint64_t> fptr;  // full rows (only when something is flattened)
     std::vector<uint32_t> fcol;
+    if (n_flat && !reconstruct_full_rows(v, bfs, fptr, fcol)) {
+      // a delta row that removes a column its parent lacks, or adds one it
+      // already has: the reference still multiplies it (U = deltas + U_parent,
+      // kernels.cpp:27-53) but it has no full-row form, so nothing is flattened
+      // and every row keeps its chain link (exactly the reference's values)
+      n_flat = 0;
+      L.n_flattened = 0;
+      L.inconsistent = true;
+    }
     if (n_flat) {
-      // rows from the chain, parents first (reconstruct_rows, builder.cpp:452-490)
-      std::vector<uint64_t> len(m, 0);
-      fptr.assign(m, 0);
-      uint64_t total = 0;
-      for (uint32_t x : bfs) {
-        uint64_t plus = 0, minus = 0;
-        for (uint64_t k = v.row_ptr[x]; k < v.row_ptr[x + 1]; ++k)
-          (v.values[k] < 0.0f ? minus : plus) += 1;
-        const uint32_t p = v.parent[x];
-        len[x] = p == kVirtual ? plus : len[p] + plus - minus;
-        fptr[x] = total;
-        total += len[x];
-      }
-      fcol.resize(total);
-      for (uint32_t x : bfs) {
-        uint32_t* out = fcol.data() + fptr[x];
-        const uint32_t p = v.parent[x];
-        uint64_t k = v.row_ptr[x];
-        const uint64_t ke = v.row_ptr[x + 1];
-        if (p == kVirtual) {
-          for (; k < ke; ++k) *out++ = v.col_idx[k];
-          continue;
-        }
-        const uint32_t* pr = fcol.data() + fptr[p];
-        const uint32_t* pe = pr + len[p];
-        while (pr < pe || k < ke) {  // (parent + plus) - minus, ascending
-          if (k == ke || (pr < pe && *pr < v.col_idx[k])) {
-            *out++ = *pr++;
-          } else if (pr == pe || v.col_idx[k] < *pr) {
-            if (v.values[k] > 0.0f) *out++ = v.col_idx[k];
-            ++k;
-          } else {
-            if (v.values[k] > 0.0f) *out++ = *pr;
-            ++pr;
-            ++k;
-          }
-        }
-      }
       for (uint32_t x = 0; x < m; ++x)
         if (flat[x]) eparent[x] = kVirtual;
       for (uint32_t x = 0; x < m; ++x)
-        eptr[x + 1] = eptr[x] + (flat[x] ? len[x] : v.row_ptr[x + 1] - v.row_ptr[x]);
+        eptr[x + 1] = eptr[x] + (flat[x] ? fptr[x + 1] - fptr[x] : v.row_ptr[x + 1] - v.row_ptr[x]);
     } else {
       for (uint32_t x = 0; x < m; ++x) eptr[x + 1] = v.row_ptr[x + 1];
     }

@@ -39,6 +39,7 @@ struct Layout {
   uint32_t n_merge_items = 0;
   uint32_t n_interior = 0;     // rows with children (scratch slots, normalized)
   uint32_t n_levels = 0, n_roots = 0, max_row_deltas = 0;
+  bool inconsistent = false;  // some delta row has no full-row form (nothing flattened)
   uint64_t nnz = 0;            // deltas of the uploaded CBM
   uint64_t nnz_effective = 0;  // deltas after flattening (what the kernel sums)
   uint32_t n_flattened = 0;    // rows summed directly instead of via their parent
@@ -62,6 +63,11 @@ struct Layout {
 // Validates the view like load_cbm (io.cpp:346-380) and builds the layout.
 // Throws cbmb::invalid_argument with a reference-style message.
 // warps_hint: resident warps of the target device (sizes the auto split).
+// Full rows of every row, parents first; false if some delta row is
+// inconsistent with its parent's row (layout.cpp).
+bool reconstruct_full_rows(const cbm_b200_cbm_view& v, const std::vector<uint32_t>& bfs,
+                           std::vector<uint64_t>& fptr, std::vector<uint32_t>& fcol);
+
 Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t split_threshold,
                    uint32_t chunk, uint32_t flatten_gain, uint32_t warps_hint);
 

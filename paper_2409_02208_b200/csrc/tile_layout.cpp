@@ -163,10 +163,11 @@ TileLayout plan_tiles(const cbm_b200_cbm_view& v, uint32_t rows_cap, uint32_t st
       if (k == ke || (a < base.size() && base[a] < v.col_idx[k])) {
         out.push_back(base[a++]);
       } else if (a == base.size() || v.col_idx[k] < base[a]) {
-        if (v.values[k] > 0.0f) out.push_back(v.col_idx[k]);
+        if (v.values[k] < 0.0f) throw inconsistent_rows();  // removes a missing column
+        out.push_back(v.col_idx[k]);
         ++k;
       } else {
-        if (v.values[k] > 0.0f) out.push_back(base[a]);
+        if (v.values[k] > 0.0f) throw inconsistent_rows();  // adds a present column
         ++a;
         ++k;
       }
