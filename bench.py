@@ -2,25 +2,41 @@
 """Benchmark of the CBM multiply Y = A.X on B200 (BASELINE.json metric).
 
 Prints ONE JSON line on rank 0. A "step" is one multiply over the whole
-workload (all d columns, column-sharded across ranks when N > 1).
+workload (all d columns; rows x columns partitioned across ranks when N > 1).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1]
-  python bench.py --impl reference ...   # reference CPU path (oracle/_ref)
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4_b256]
+  python bench.py --impl reference ...   # the reference's own CPU path
+
+Default workload: cfg4_b256 = BASELINE.json configs[4] (the "1/2/4/8 B200"
+scaling sweep the metric is quoted on), binary A.X at d=256 — the largest
+single-GPU configuration. The north_star's "config 3" (configs[3]: normalized
+A_hat.X at d=256, the GCN's products) is measured in the same run and carried
+as the `north_star_cfg3` key.
 
 value    : effective GFLOP/s = 2 * nnz(represented A) * d / t, device-resident
            operands, CUDA events on the launching stream, L2 flushed (256 MiB
            write) before every timed step; whole job, max time over ranks.
+parity   : before any timing, Y is compared with the reference's own
+           spmm_into (oracle/_ref, the reference compiled from its sources) on
+           the same CBM and X: bitwise for integer X on a binary matrix,
+           max|G-R|/max|R| <= 1e-5 otherwise (north_star tolerance). A failed
+           check withholds `value` (cbm_main.cpp:254-269 does the same).
 e2e      : the same metric through the C-ABI host-buffer entry point
            (cbm_b200_spmm_host: pinned H2D of X, multiply, D2H of Y, sync).
-roofline : B_alg / kernel time against MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline : the reference's own spmm_into (compiled from its sources into
-           oracle/_ref) on this host's cores, same CBM, same operand.
+roofline : B_alg per launch / kernel time against MEASURED_PEAKS.json
+           hbm_gbs (DESIGN.md §6 Roofline).
+cpu_baseline : the reference's spmm_into AND csr_spmm_into (oracle/_ref) on
+           this host, pinned like pin_to_cores (cbm_main.cpp:92-104), at
+           T = all host threads and T = 1; runtime_reduction_pct as
+           cbm_main.cpp:276-283.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,18 +50,24 @@ sys.path.insert(0, ROOT)
 METRIC = "CBM A·X effective GFLOP/s (2·nnz·d/t)"
 UNIT = "GFLOP/s"
 L2_FLUSH_BYTES = 256 << 20
+TOL = 1e-5           # north_star: <= 1e-5 relative (normwise)
+DEFAULT_CONFIG = "cfg4_b256"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=10.0,
-                    help="bounded CPU-baseline sample (seconds of reference work)")
+    ap.add_argument("--cpu-seconds", type=float, default=6.0,
+                    help="seconds of reference work per CPU-baseline leg (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the pre-timing check (dev only: the line then has no value)")
+    ap.add_argument("--no-north-star", action="store_true",
+                    help="do not measure configs[3] beside the workload")
     ap.add_argument("--order-faithful", action="store_true")
     ap.add_argument("--kernel", default="auto", choices=["auto", "scalar"])
     ap.add_argument("--tile", type=int, default=-1, choices=[-1, 0, 1],
@@ -60,6 +82,32 @@ def parse():
     return ap.parse_args()
 
 
+# ---------------------------------------------------------------------------
+# launcher: --gpus N re-executes itself under torch.distributed.run
+# ---------------------------------------------------------------------------
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_relaunch(args):
+    """`python bench.py --gpus N` (N > 1, no torchrun env) -> one rank per GPU.
+    Returns an exit code when it relaunched, None when this process is a rank."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -71,6 +119,20 @@ def dist_env():
     if os.environ.get("BENCH_DEV_SHARE_GPU") == "1":
         local = 0
     return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# shared helpers
+# ---------------------------------------------------------------------------
+def load_workloads():
+    """The workload table, loaded by file path so the reference arm never
+    imports (and so never loads) the product package."""
+    path = os.path.join(ROOT, "paper_2409_02208_b200", "workloads.py")
+    spec = importlib.util.spec_from_file_location("cbm_bench_workloads", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod
+    spec.loader.exec_module(mod)
+    return mod.WORKLOADS
 
 
 def peaks():
@@ -88,6 +150,16 @@ def traffic_for(workload):
         with open(p) as f:
             return json.load(f).get(workload)
     return None
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -151,70 +223,252 @@ def b_alg_bytes(nnz_delta, n_rows, n_cols, d, normalized):
     return s + 4 * d * (n_cols + n_rows)
 
 
-def represented_nnz(a, normalized):
+def represented_nnz(n_rows, row_ptr, col_idx, normalized):
+    """nnz(A), or nnz(A + I) for the normalized operator (builder.cpp:452)."""
+    nnz = int(row_ptr[-1])
     if not normalized:
-        return a.nnz
-    # nnz(A + I): add the diagonal entries that are missing
-    rp, ci = a.row_ptr.astype(np.int64), a.col_idx
-    rows = np.repeat(np.arange(a.n_rows), np.diff(rp))
-    has_diag = np.zeros(a.n_rows, bool)
-    has_diag[rows[ci == rows]] = True
-    return a.nnz + int((~has_diag).sum())
+        return nnz
+    rp = np.asarray(row_ptr, np.int64)
+    rows = np.repeat(np.arange(n_rows), np.diff(rp))
+    has_diag = np.zeros(n_rows, bool)
+    has_diag[rows[np.asarray(col_idx) == rows]] = True
+    return nnz + int((~has_diag).sum())
+
+
+def parity(got, want, exact):
+    """SURVEY §8d gates: bitwise (integer X, binary) or normwise <= 1e-5."""
+    got = np.asarray(got, np.float32)
+    want = np.asarray(want, np.float32)
+    if got.shape != want.shape:
+        return {"ok": False, "why": f"shape {got.shape} vs {want.shape}"}
+    if exact:
+        nd = int(np.count_nonzero(got.view(np.uint32) != want.view(np.uint32)))
+        return {"ok": nd == 0, "mode": "bitwise", "differing": nd}
+    den = float(np.abs(want).max()) if want.size else 0.0
+    num = float(np.abs(got.astype(np.float64) - want).max()) if want.size else 0.0
+    err = num / den if den > 0 else num
+    return {"ok": err <= TOL, "mode": f"normwise max|G-R|/max|R| <= {TOL:g}",
+            "normwise_err": err}
+
+
+class Pinned:
+    """pin_to_cores (cbm_main.cpp:92-104): cores 0..T-1 for the CPU legs."""
+
+    def __init__(self, threads):
+        self.threads = threads
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        hw = os.cpu_count() or 1
+        take = min(max(self.threads, 1), hw)
+        try:
+            os.sched_setaffinity(0, set(range(take)))
+            self.ok = True
+        except OSError:
+            self.ok = False
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.old)
+
+
+def time_reference(op, x, threads, seconds, n_rows):
+    """Mean seconds per call of a reference operator (RefCbm: spmm_into,
+    RefCsrReal: csr_spmm_into), one untimed warm-up first (time_runs,
+    cbm_main.cpp:116-122), at least 2 calls, about `seconds` of work."""
+    with Pinned(threads) as pin:
+        t, runs = op.time_spmm(x, threads, 2, seconds)
+    return t, runs, pin.ok
+
+
+def cpu_legs(O, rc, rcsr, x, nnz, d, threads, seconds, flops_note):
+    """The reference's CBM and CSR CPU paths at T = all and T = 1. The T = 1
+    legs run on a column slab of X (columns are independent, kernels.cpp:27-62,
+    so GFLOP/s is per-column work) sized to a bounded sample."""
+    out = {"cores": threads, "cpu_model": cpu_model(), "pinned": True}
+    legs = {}
+    slab1 = d
+    per_col = 2.0 * nnz
+    # ~2 GFLOP per T=1 call at most (a few seconds of one core)
+    while slab1 > 4 and per_col * slab1 > 2e9:
+        slab1 //= 2
+    x1 = np.ascontiguousarray(x[:, :slab1])
+    for name, op in (("cbm", rc), ("csr", rcsr)):
+        if op is None:
+            continue
+        for t, xx, w in ((threads, x, d), (1, x1, slab1)):
+            s, runs, pinned = time_reference(op, xx, t, seconds, None)
+            legs[f"{name}_t{'all' if t == threads else 1}"] = {
+                "gflops": per_col * w / s / 1e9, "ms_per_call": s * 1e3, "threads": t,
+                "columns": w, "calls": runs, "pinned": pinned}
+    out["legs"] = legs
+    if "cbm_tall" in legs and "csr_tall" in legs:
+        tc, tr = legs["cbm_tall"]["ms_per_call"], legs["csr_tall"]["ms_per_call"]
+        out["runtime_reduction_pct"] = (tr - tc) / tr * 100.0   # cbm_main.cpp:276-283
+    if "cbm_t1" in legs and "csr_t1" in legs:
+        tc, tr = legs["cbm_t1"]["ms_per_call"], legs["csr_t1"]["ms_per_call"]
+        out["runtime_reduction_pct_t1"] = (tr - tc) / tr * 100.0
+    out["note"] = flops_note
+    return out
 
 
 # ---------------------------------------------------------------------------
+# reference arm: the reference's own CPU path (oracle/_ref), no product code
+# ---------------------------------------------------------------------------
+def ref_operands(O, wl):
+    """Graph and X through the restated generators (oracle/gen_oracle.c)."""
+    n, ncols, rp, ci = O.oracle_gen_graph(wl.graph_kind, list(wl.graph_params), wl.graph_seed)
+    lo, hi = wl.x_range
+    x = O.oracle_gen_dense(wl.x_kind, ncols, wl.d, wl.x_seed, lo, hi)
+    return n, ncols, rp, ci, x
+
+
 def run_reference(args, wl):
-    """--impl reference: the reference's own CPU spmm_into (oracle/_ref)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     import oracle as O
-    a = wl.graph()
-    nnz = represented_nnz(a, wl.normalized)
     t0 = time.perf_counter()
-    if a.n_rows <= 50000:
-        # the reference's own builder (builder.cpp:394-429)
-        ra = O.RefCsr.from_arrays(a.n_rows, a.n_cols, a.row_ptr, a.col_idx)
-        rc = O.RefCbm.build(ra, wl.alpha, args.threads, wl.normalized)
-        built_by = "reference build_cbm"
+    n, ncols, rp, ci, x = ref_operands(O, wl)
+    t_gen = time.perf_counter() - t0
+    nnz = represented_nnz(n, rp, ci, wl.normalized)
+    csr = O.RefCsr.from_arrays(n, ncols, rp, ci)
+    # The reference's own builder is O(m^2) (builder.cpp:80-109; SURVEY §0.6):
+    # it finishes in seconds only on the small configs. Where it does, the
+    # timed path is its CBM spmm_into; otherwise its CSR csr_spmm_into on
+    # to_real(A) / normalized_adjacency_csr(A) (kernels.cpp:152-168), the
+    # stock path the reference's CLI times beside the CBM.
+    t0 = time.perf_counter()
+    if n <= 50000:
+        op = O.RefCbm.build(csr, wl.alpha, args.threads, wl.normalized)
+        path = "reference build_cbm + spmm_into (CBM)"
     else:
-        # O(m^2) reference builder is infeasible here (SURVEY §7 H5): our builder's
-        # output (field-identical on every size both can build) wrapped by the
-        # reference's own validating constructors
-        c = wl.build(a, args.threads)
-        rc = O.RefCbm.from_arrays(O.RefCbmArrays(c.n_rows, c.n_cols, c.alpha, c.is_normalized,
-                                                 c.parent, c.row_ptr, c.col_idx, c.values,
-                                                 c.row_scale))
-        built_by = "ours (identical chain), wrapped in reference CbmMatrix"
-    t_build = time.perf_counter() - t0
-    x = wl.operand(a.n_cols)
-    t, runs = rc.time_spmm(x, args.threads, max(1, args.steps), 0.0)
-    flops = 2.0 * nnz * wl.d
-    v = flops / t / 1e9
-    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": runs,
-           "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-           "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, DESIGN.md §Workloads)",
+        op = O.RefCsrReal(csr, wl.normalized)
+        path = ("reference csr_spmm_into on "
+                + ("normalized_adjacency_csr(A)" if wl.normalized else "to_real(A)")
+                + " (its build_cbm is O(m^2) here)")
+    t_prep = time.perf_counter() - t0
+    # bounded sample per step: a column slab of X sized to ~2-3 s of
+    # all-thread work (columns are independent; GFLOP/s counts its own columns)
+    w = wl.d
+    while w > 4 and 2.0 * nnz * w > 50e9:
+        w //= 2
+    xs = np.ascontiguousarray(x[:, :w])
+    with Pinned(args.threads):
+        op.time_spmm(xs, args.threads, 1, 0.0)            # warm-up
+        ts = []
+        for _ in range(max(1, args.steps)):
+            s, _r = op.time_spmm(xs, args.threads, 1, 0.0)
+            ts.append(s)
+    t = float(statistics.mean(ts))
+    v = 2.0 * nnz * w / t / 1e9
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": len(ts),
+           "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (seeded generators restated in oracle/gen_oracle.c)",
            "impl": "reference",
-           "config": {"workload": wl.name, "n": a.n_rows, "nnz": nnz, "d": wl.d,
-                      "alpha": wl.alpha, "normalized": wl.normalized,
-                      "build_s": t_build, "built_by": built_by},
+           "config": {"workload": wl.name, "n": n, "nnz": nnz, "d": wl.d,
+                      "alpha": wl.alpha, "normalized": wl.normalized, "path": path,
+                      "columns_per_step": w, "gen_s": t_gen, "prep_s": t_prep},
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": args.threads,
-                            "kind": "reference",
-                            "sample": f"full {wl.name} multiply x {runs} calls after 1 warm-up "
-                                      "(time_runs protocol, cbm_main.cpp:116-122)"},
+                            "cpu_model": cpu_model(), "kind": "reference",
+                            "sample": f"{path}: X[:, :{w}] of the {wl.name} operand per step, "
+                                      f"{len(ts)} steps after 1 warm-up, pinned to cores "
+                                      f"0..{args.threads - 1}"},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------------------
-def run_ours(args, wl):
+# our arm
+# ---------------------------------------------------------------------------
+def time_steps(fn, steps, stream, flush):
+    import torch
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(float(i))             # L2 flush, outside the event pair
+        starts[i].record(stream)
+        fn()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+
+
+def roofline_for(info, ms, n_out, n_cols, d_local, normalized, workload):
+    peak, peak_src = peaks()
+    b_alg = b_alg_bytes(info["nnz_delta"], n_out, n_cols, d_local, normalized)
+    achieved = b_alg / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    tiled = bool(info["tile_active"]) and d_local >= 32
+    if tiled:
+        l2_bytes = (int(info["tile_staged_rows"]) + int(info["tile_deltas"])
+                    - int(info["tile_staged_deltas"])) * d_local * 4
+    else:
+        l2_bytes = int(info["nnz_effective"]) * d_local * 4
+    r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+         "frac": achieved / peak, "traffic": traffic_for(workload), "b_alg_bytes": b_alg,
+         "kernel": "tile_kernel" if tiled else "cbm_kernel", "peak_source": peak_src,
+         # what bounds the gather: X rows moved L2 -> SM per step (one row per
+         # summed delta; DESIGN.md §6)
+         "l2_gather": {"bytes": l2_bytes,
+                       "achieved_tbps": l2_bytes / (ms * 1e-3) / 1e12 if ms > 0 else 0.0}}
+    if tiled:
+        r["smem_gather_bytes"] = int(info["tile_staged_deltas"]) * d_local * 4
+    return r
+
+
+def run_north_star(args, P, O, WL, dev, stream, flush):
+    """configs[3] (north_star "config 3"): normalized A_hat.X at d=256 on one
+    GPU, parity-gated like the headline, same timing rules."""
+    import torch
+    wl = WL["cfg3"]
+    a = wl.graph()
+    nnz = represented_nnz(a.n_rows, a.row_ptr, a.col_idx, True)
+    t0 = time.perf_counter()
+    c = wl.build(a, args.threads)
+    t_build = time.perf_counter() - t0
+    op = P.DeviceCbm(c, device=dev.index)
+    info = op.info()
+    x_np = wl.operand(a.n_cols)
+    x = torch.from_numpy(x_np).to(dev)
+    y = torch.empty((a.n_rows, wl.d), dtype=torch.float32, device=dev)
+    op.reserve(wl.d)
+    op.spmm_into(x, y, stream)
+    torch.cuda.synchronize()
+    out = {"workload": "cfg3", "n": a.n_rows, "nnz": nnz, "nnz_delta": int(c.nnz), "d": wl.d,
+           "alpha": wl.alpha, "build_s": t_build}
+    if O is not None and O.ref_available():
+        rc = O.RefCbm.from_arrays(O.RefCbmArrays(c.n_rows, c.n_cols, c.alpha, c.is_normalized,
+                                                 c.parent, c.row_ptr, c.col_idx, c.values,
+                                                 c.row_scale))
+        out["parity"] = parity(y.cpu().numpy(), rc.spmm(x_np, args.threads), exact=False)
+        out["parity"]["against"] = "reference spmm_into (oracle/_ref)"
+    for _ in range(max(3, args.warmup)):
+        op.spmm_into(x, y, stream)
+    torch.cuda.synchronize()
+    ms = float(statistics.mean(time_steps(lambda: op.spmm_into(x, y, stream),
+                                          args.steps, stream, flush)))
+    gated = out.get("parity", {}).get("ok", False)
+    out["ms_per_step"] = ms
+    out["value"] = 2.0 * nnz * wl.d / (ms * 1e-3) / 1e9 if gated else None
+    out["unit"] = UNIT
+    out["roofline"] = roofline_for(info, ms, a.n_rows, a.n_cols, wl.d, True, "cfg3")
+    out["gpu_launches_per_step"] = int(op.info()["launches_per_call"])
+    op.close()
+    return out
+
+
+def run_ours(args, wl, WL):
     import torch
     rank, world, local = dist_env()
+    share = os.environ.get("BENCH_DEV_SHARE_GPU") == "1"
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")         # init log: nranks per comm
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
-        if os.environ.get("BENCH_DEV_SHARE_GPU") == "1":
+        if share:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -223,9 +477,14 @@ def run_ours(args, wl):
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2409_02208_b200 as P
+    O = None
+    try:
+        import oracle as O   # the checker and the CPU baseline only
+    except OSError:
+        O = None
 
     a = wl.graph()
-    nnz = represented_nnz(a, wl.normalized)
+    nnz = represented_nnz(a.n_rows, a.row_ptr, a.col_idx, wl.normalized)
     t0 = time.perf_counter()
     c = wl.build(a, args.threads)
     t_build = time.perf_counter() - t0
@@ -234,7 +493,7 @@ def run_ours(args, wl):
     if args.row_groups < 0:
         args.row_groups = 1 if wl.normalized else auto_row_groups(wl.d, world)
     group, slab_rank, n_slabs = grid_position(world, rank, args.row_groups)
-    c_local, n_out = c, a.n_rows
+    c_local, n_out, rows_g = c, a.n_rows, None
     if args.row_groups > 1:
         # this rank's row group (cross-group parents flattened); host-side
         # construction, outside every timed region like the build itself
@@ -253,7 +512,6 @@ def run_ours(args, wl):
     d_local = hi - lo
     x_full = wl.operand(a.n_cols)
     x_host = torch.from_numpy(np.ascontiguousarray(x_full[:, lo:hi])).pin_memory()
-    del x_full
     x = x_host.to(dev)
     y = torch.empty((n_out, d_local), dtype=torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
@@ -264,32 +522,46 @@ def run_ours(args, wl):
         if d_local:
             op.spmm_into(x, y, stream)
 
+    # ---- parity gate (before any timing): this rank's block of Y against the
+    # reference's spmm_into on the same CBM (cbm_main.cpp:254-269)
+    step()
+    torch.cuda.synchronize()
+    gate = {"ok": False, "why": "not checked"}
+    ref_cbm = None
+    if args.no_parity:
+        gate = {"ok": False, "why": "--no-parity"}
+    elif O is not None and O.ref_available():
+        ref_cbm = O.RefCbm.from_arrays(O.RefCbmArrays(c_local.n_rows, c_local.n_cols,
+                                                      c_local.alpha, c_local.is_normalized,
+                                                      c_local.parent, c_local.row_ptr,
+                                                      c_local.col_idx, c_local.values,
+                                                      c_local.row_scale))
+        threads = max(1, args.threads // max(1, world))
+        want = ref_cbm.spmm(x_host.numpy(), threads) if d_local else np.zeros((n_out, 0))
+        gate = parity(y.cpu().numpy(), want, exact=(wl.x_kind == "int" and not wl.normalized))
+        gate["against"] = "reference spmm_into (oracle/_ref) on the same CBM and X"
+        del want
+    else:
+        gate = {"ok": False, "why": "oracle/_ref not available"}
+
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     sampler = ClockSampler(local)
     with sampler:
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.fill_(float(i))             # L2 flush, outside the event pair
-            starts[i].record(stream)
-            step()
-            ends[i].record(stream)
-        torch.cuda.synchronize()
+        dev_ms = time_steps(step, args.steps, stream, flush)
         if dist:
             dist.barrier()
-        dev_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         total_ms = float(sum(dev_ms))
         launches = op.info()["launches_per_call"] * args.steps if d_local else 0
 
         # e2e: C-ABI host-buffer entry point, pinned host memory
         y_host = torch.empty((n_out, d_local), dtype=torch.float32).pin_memory()
-        e2e_steps = max(3, min(args.steps, 50))
+        e2e_steps = max(3, min(args.steps, 20))
         for _ in range(2):
             if d_local:
                 op.spmm_host_ptr(x_host.data_ptr(), a.n_cols, d_local, y_host.data_ptr(),
@@ -310,114 +582,86 @@ def run_ours(args, wl):
         if dist:
             dist.barrier()
 
-    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64,
-                     device="cpu" if os.environ.get("BENCH_DEV_SHARE_GPU") == "1" else dev)
+    ok_local = 1.0 if gate.get("ok") else 0.0
+    t = torch.tensor([total_ms, e2e_ms, -ok_local], dtype=torch.float64,
+                     device="cpu" if share else dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, e2e_ms = float(t[0]), float(t[1])
+    total_ms, e2e_ms, all_ok = float(t[0]), float(t[1]), float(t[2]) < 0
     ms = total_ms / args.steps
 
     flops = 2.0 * nnz * wl.d
     value = flops / (ms * 1e-3) / 1e9
     e2e_value = flops / (e2e_ms * 1e-3) / 1e9
-
-    # roofline of the dominant (only) kernel: B_alg per launch / its duration.
-    # With pre-scaling (normalized, dense rows) two kernels run; the step is
-    # then attributed to the pair (documented in DESIGN.md).
-    peak, peak_src = peaks()
-    b_alg_local = b_alg_bytes(info["nnz_delta"], n_out, a.n_cols, d_local, wl.normalized)
-    achieved = b_alg_local / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-    tiled = bool(info["tile_active"]) and d_local >= 32
-    if tiled:
-        # tiled path: staged X rows come through L2 once per (block, slab) unit,
-        # cold deltas gather their rows from L2, staged deltas read shared memory
-        l2_bytes = (int(info["tile_staged_rows"]) + int(info["tile_deltas"])
-                    - int(info["tile_staged_deltas"])) * d_local * 4
-        smem_bytes = int(info["tile_staged_deltas"]) * d_local * 4
-    else:
-        l2_bytes = int(info["nnz_effective"]) * d_local * 4
-        smem_bytes = 0
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic_for(wl.name),
-                "b_alg_bytes": b_alg_local, "kernel": "tile_kernel" if tiled else "cbm_kernel",
-                "peak_source": peak_src,
-                # what actually bounds the gather: X rows moved L2 -> SM per step
-                # (one row per summed delta) against the measured gather rate of
-                # profiles/r01_ubench_gather.txt
-                "l2_gather": {"bytes": l2_bytes,
-                              "achieved_tbps": l2_bytes / (ms * 1e-3) / 1e12 if ms > 0 else 0.0,
-                              "measured_peak_tbps": 15.7}}
-    if tiled:
-        roofline["smem_gather"] = {
-            "bytes": smem_bytes,
-            "achieved_tbps": smem_bytes / (ms * 1e-3) / 1e12 if ms > 0 else 0.0,
-            "staged_fraction": int(info["tile_staged_deltas"]) / max(1, int(info["tile_deltas"])),
-            "blocks": int(info["tile_blocks"]),
-            "note": "staged deltas read the shared-memory X tile (128 B/clk/SM LSU limit)"}
+    roofline = roofline_for(info, ms, n_out, a.n_cols, d_local, wl.normalized, wl.name)
 
     gpu_csr = None
-    if not args.no_csr_comparator and args.row_groups == 1:
+    if not args.no_csr_comparator and args.row_groups == 1 and world == 1:
         # same kernel on the uncompressed matrix: the paper's runtime reduction
         # (t_csr - t_cbm) / t_csr, both on this B200
-        csr_op = P.DeviceCbm(P.csr_operator(a, wl.normalized), device=local)
+        csr_op = P.DeviceCbm(P.csr_operator(a, wl.normalized), device=local, tile=args.tile)
         csr_op.reserve(max(1, d_local))
-        if d_local:
-            for _ in range(3):
-                csr_op.spmm_into(x, y, stream)
+        for _ in range(3):
+            csr_op.spmm_into(x, y, stream)
         torch.cuda.synchronize()
-        t_csr = []
-        for i in range(min(args.steps, 50)):
-            flush.fill_(float(i))
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            if d_local:
-                csr_op.spmm_into(x, y, stream)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            t_csr.append(e0.elapsed_time(e1))
-        csr_ms = float(statistics.mean(t_csr))
+        csr_ms = float(statistics.mean(time_steps(lambda: csr_op.spmm_into(x, y, stream),
+                                                  min(args.steps, 20), stream, flush)))
         gpu_csr = {"ms_per_step": csr_ms, "value": flops / (csr_ms * 1e-3) / 1e9,
                    "runtime_reduction_pct": (csr_ms - ms) / csr_ms * 100.0,
-                   "note": "uncompressed matrix through the same kernel (every parent virtual)"}
-        del csr_op
+                   "note": "uncompressed matrix through the same kernels (every parent virtual)"}
+        csr_op.close()
 
-    # spmv (d = 1, the lane-per-delta kernel) on the same matrix: reported
-    # beside the headline, with the reference's spmv_into on the host cores
     spmv = None
-    if rank == 0:
+    if rank == 0 and world == 1:
+        # spmv (d = 1, the lane-per-delta kernel) on the same whole matrix
         v = torch.from_numpy(wl.operand(a.n_cols, 1)).to(dev)
         u = torch.empty((n_out, 1), dtype=torch.float32, device=dev)
         op.reserve(1)
         for _ in range(3):
             op.spmv_into(v, u, stream)
         torch.cuda.synchronize()
-        t_v = []
-        for i in range(min(args.steps, 50)):
-            flush.fill_(float(i))
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            op.spmv_into(v, u, stream)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            t_v.append(e0.elapsed_time(e1))
-        spmv_ms = float(statistics.mean(t_v))
+        spmv_ms = float(statistics.mean(time_steps(lambda: op.spmv_into(v, u, stream),
+                                                   min(args.steps, 20), stream, flush)))
         spmv = {"ms_per_call": spmv_ms, "value": 2.0 * nnz / (spmv_ms * 1e-3) / 1e9,
                 "unit": UNIT, "kernel": "cbm_spmv_kernel", "l2": "flushed before every call"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, wl, c, nnz)
-        if spmv is not None and cpu is not None:
-            spmv["cpu_reference"] = cpu_spmv(args, wl, c, nnz)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and O is not None \
+            and O.ref_available():
+        if ref_cbm is None:
+            ref_cbm = O.RefCbm.from_arrays(O.RefCbmArrays(c.n_rows, c.n_cols, c.alpha,
+                                                          c.is_normalized, c.parent, c.row_ptr,
+                                                          c.col_idx, c.values, c.row_scale))
+        ref_csr = O.RefCsrReal(O.RefCsr.from_arrays(a.n_rows, a.n_cols, a.row_ptr, a.col_idx),
+                               wl.normalized)
+        legs = cpu_legs(O, ref_cbm, ref_csr, x_host.numpy(), nnz, wl.d, args.threads,
+                        args.cpu_seconds, "reference spmm_into (CBM built by our builder, "
+                        "field-identical to build_cbm, wrapped in the reference's validating "
+                        "CbmMatrix) and csr_spmm_into on "
+                        + ("normalized_adjacency_csr(A)" if wl.normalized else "to_real(A)"))
+        cbm_all = legs["legs"]["cbm_tall"]
+        cpu = {"value": cbm_all["gflops"], "unit": UNIT, "cores": args.threads,
+               "kind": "reference",
+               "sample": f"full {wl.name} multiply (reference spmm_into, f32 build) x "
+                         f"{cbm_all['calls']} calls after 1 warm-up at T={args.threads}; T=1 "
+                         f"legs on X[:, :{legs['legs']['cbm_t1']['columns']}]",
+               **legs}
+        del ref_csr
+    del ref_cbm
 
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    north = None
+    if rank == 0 and world == 1 and not args.no_north_star and wl.name != "cfg3":
+        op.close()   # free the headline matrix before the second workload
+        north = run_north_star(args, P, O, WL, dev, stream, flush)
+
+    out = {"metric": METRIC, "value": value if all_ok else None, "unit": UNIT,
+           "n_gpus": world, "steps": args.steps,
            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-           "data": "synthetic (seeded generators, DESIGN.md §Workloads)",
+           "data": "synthetic (seeded generators, DESIGN.md §8)",
            "config": {"workload": wl.name, "note": wl.note, "n": a.n_rows, "nnz": nnz,
-                      "nnz_delta": info["nnz_delta"], "d": wl.d, "d_per_rank": d_local,
+                      "nnz_delta": int(c.nnz), "nnz_delta_local": info["nnz_delta"],
+                      "d": wl.d, "d_per_rank": d_local,
                       "alpha": wl.alpha, "normalized": wl.normalized,
                       "parallelism": (f"column-shard x{world}" if args.row_groups == 1 else
                                       f"{args.row_groups} row groups x {n_slabs} column slabs"),
@@ -426,7 +670,9 @@ def run_ours(args, wl):
                       "l2": "flushed (256 MiB write) before every timed step",
                       "levels": info["n_levels"], "chunk_items": info["n_chunk_items"],
                       "actual_ops_per_step": int(sum(P.count_scalar_ops(c_local)) * d_local),
-                      "build_s": t_build, "upload_s": t_upload},
+                      "build_s": t_build, "upload_s": t_upload,
+                      "seeds": {"graph": hex(wl.graph_seed), "x": hex(wl.x_seed)}},
+           "parity": dict(gate, all_ranks_ok=all_ok),
            "roofline": roofline,
            "cpu_baseline": cpu,
            "gpu_csr_comparator": gpu_csr,
@@ -437,49 +683,26 @@ def run_ours(args, wl):
                    "entry": "cbm_b200_spmm_host (C ABI, pinned host buffers)"},
            "gpu_launches": int(launches),
            "clocks": sampler.summary()}
+    if north is not None:
+        out["north_star_cfg3"] = north
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
-    return 0
-
-
-def cpu_baseline(args, wl, c, nnz):
-    """The reference's spmm_into on this host (oracle/_ref), same CBM and X."""
-    import oracle as O
-    if not O.ref_available():
-        return None
-    rc = O.RefCbm.from_arrays(O.RefCbmArrays(c.n_rows, c.n_cols, c.alpha, c.is_normalized,
-                                             c.parent, c.row_ptr, c.col_idx, c.values,
-                                             c.row_scale))
-    x = wl.operand(c.n_cols)
-    t, runs = rc.time_spmm(x, args.threads, 3, args.cpu_seconds)
-    return {"value": 2.0 * nnz * wl.d / t / 1e9, "unit": UNIT, "cores": args.threads,
-            "kind": "reference",
-            "sample": f"full {wl.name} multiply (reference spmm_into, f32 build) x {runs} calls "
-                      f"after 1 warm-up, {t * 1e3:.2f} ms/call"}
-
-
-def cpu_spmv(args, wl, c, nnz):
-    """The reference's spmv_into on this host (oracle/_ref), same CBM, d = 1."""
-    import oracle as O
-    rc = O.RefCbm.from_arrays(O.RefCbmArrays(c.n_rows, c.n_cols, c.alpha, c.is_normalized,
-                                             c.parent, c.row_ptr, c.col_idx, c.values,
-                                             c.row_scale))
-    v = wl.operand(c.n_cols, 1)
-    t, runs = rc.time_spmv(v, args.threads, 3, min(2.0, args.cpu_seconds))
-    return {"value": 2.0 * nnz / t / 1e9, "unit": UNIT, "cores": args.threads,
-            "kind": "reference", "sample": f"spmv_into x {runs} calls, {t * 1e3:.3f} ms/call"}
+    return 0 if all_ok else 1
 
 
 def main():
     args = parse()
-    from paper_2409_02208_b200.workloads import WORKLOADS
-    wl = WORKLOADS[args.config]
+    rc = maybe_relaunch(args)
+    if rc is not None:
+        return rc
+    WL = load_workloads()
+    wl = WL[args.config]
     if args.impl == "reference":
         return run_reference(args, wl)
-    return run_ours(args, wl)
+    return run_ours(args, wl, WL)
 
 
 if __name__ == "__main__":

@@ -55,8 +55,57 @@ def restated() -> C.CDLL:
         lib.oracle_random_binary.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_uint64,
                                              _u64p, _u32p]
         lib.oracle_random_binary.restype = C.c_uint64
+        lib.oracle_gen_graph.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_uint64,
+                                         C.POINTER(_OracleGraph)]
+        lib.oracle_graph_free.argtypes = [C.POINTER(_OracleGraph)]
+        lib.oracle_gen_dense.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_double,
+                                         C.c_double, C.c_uint64, _f32p]
         _orc = lib
     return _orc
+
+
+class _OracleGraph(C.Structure):
+    _fields_ = [("n_rows", C.c_uint32), ("n_cols", C.c_uint32), ("nnz", C.c_uint64),
+                ("row_ptr", C.POINTER(C.c_uint64)), ("col_idx", C.POINTER(C.c_uint32))]
+
+
+_GRAPH_KINDS = {"community": 0, "pa_triangle": 1, "clique_overlay": 2}
+_DENSE_KINDS = {"int": 1, "normal": 2, "glorot": 3}
+
+
+def oracle_gen_graph(kind: str, params, seed: int):
+    """Restated seeded graph generators (oracle/gen_oracle.c): returns
+    (n, row_ptr u64[n+1], col_idx u32[nnz]) — the same CSR the product's
+    generate_graph draws (pinned by tests/test_oracle_gen.py)."""
+    if kind == "random_binary":
+        rows, cols, dens = params
+        rp, ci = oracle_random_binary(int(rows), int(cols), float(dens), seed)
+        return int(rows), int(cols), rp, ci
+    lib = restated()
+    p = (C.c_double * len(params))(*[float(v) for v in params])
+    g = _OracleGraph()
+    rc = lib.oracle_gen_graph(_GRAPH_KINDS[kind], p, seed, C.byref(g))
+    if rc != 0:
+        raise RuntimeError(f"oracle_gen_graph({kind}) failed ({rc})")
+    try:
+        n = g.n_rows
+        rp = np.ctypeslib.as_array(g.row_ptr, shape=(n + 1,)).copy()
+        ci = (np.ctypeslib.as_array(g.col_idx, shape=(g.nnz,)).copy() if g.nnz
+              else np.zeros(0, np.uint32))
+    finally:
+        lib.oracle_graph_free(C.byref(g))
+    return n, g.n_cols if g.n_cols else n, rp, ci
+
+
+def oracle_gen_dense(kind: str, rows: int, cols: int, seed: int, lo: float = -8.0,
+                     hi: float = 8.0) -> np.ndarray:
+    """Restated seeded dense operands: "int" (below(hi-lo+1)+lo), "normal"
+    (Box–Muller N(0,1)), "glorot" (Glorot-uniform rows x cols weight)."""
+    out = np.empty((rows, cols), np.float32)
+    rc = restated().oracle_gen_dense(_DENSE_KINDS[kind], rows, cols, lo, hi, seed, out)
+    if rc != 0:
+        raise ValueError(f"oracle_gen_dense({kind}) failed")
+    return out
 
 
 def topo_order_from_parents(parent: np.ndarray) -> np.ndarray:
