@@ -157,6 +157,12 @@ void cbm_b200_default_options(cbm_b200_options* opt);
 int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
                     cbm_b200_matrix** out);
 void cbm_b200_free(cbm_b200_matrix* h);
+/* Ship-pre-compressed path: a CBM1 container file straight to
+ * the device — the file is memory-mapped and validated by all host threads
+ * with load_cbm's rules and messages (io.cpp:293-382; EFORMAT), then uploaded
+ * as cbm_b200_upload does. Equivalent to load_cbm1 + upload + host_free. */
+int cbm_b200_upload_cbm1(const char* path, const cbm_b200_options* opt,
+                         cbm_b200_matrix** out);
 
 /* Y = A X on device memory (spmm_into, kernels.hpp:36-39, kernels.cpp:105-123).
  * X is x_rows x x_cols row-major with leading dimension ldx (floats); Y is

@@ -114,6 +114,7 @@ _sig = {
     "cbm_b200_count_ops": (C.c_int, [C.POINTER(_CbmView), C.POINTER(_u64), C.POINTER(_u64)]),
     "cbm_b200_default_options": (None, [C.POINTER(_Options)]),
     "cbm_b200_upload": (C.c_int, [C.POINTER(_CbmView), C.POINTER(_Options), C.POINTER(_vp)]),
+    "cbm_b200_upload_cbm1": (C.c_int, [C.c_char_p, C.POINTER(_Options), C.POINTER(_vp)]),
     "cbm_b200_free": (None, [_vp]),
     "cbm_b200_reserve": (C.c_int, [_vp, _i64]),
     "cbm_b200_reserve_on": (C.c_int, [_vp, _i64, _vp]),
@@ -464,11 +465,12 @@ def _torch():
 class DeviceCbm:
     """A CBM uploaded once into the device layout."""
 
-    def __init__(self, c: CbmMatrix, device: int | None = None, order_faithful: bool = False,
-                 split_threshold: int = 0, chunk: int = 0, prescale: int = -1,
-                 kernel: str = "auto", max_segments: int = 0, flatten_gain: int = -1,
-                 prefetch: bool = False, tile: int = -1, tile_rows: int = 0,
-                 tile_stage: int = 0, tile_vec: int = 0):
+    def __init__(self, c: CbmMatrix | None, device: int | None = None,
+                 order_faithful: bool = False, split_threshold: int = 0, chunk: int = 0,
+                 prescale: int = -1, kernel: str = "auto", max_segments: int = 0,
+                 flatten_gain: int = -1, prefetch: bool = False, tile: int = -1,
+                 tile_rows: int = 0, tile_stage: int = 0, tile_vec: int = 0,
+                 _cbm1_path=None):
         opt = _Options()
         _lib.cbm_b200_default_options(C.byref(opt))
         opt.device = -1 if device is None else int(device)
@@ -487,11 +489,24 @@ class DeviceCbm:
         opt.tile_stage = tile_stage
         opt.tile_vec = tile_vec
         self._h = _vp()
-        view = c._view()
-        _check(_lib.cbm_b200_upload(C.byref(view), C.byref(opt), C.byref(self._h)))
-        self.n_rows, self.n_cols = c.n_rows, c.n_cols
-        self.is_normalized = c.is_normalized
+        if _cbm1_path is not None:
+            _check(_lib.cbm_b200_upload_cbm1(str(_cbm1_path).encode(), C.byref(opt),
+                                             C.byref(self._h)))
+            info = self.info()
+            self.n_rows, self.n_cols = info["n_rows"], info["n_cols"]
+            self.is_normalized = bool(info["is_normalized"])
+        else:
+            view = c._view()
+            _check(_lib.cbm_b200_upload(C.byref(view), C.byref(opt), C.byref(self._h)))
+            self.n_rows, self.n_cols = c.n_rows, c.n_cols
+            self.is_normalized = c.is_normalized
         self.device = opt.device
+
+    @classmethod
+    def from_cbm1(cls, path, **options) -> "DeviceCbm":
+        """A CBM1 container file straight to the device (cbm_b200_upload_cbm1:
+        mapped, validated like load_cbm, uploaded)."""
+        return cls(None, _cbm1_path=path, **options)
 
     def close(self, _free=_lib.cbm_b200_free):
         if getattr(self, "_h", None):

@@ -67,6 +67,27 @@ void check_spmm_shapes(const cbmb::Layout& L, int64_t x_rows, int64_t x_cols, in
   if (x_cols < 0 || x_cols > 0x7FFFFFFF)
     throw cbmb::invalid_argument(std::string(who) + ": bad column count");
 }
+
+// Options check + device upload of a borrowed view (throws).
+cbm_b200_matrix* upload_view(const cbm_b200_cbm_view& view, const cbm_b200_options* opt) {
+  const cbm_b200_cbm_view* c = &view;
+  cbm_b200_options o;
+  cbm_b200_default_options(&o);
+  if (opt) o = *opt;
+  need(o.kernel == 0 || o.kernel == 1, "upload: options.kernel must be 0 (auto) or 1 (scalar)");
+  need(o.max_segments >= 0 && o.max_segments <= 4, "upload: options.max_segments must be 0..4");
+  need(o.tile >= -1 && o.tile <= 1, "upload: options.tile must be -1, 0 or 1");
+  need(o.tile_vec == 0 || o.tile_vec == 1 || o.tile_vec == 2 || o.tile_vec == 4,
+       "upload: options.tile_vec must be 0, 1, 2 or 4");
+  auto* h = new cbm_b200_matrix{nullptr};
+  try {
+    h->d = cbmb::device_upload(*c, o);
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  return h;
+}
 }  // namespace
 
 extern "C" {
@@ -211,22 +232,21 @@ int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
   return guard([&] {
     need(c && out, "upload: null argument");
     *out = nullptr;
-    cbm_b200_options o;
-    cbm_b200_default_options(&o);
-    if (opt) o = *opt;
-    need(o.kernel == 0 || o.kernel == 1, "upload: options.kernel must be 0 (auto) or 1 (scalar)");
-    need(o.max_segments >= 0 && o.max_segments <= 4, "upload: options.max_segments must be 0..4");
-    need(o.tile >= -1 && o.tile <= 1, "upload: options.tile must be -1, 0 or 1");
-    need(o.tile_vec == 0 || o.tile_vec == 1 || o.tile_vec == 2 || o.tile_vec == 4,
-         "upload: options.tile_vec must be 0, 1, 2 or 4");
-    auto* h = new cbm_b200_matrix{nullptr};
-    try {
-      h->d = cbmb::device_upload(*c, o);
-    } catch (...) {
-      delete h;
-      throw;
-    }
-    *out = h;
+    *out = upload_view(*c, opt);
+  });
+}
+
+int cbm_b200_upload_cbm1(const char* path, const cbm_b200_options* opt,
+                         cbm_b200_matrix** out) {
+  return guard([&] {
+    need(path && out, "upload_cbm1: null argument");
+    *out = nullptr;
+    const cbmb::HostCbm c = cbmb::load_cbm1(path);   // mapped, validated by all host threads
+    cbm_b200_cbm_view v{c.n_rows, c.n_cols, c.row_ptr.back(), c.alpha, c.normalized ? 1 : 0,
+                        c.parent.data(), c.topo_order.data(), c.row_ptr.data(),
+                        c.col_idx.data(), c.values.data(),
+                        c.normalized ? c.row_scale.data() : nullptr};
+    *out = upload_view(v, opt);
   });
 }
 

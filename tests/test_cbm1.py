@@ -99,3 +99,81 @@ def test_container_to_device(tmp_path):
     x = P.generate_dense("normal", 2000, 96, 10)
     y = P.DeviceCbm(back, order_faithful=True).spmm(torch.from_numpy(x).cuda()).cpu().numpy()
     assert_bitwise(y, O.oracle_spmm(oracle_arrays(c), x), "cbm1 -> device")
+
+
+@pytest.mark.parametrize("normalized", [False, True])
+def test_corruptions_report_the_reference_error(normalized, tmp_path):
+    """Random byte corruptions (several at once, so several rules can break):
+    our mapped parallel loader accepts exactly what the reference's load_cbm
+    accepts and reports the same first error (io.cpp:293-382 order)."""
+    if not O.ref_available():
+        pytest.skip("compiled reference absent")
+    a = P.CsrBinaryMatrix(40, 40, *O.oracle_random_binary(40, 40, 0.3, 11))
+    c = (P.build_cbm_normalized if normalized else P.build_cbm)(a, 0)
+    path = tmp_path / "g.cbm"
+    P.save_cbm(c, path)
+    good = bytes(open(path, "rb").read())
+    rng = np.random.default_rng(7 + normalized)
+    seen = set()
+    for trial in range(300):
+        b = bytearray(good)
+        for _ in range(int(rng.integers(1, 4))):
+            pos = int(rng.integers(40, len(b)))
+            b[pos] = int(rng.integers(0, 256)) if rng.random() < 0.5 else b[pos] ^ (1 << int(rng.integers(0, 8)))
+        p = tmp_path / f"t{trial}.cbm"
+        open(p, "wb").write(bytes(b))
+        try:
+            ref = O.RefCbm.load(p)
+            ref_err = None
+        except Exception as e:  # noqa: BLE001  (the reference's format_error text)
+            ref, ref_err = None, str(e)
+        try:
+            ours = P.load_cbm(p)
+            our_err = None
+        except P.FormatError as e:
+            ours, our_err = None, str(e).split("] ", 1)[-1] if str(e).startswith("[") else str(e)
+        if ref_err is None:
+            assert our_err is None, (trial, our_err)
+            assert same_cbm(ours, ref.arrays())
+        else:
+            assert our_err is not None and our_err.endswith(ref_err) or ref_err.endswith(our_err), \
+                (trial, our_err, ref_err)
+            seen.add(ref_err.split(":")[0])
+    assert len(seen) >= 3, seen
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("normalized", [False, True])
+def test_reference_container_straight_to_device(normalized, tmp_path):
+    """The reference's own save_cbm -> cbm_b200_upload_cbm1 (mapped, validated,
+    uploaded in one call) -> multiply, against the compiled reference's
+    spmm_into on the same file and against the oracle."""
+    if not O.ref_available():
+        pytest.skip("compiled reference absent")
+    import torch
+    from helpers import assert_bitwise, normwise_err, oracle_arrays
+    a = O.RefCsr.community_graph(40, 50, 35, 3, 91)
+    ref = O.RefCbm.build(a, 0, threads=4, normalized=normalized)
+    path = tmp_path / "ref.cbm"
+    ref.save(path)
+    n = ref.dims()[1]
+    x = (P.generate_dense("int", n, 64, 12, -8, 8) if not normalized
+         else P.generate_dense("normal", n, 128, 12))
+    want = O.RefCbm.load(path).spmm(x, 4)
+    assert_bitwise(O.oracle_spmm(ref.arrays(), x), want, "oracle vs reference")
+    for faithful in (True, False):
+        op = P.DeviceCbm.from_cbm1(path, device=0, order_faithful=faithful)
+        assert (op.n_rows, op.is_normalized) == (ref.dims()[0], normalized)
+        got = op.spmm(torch.from_numpy(x).cuda()).cpu().numpy()
+        if faithful or not normalized:
+            assert_bitwise(got, want, f"cbm1 -> device, faithful={faithful}")
+        else:
+            assert normwise_err(got, want) <= 1e-5
+
+
+def test_upload_cbm1_reports_format_errors_without_a_device(tmp_path):
+    blob, _ = _good(tmp_path)
+    p = tmp_path / "bad.cbm"
+    open(p, "wb").write(bytes(blob[:-1]))
+    with pytest.raises(P.FormatError, match="payload size mismatch"):
+        P.DeviceCbm.from_cbm1(p)
