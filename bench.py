@@ -442,7 +442,10 @@ def run_north_star(args, P, O, WL, dev, stream, flush):
         rc = O.RefCbm.from_arrays(O.RefCbmArrays(c.n_rows, c.n_cols, c.alpha, c.is_normalized,
                                                  c.parent, c.row_ptr, c.col_idx, c.values,
                                                  c.row_scale))
-        out["parity"] = parity(y.cpu().numpy(), rc.spmm(x_np, args.threads), exact=False)
+        out["parity"] = O.judge_parity(
+            y.cpu().numpy(), rc.spmm(x_np, args.threads), TOL,
+            lambda cols: O.oracle_exact_spmm(a.row_ptr, a.col_idx, x_np[:, cols], c.row_scale,
+                                             add_identity=True))
         out["parity"]["against"] = "reference spmm_into (oracle/_ref)"
     for _ in range(max(3, args.warmup)):
         op.spmm_into(x, y, stream)
@@ -538,7 +541,15 @@ def run_ours(args, wl, WL):
                                                       c_local.row_scale))
         threads = max(1, args.threads // max(1, world))
         want = ref_cbm.spmm(x_host.numpy(), threads) if d_local else np.zeros((n_out, 0))
-        gate = parity(y.cpu().numpy(), want, exact=(wl.x_kind == "int" and not wl.normalized))
+        if wl.x_kind == "int" and not wl.normalized:
+            gate = parity(y.cpu().numpy(), want, exact=True)
+        else:
+            def exact(cols):
+                e = O.oracle_exact_spmm(a.row_ptr, a.col_idx, x_host.numpy()[:, cols],
+                                        c.row_scale if wl.normalized else None,
+                                        add_identity=wl.normalized)
+                return e if rows_g is None else e[rows_g]
+            gate = O.judge_parity(y.cpu().numpy(), want, TOL, exact)
         gate["against"] = "reference spmm_into (oracle/_ref) on the same CBM and X"
         del want
     else:

@@ -134,7 +134,15 @@ def test_cfg4_full_size_binary(cfg4):
     x = wl.operand(a.n_cols)
     want = rc.spmm(x, THREADS)
     got, _ = run(c, x)
-    assert normwise_err(got, want) <= TOL
+    # the hub row has ~1.4M entries: the reference's sequential f32 sum is
+    # itself ~3e-5 (normwise) from the exact product, so the device result is
+    # judged against the f64 product on a column sample when it differs from
+    # the reference by more than the tolerance (oracle.judge_parity)
+    j = O.judge_parity(got, want, TOL, lambda cols: O.oracle_exact_spmm(
+        a.row_ptr, a.col_idx, x[:, cols]))
+    assert j["ok"], j
+    if "exact_err" in j:
+        assert j["exact_err"] <= j["reference_exact_err"], j
     del got, want, x
     xi = P.generate_dense("int", a.n_cols, 32, 0xC0F61104, -8, 8)
     got, _ = run(c, xi)
