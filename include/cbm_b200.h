@@ -146,6 +146,14 @@ typedef struct cbm_b200_options {
   uint32_t tile_rows;        /* rows per tile block (0 = auto, 64..512) */
   uint32_t tile_stage;       /* staged X rows per block (0 = auto, 600) */
   int32_t tile_vec;          /* floats per lane of a tile slab: 0 auto, 1, 2, 4 */
+  int32_t dense;             /* default mode only: dense-block path:
+                                the columns shared by >= dense_min rows of each
+                                128-row tile multiplied on the tensor cores
+                                (tcgen05, exact tf32 split), the remaining entries
+                                by the streaming kernel on top. -1 auto (when the
+                                cost model favours it), 0 off, 1 force */
+  uint32_t dense_min;        /* entries per column per tile to count as shared
+                                (0 = auto, 3) */
 } cbm_b200_options;
 
 void cbm_b200_default_options(cbm_b200_options* opt);
@@ -274,6 +282,11 @@ typedef struct cbm_b200_info {
   uint64_t tile_deltas;      /* entries the tiled kernel sums (cut rows flattened) */
   uint64_t tile_staged_deltas; /* of which read from the shared-memory tile */
   uint64_t tile_staged_rows;   /* staged X rows over all blocks */
+  int32_t dense_active;        /* multiplies with d >= 32 take the dense-block path */
+  uint32_t dense_tiles;        /* 128-row tiles */
+  uint64_t dense_chunks;       /* 32-column chunks multiplied on the tensor cores */
+  uint64_t dense_entries;      /* entries summed by the tensor cores */
+  uint64_t cold_entries;       /* entries summed by the streaming kernel */
 } cbm_b200_info;
 int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* out);
 

@@ -76,7 +76,8 @@ class _Options(C.Structure):
                 ("split_threshold", C.c_uint32), ("chunk", C.c_uint32), ("prescale", C.c_int32),
                 ("kernel", C.c_int32), ("max_segments", C.c_int32),
                 ("flatten_gain", C.c_int32), ("prefetch", C.c_int32), ("tile", C.c_int32),
-                ("tile_rows", C.c_uint32), ("tile_stage", C.c_uint32), ("tile_vec", C.c_int32)]
+                ("tile_rows", C.c_uint32), ("tile_stage", C.c_uint32), ("tile_vec", C.c_int32),
+                ("dense", C.c_int32), ("dense_min", C.c_uint32)]
 
 
 class _Info(C.Structure):
@@ -90,7 +91,9 @@ class _Info(C.Structure):
                 ("tile_blocks", C.c_uint32), ("tile_max_rows", C.c_uint32),
                 ("tile_max_staged", C.c_uint32), ("tile_cut_rows", C.c_uint32),
                 ("tile_deltas", C.c_uint64), ("tile_staged_deltas", C.c_uint64),
-                ("tile_staged_rows", C.c_uint64)]
+                ("tile_staged_rows", C.c_uint64), ("dense_active", C.c_int32),
+                ("dense_tiles", C.c_uint32), ("dense_chunks", C.c_uint64),
+                ("dense_entries", C.c_uint64), ("cold_entries", C.c_uint64)]
 
 
 class _Stats(C.Structure):
@@ -470,7 +473,7 @@ class DeviceCbm:
                  prescale: int = -1, kernel: str = "auto", max_segments: int = 0,
                  flatten_gain: int = -1, prefetch: bool = False, tile: int = -1,
                  tile_rows: int = 0, tile_stage: int = 0, tile_vec: int = 0,
-                 _cbm1_path=None):
+                 dense: int = -1, dense_min: int = 0, _cbm1_path=None):
         opt = _Options()
         _lib.cbm_b200_default_options(C.byref(opt))
         opt.device = -1 if device is None else int(device)
@@ -488,6 +491,8 @@ class DeviceCbm:
         opt.tile_rows = tile_rows
         opt.tile_stage = tile_stage
         opt.tile_vec = tile_vec
+        opt.dense = int(dense)
+        opt.dense_min = dense_min
         self._h = _vp()
         if _cbm1_path is not None:
             _check(_lib.cbm_b200_upload_cbm1(str(_cbm1_path).encode(), C.byref(opt),

@@ -77,6 +77,7 @@ cbm_b200_matrix* upload_view(const cbm_b200_cbm_view& view, const cbm_b200_optio
   need(o.kernel == 0 || o.kernel == 1, "upload: options.kernel must be 0 (auto) or 1 (scalar)");
   need(o.max_segments >= 0 && o.max_segments <= 4, "upload: options.max_segments must be 0..4");
   need(o.tile >= -1 && o.tile <= 1, "upload: options.tile must be -1, 0 or 1");
+  need(o.dense >= -1 && o.dense <= 1, "upload: options.dense must be -1, 0 or 1");
   need(o.tile_vec == 0 || o.tile_vec == 1 || o.tile_vec == 2 || o.tile_vec == 4,
        "upload: options.tile_vec must be 0, 1, 2 or 4");
   auto* h = new cbm_b200_matrix{nullptr};
@@ -225,6 +226,8 @@ void cbm_b200_default_options(cbm_b200_options* o) {
   o->tile_rows = 0;
   o->tile_stage = 0;
   o->tile_vec = 0;
+  o->dense = -1;
+  o->dense_min = 0;
 }
 
 int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
@@ -479,6 +482,12 @@ int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* o) {
     o->tile_deltas = T.n_deltas;
     o->tile_staged_deltas = T.n_staged_deltas;
     o->tile_staged_rows = T.n_staged_cols;
+    const auto& D = h->d->dense;
+    o->dense_active = h->d->dense_on ? 1 : 0;
+    o->dense_tiles = D.n_tiles;
+    o->dense_chunks = D.n_chunks;
+    o->dense_entries = D.dense_entries;
+    o->cold_entries = D.cold_entries;
   });
 }
 

@@ -157,6 +157,8 @@ struct Params {
   unsigned long long* trace;  // dev tool (CBM_B200_TRACE): 4 x u64 per warp, else null
   uint32_t ldx32;             // ldx in floats (< 2^30): 32x32->64 address multiply
   uint32_t ldxb;              // ldx in bytes (< 2^32): one IMAD.WIDE per gathered row
+  const float* base;          // optional addend per output row (unscaled), may alias y
+  long long ldbase;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -702,6 +704,15 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
       for (int u = 0; u < U; ++u) acc[u] = W::add(acc[u], pv[u]);
     }
     const uint32_t row = r.rowk & 0x7FFFFFFFu;
+    if (p.base) {  // + the row's dense-block (tensor-core) sum, read before Y is written
+      const float* src = p.base + (long long)row * p.ldbase;
+      T4 bv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        bv[u] = col + uint32_t(u) * kSeg < p.d ? W::ldcg(src + col + u * kSeg) : W::zero();
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u] = W::add(acc[u], bv[u]);
+    }
     const bool is_parent = (r.rowk >> 31) != 0;
     float* yrow = p.y + (long long)row * p.ldy;
     if constexpr (NORM) {
@@ -983,18 +994,29 @@ uint32_t pick_vec(uint32_t d, const float* x, int64_t ldx, const float* y, int64
 }  // namespace
 
 void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
-                 int64_t ldy, void* stream, bool relu) {
+                 int64_t ldy, void* stream, bool relu, const float* base, int64_t ldbase) {
   const Layout& L = h->info;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   h->last_launches = 0;
   if (L.n_rows == 0 || d == 0) return;
   if (ldx >= (int64_t(1) << 31)) throw invalid_argument("spmm: leading dimension too large");
   ck(cudaSetDevice(h->device), "cudaSetDevice");
+  if (h->dense_on && d >= kDenseMinD && !base) {
+    // dense-block path: the tensor cores write the shared-column part of
+    // every row (unscaled) into Y, the streaming kernel adds the cold
+    // entries to it in place and applies the row scale / ReLU
+    if (ldx >= (int64_t(1) << 30))
+      throw invalid_argument("spmm: leading dimension of X must be below 2^30");
+    dense_spmm(h, x, ldx, d, y, ldy, s);
+    device_spmm(h->cold, x, ldx, d, y, ldy, stream, relu, y, ldy);
+    h->last_launches = 1 + h->cold->last_launches;
+    return;
+  }
   device_reserve(h, d, stream);
   auto& ws = h->ws[stream];
   const uint32_t dpad = (d + 3) & ~3u;
   // tiled path (tile_kernel.cu): community-structured matrices, d >= 32
-  if (h->tile_on && d >= 32) {
+  if (h->tile_on && d >= 32 && !base) {
     if (const uint32_t tv = tile_pick_vec(h, d, x, ldx, y, ldy)) {
       tile_spmm(h, tv, x, ldx, d, y, ldy, ws.tinterior, dpad, relu, s);
       h->last_launches = 1;
@@ -1049,6 +1071,8 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     ws.epoch = 1;
   }
   Params p;
+  p.base = base;
+  p.ldbase = ldbase;
   p.dcol = h->dcol;
   p.dval = h->dval;
   p.scale = h->scale;

@@ -1,0 +1,372 @@
+// Dense-block path: the shared columns of each 128-row tile of
+// the represented matrix (dense_layout.cpp) multiplied on the 5th-generation
+// tensor cores. Per work unit (tile t, feature block of 128 columns of X):
+//
+//   D[f, r] = sum_k X'[col_k, f] * B[r, k]        (f: 128 features, r: 128 rows)
+//
+// with X' = X (binary) or fl(s_col * X) (normalized, the reference's per-product
+// rounding, kernels.cpp:30-35) and B the tile's 0/1 pattern on the chunk
+// columns. This is the transposed product Y_tile^T = X'^T B^T, so that:
+//   * A operand = X'^T, written straight from registers into TMEM by the
+//     producer warps (tcgen05.st; lane = feature, one column per K element):
+//     the gathered X rows never touch shared memory;
+//   * B operand = the 0/1 tile, expanded from bit masks into shared memory in
+//     the 128-byte-swizzled K-major layout the MMA reads (1.0f / 0.0f);
+//   * D accumulates in TMEM (fp32), double-buffered so the epilogue of one
+//     unit overlaps the MMAs of the next.
+// Exactness: kind::tf32 multiplies 19-bit operands, so each X' element is
+// split into hi = X' with the low 13 mantissa bits cleared and lo = X' - hi
+// (exact); D += A_hi B + A_lo B. B is exactly 0 or 1, integer X is exact in
+// hi alone, and the lo term carries the rest to within 2^-21 relative.
+// Sums run in a different order than the reference (default mode: bit-exact
+// on integer X, <= 1e-5 normwise otherwise).
+//
+// Warp roles (20 warps, one CTA per SM, persistent over the units):
+//   w0      MMA issuer (one elected lane) and TMEM owner (512 columns)
+//   w1, w2  B expanders: chunk masks -> swizzled 0/1 tiles (64 rows each)
+//   w4-w15  three producer sets of four warps (one per TMEM lane quarter);
+//           set j fills the X' stages of chunks g = j mod 3
+//   w16-w19 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
+//           adds the cold entries and applies the row scale on top)
+// Stages: 4 X'/B stages (64 TMEM columns + 16 KB smem each), 2 accumulators
+// (128 TMEM columns each): 4 * 64 + 2 * 128 = 512 columns.
+#include <algorithm>
+#include <cstdint>
+
+#include "cuda_common.hpp"
+#include "dense_layout.hpp"
+
+namespace cbmb {
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kSets = 3;
+constexpr int kWarps = 20;
+constexpr int kThreads = kWarps * 32;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kAccCol = 0;       // two accumulators: columns [0,128), [128,256)
+constexpr uint32_t kStageCol = 256;   // stage s: [256 + 64 s, 256 + 64 s + 64): hi | lo
+constexpr uint32_t kBBytes = kDenseRows * kDenseK * 4;  // 16 KB per B stage
+
+struct DenseParams {
+  const float* __restrict__ x;
+  long long ldx;
+  float* y;
+  long long ldy;
+  const float* __restrict__ scale;     // normalized: per-column scale, else null
+  const uint4* __restrict__ tiles;     // row0, rows, first chunk, chunks
+  const uint32_t* __restrict__ cols;   // kDenseK per chunk
+  const uint32_t* __restrict__ masks;  // kDenseRows per chunk
+  uint32_t n_units;                    // tiles x feature blocks
+  uint32_t n_fb;                       // feature blocks of kDenseFeat
+  uint32_t d;
+};
+
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(saddr(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   saddr(b))
+               : "memory");
+}
+// K-major operand, 128-byte rows, 128-byte swizzle (8-row groups 1024 B apart)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_byte_addr) {
+  return uint64_t((smem_byte_addr & 0x3FFFF) >> 4) | (uint64_t(1) << 16) |
+         (uint64_t(1024 >> 4) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+#define R32(a)                                                                                   \
+  "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]),        \
+      "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]), "r"(a[14]),          \
+      "r"(a[15]), "r"(a[16]), "r"(a[17]), "r"(a[18]), "r"(a[19]), "r"(a[20]), "r"(a[21]),        \
+      "r"(a[22]), "r"(a[23]), "r"(a[24]), "r"(a[25]), "r"(a[26]), "r"(a[27]), "r"(a[28]),        \
+      "r"(a[29]), "r"(a[30]), "r"(a[31])
+#define W32(a)                                                                                   \
+  "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),            \
+      "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]),    \
+      "=r"(a[14]), "=r"(a[15]), "=r"(a[16]), "=r"(a[17]), "=r"(a[18]), "=r"(a[19]),              \
+      "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23]), "=r"(a[24]), "=r"(a[25]),              \
+      "=r"(a[26]), "=r"(a[27]), "=r"(a[28]), "=r"(a[29]), "=r"(a[30]), "=r"(a[31])
+#define ARGS32                                                                                   \
+  "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, " \
+  "%21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32}"
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], " ARGS32 ";" ::"r"(taddr), R32(r)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : W32(r)
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct __align__(8) DenseBars {
+  uint64_t xfull[kStages], xempty[kStages], bfull[kStages], bempty[kStages];
+  uint64_t accfull[2], accempty[2];
+  uint32_t tmem_base;
+};
+
+// Units are walked identically by every role: CTA b takes b, b + G, b + 2G...
+__device__ __forceinline__ uint4 unit_tile(const DenseParams& p, uint32_t u, uint32_t& fb) {
+  fb = u % p.n_fb;
+  return p.tiles[u / p.n_fb];
+}
+
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p) {
+  extern __shared__ __align__(1024) unsigned char dsmem[];
+  // B stages at the first 1024-byte boundary (the swizzle is address-based)
+  unsigned char* bstage = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  DenseBars* bars = reinterpret_cast<DenseBars*>(bstage + kStages * kBBytes);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     saddr(&bars->tmem_base)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  } else if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&bars->xfull[s], 4);
+      mbar_init(&bars->xempty[s], 1);
+      mbar_init(&bars->bfull[s], 2);
+      mbar_init(&bars->bempty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&bars->accfull[a], 1);
+      mbar_init(&bars->accempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = bars->tmem_base;
+  const uint32_t G = gridDim.x;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((kDenseRows >> 3) << 17) |
+                           ((kDenseFeat >> 4) << 24);
+    uint32_t g = 0, nacc = 0;
+    for (uint32_t u = blockIdx.x; u < p.n_units; u += G) {
+      uint32_t fb;
+      const uint4 t = unit_tile(p, u, fb);
+      if (t.w == 0) continue;
+      const uint32_t a = nacc & 1;
+      mbar_wait(&bars->accempty[a], ((nacc >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (uint32_t j = 0; j < t.w; ++j, ++g) {
+        const uint32_t s = g % kStages, ph = (g / kStages) & 1;
+        mbar_wait(&bars->xfull[s], ph);
+        mbar_wait(&bars->bfull[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint64_t bdesc = sw128_desc(saddr(bstage + s * kBBytes));
+#pragma unroll
+          for (uint32_t piece = 0; piece < 2; ++piece)
+#pragma unroll
+            for (uint32_t ks = 0; ks < kDenseK / 8; ++ks)
+              mma_tf32(tb + kAccCol + 128 * a, tb + kStageCol + 64 * s + 32 * piece + 8 * ks,
+                       bdesc + 2 * ks, idesc, (j | piece | ks) != 0);
+          tc_commit(&bars->xempty[s]);
+          tc_commit(&bars->bempty[s]);
+          if (j + 1 == t.w) tc_commit(&bars->accfull[a]);
+        }
+        __syncwarp();
+      }
+      ++nacc;
+    }
+  } else if (warp == 1 || warp == 2) {
+    // ------------------------------------------------------------ B expanders
+    const uint32_t e = warp - 1;  // rows [64 e, 64 e + 64)
+    uint32_t g = 0;
+    for (uint32_t u = blockIdx.x; u < p.n_units; u += G) {
+      uint32_t fb;
+      const uint4 t = unit_tile(p, u, fb);
+      for (uint32_t j = 0; j < t.w; ++j, ++g) {
+        const uint32_t s = g % kStages, ph = (g / kStages) & 1;
+        const uint32_t* mk = p.masks + size_t(t.z + j) * kDenseRows + 64 * e;
+        const uint32_t m0 = mk[lane], m1 = mk[32 + lane];
+        mbar_wait(&bars->bempty[s], ph ^ 1);
+        unsigned char* bs = bstage + s * kBBytes;
+#pragma unroll 4
+        for (uint32_t it = 0; it < 16; ++it) {
+          const uint32_t item = it * 32 + lane, rl = item >> 3, q = item & 7;
+          const uint32_t mask = __shfl_sync(0xFFFFFFFFu, it < 8 ? m0 : m1, rl & 31);
+          const uint32_t bits = mask >> (4 * q);
+          const float4 v = make_float4((bits & 1) ? 1.f : 0.f, (bits & 2) ? 1.f : 0.f,
+                                       (bits & 4) ? 1.f : 0.f, (bits & 8) ? 1.f : 0.f);
+          const uint32_t r = 64 * e + rl;
+          *reinterpret_cast<float4*>(bs + (r >> 3) * 1024 + (r & 7) * 128 +
+                                     ((q ^ (r & 7)) << 4)) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->bfull[s]);
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + 4 * kSets) {
+    // ------------------------------------------------------------ X' producers
+    const uint32_t set = (warp - 4) / 4, quarter = warp & 3;
+    uint32_t g = 0;
+    for (uint32_t u = blockIdx.x; u < p.n_units; u += G) {
+      uint32_t fb;
+      const uint4 t = unit_tile(p, u, fb);
+      const uint32_t f = fb * kDenseFeat + quarter * 32 + lane;
+      const bool live = f < p.d;
+      for (uint32_t j = 0; j < t.w; ++j, ++g) {
+        if (g % kSets != set) continue;
+        const uint32_t s = g % kStages, ph = (g / kStages) & 1;
+        const uint32_t mycol = p.cols[size_t(t.z + j) * kDenseK + lane];
+        float mysc = 1.f;
+        if constexpr (NORM) mysc = p.scale[mycol];
+        uint32_t hi[32], lo[32];
+        float v[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycol, k);
+          v[k] = live ? __ldg(p.x + (long long)c * p.ldx + f) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          float w = v[k];
+          if constexpr (NORM) w = __fmul_rn(w, __shfl_sync(0xFFFFFFFFu, mysc, k));
+          hi[k] = __float_as_uint(w) & 0xFFFFE000u;
+          lo[k] = __float_as_uint(__fsub_rn(w, __uint_as_float(hi[k])));
+        }
+        mbar_wait(&bars->xempty[s], ph ^ 1);
+        tc_fence_after();
+        const uint32_t taddr = tb + ((quarter * 32) << 16) + kStageCol + 64 * s;
+        tmem_st32(taddr, hi);
+        tmem_st32(taddr + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->xfull[s]);
+      }
+    }
+  } else if (warp >= 16) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t quarter = warp & 3;
+    uint32_t nacc = 0;
+    for (uint32_t u = blockIdx.x; u < p.n_units; u += G) {
+      uint32_t fb;
+      const uint4 t = unit_tile(p, u, fb);
+      const uint32_t f = fb * kDenseFeat + quarter * 32 + lane;
+      const bool live = f < p.d;
+      float* ybase = p.y + (long long)t.x * p.ldy + f;
+      if (t.w == 0) {  // no shared columns: the dense part is zero
+        if (live)
+          for (uint32_t r = 0; r < t.y; ++r) ybase[(long long)r * p.ldy] = 0.f;
+        continue;
+      }
+      const uint32_t a = nacc & 1;
+      mbar_wait(&bars->accfull[a], (nacc >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (uint32_t c0 = 0; c0 < kDenseRows; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tb + ((quarter * 32) << 16) + kAccCol + 128 * a + c0, r);
+        if (c0 + 32 == kDenseRows) {  // accumulator drained: the MMA may reuse it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->accempty[a]);
+        }
+        if (live) {
+#pragma unroll
+          for (uint32_t j = 0; j < 32; ++j)
+            if (c0 + j < t.y) ybase[(long long)(c0 + j) * p.ldy] = __uint_as_float(r[j]);
+        }
+      }
+      ++nacc;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+}  // namespace
+
+void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
+                int64_t ldy, cudaStream_t s) {
+  const DenseLayout& D = h->dense;
+  DenseParams p;
+  p.x = x;
+  p.ldx = ldx;
+  p.y = y;
+  p.ldy = ldy;
+  p.scale = h->info.normalized ? h->scale : nullptr;
+  p.tiles = reinterpret_cast<const uint4*>(h->dtiles);
+  p.cols = h->dcols;
+  p.masks = h->dmasks;
+  p.n_fb = (d + kDenseFeat - 1) / kDenseFeat;
+  p.d = d;
+  const uint64_t units = uint64_t(D.n_tiles) * p.n_fb;
+  if (units >= 0xFFFFFFFFull) throw invalid_argument("spmm: too many dense-block units");
+  p.n_units = uint32_t(units);
+  const size_t smem = 1024 + kStages * kBBytes + sizeof(DenseBars);
+  const int grid = int(std::min<uint64_t>(units, uint64_t(h->num_sms)));
+  if (grid == 0) return;
+  if (h->info.normalized) {
+    ck(cudaFuncSetAttribute(dense_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smem)), "dense smem");
+    dense_kernel<true><<<grid, kThreads, smem, s>>>(p);
+  } else {
+    ck(cudaFuncSetAttribute(dense_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smem)), "dense smem");
+    dense_kernel<false><<<grid, kThreads, smem, s>>>(p);
+  }
+  ck(cudaGetLastError(), "dense_kernel launch");
+}
+
+}  // namespace cbmb

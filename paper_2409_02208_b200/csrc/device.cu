@@ -55,8 +55,45 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       }
       put(h->dval, dval, "upload dval");
     }
+    // dense-block path (default mode): the tensor cores take the columns each
+    // 128-row tile shares, a streaming operator the rest
+    if (!L.order_faithful && opt.dense != 0 && v.n_rows > 0) {
+      DenseLayout D = plan_dense(v, opt.dense_min);
+      if (opt.dense == 1 && !D.ok)
+        throw invalid_argument("upload: the dense-block path needs delta rows consistent "
+                               "with their parents' rows");
+      // cost in gather-equivalents (one X row slice per gathered entry): a
+      // chunk loads its 32 X rows once and runs 8 MMAs (~45 gathers' time),
+      // the cold entries are gathered; the streaming kernel gathers every
+      // effective entry
+      const double dense_cost = double(D.cold_entries) + 45.0 * double(D.n_chunks);
+      h->dense_on = D.ok && (opt.dense == 1 || dense_cost < 0.85 * double(L.nnz_effective));
+      if (h->dense_on) {
+        put(h->dtiles, D.tiles, "upload dense tiles");
+        put(h->dcols, D.cols, "upload dense cols");
+        put(h->dmasks, D.masks, "upload dense masks");
+        cbm_b200_cbm_view cv{v.n_rows, v.n_cols, D.cold_entries, v.alpha, v.is_normalized,
+                             D.cold_parent.data(), nullptr, D.cold_row_ptr.data(),
+                             D.cold_col.data(), D.cold_val.data(), v.row_scale};
+        cbm_b200_options co = opt;
+        co.order_faithful = 0;
+        co.tile = 0;
+        co.dense = 0;
+        co.flatten_gain = 0;
+        h->cold = device_upload(cv, co);
+        h->device_bytes += h->cold->device_bytes;
+      }
+      D.tiles = {};
+      D.cols = {};
+      D.masks = {};
+      D.cold_parent = {};
+      D.cold_row_ptr = {};
+      D.cold_col = {};
+      D.cold_val = {};
+      h->dense = std::move(D);
+    }
     // tiled path (default mode): planned here, kept only when it pays
-    if (!L.order_faithful && opt.tile != 0 && v.n_rows > 0) {
+    if (!L.order_faithful && opt.tile != 0 && v.n_rows > 0 && !h->dense_on) {
       TileLayout T;
       bool planned = true;
       try {
@@ -129,6 +166,9 @@ void device_free(DeviceMatrix* h) {
       if (p) cudaFree(p);
   for (auto& kv : h->ws)
     if (kv.second.tinterior) cudaFree(kv.second.tinterior);
+  if (h->cold) device_free(h->cold);
+  for (void* p : {(void*)h->dtiles, (void*)h->dcols, (void*)h->dmasks})
+    if (p) cudaFree(p);
   for (void* p : {(void*)h->dcol, (void*)h->dval, (void*)h->rec, (void*)h->srow, (void*)h->scale,
                   (void*)h->xstage, (void*)h->ystage, (void*)h->tdcol, (void*)h->tdval,
                   (void*)h->trow, (void*)h->tblock, (void*)h->tstage})
@@ -156,6 +196,7 @@ void device_reserve(DeviceMatrix* h, uint64_t d, void* stream) {
                          "workspace interior");
   if (h->tile_on) grow(ws.tinterior, ws.tinterior_cap, uint64_t(h->tile.n_interior) * dpad,
                        "workspace tile interior");
+  if (h->cold) device_reserve(h->cold, d, stream);
 }
 
 // Host-buffer entry point. Columns are independent (kernels.cpp:27-62), so X

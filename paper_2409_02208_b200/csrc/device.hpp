@@ -13,6 +13,7 @@
 
 #include "errors.hpp"
 #include "layout.hpp"
+#include "dense_layout.hpp"
 #include "tile_layout.hpp"
 
 namespace cbmb {
@@ -41,6 +42,14 @@ struct DeviceMatrix {
   uint32_t* tblock = nullptr;
   uint32_t* tstage = nullptr;
   std::map<uint64_t, uint32_t> tile_main;  // (W, slabs) -> full-width units of the launch
+  // dense-block path (dense_layout.hpp): sizes in `dense` (host vectors
+  // released); the cold entries are their own streaming-kernel operator
+  bool dense_on = false;
+  DenseLayout dense;
+  uint32_t* dtiles = nullptr;
+  uint32_t* dcols = nullptr;
+  uint32_t* dmasks = nullptr;
+  struct DeviceMatrix* cold = nullptr;
   // per-call workspace, one per stream (concurrent calls on distinct streams
   // never share flags or scratch); grown on demand, or by cbm_b200_reserve
   struct Workspace {
@@ -84,8 +93,15 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
 void device_free(DeviceMatrix* h);
 void device_reserve(DeviceMatrix* h, uint64_t d, void* stream);
 // Y = A X; x/y are device pointers; d = columns. Shapes already validated.
+// base (optional, n_rows x d, leading dimension ldbase; may alias y): added to
+// every row's unscaled sum before the row scale (the dense-block path's
+// tensor-core part under the cold entries).
 void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
-                 int64_t ldy, void* stream, bool relu = false);
+                 int64_t ldy, void* stream, bool relu = false, const float* base = nullptr,
+                 int64_t ldbase = 0);
+inline constexpr uint32_t kDenseMinD = 32;  // narrower X stays on the streaming kernel
+void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
+                int64_t ldy, cudaStream_t s);
 void device_dense_matmul(const float* a, uint32_t m, uint32_t k, const float* b, uint32_t n,
                          float* c, void* stream);
 void device_fast_matmul(const float* a, uint32_t m, uint32_t k, const float* b, uint32_t n,
