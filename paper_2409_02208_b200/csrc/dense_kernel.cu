@@ -23,7 +23,8 @@
 //
 // Warp roles (20 warps, one CTA per SM, persistent over the units):
 //   w0      MMA issuer (one elected lane) and TMEM owner (512 columns)
-//   w1, w2  B expanders: chunk masks -> swizzled 0/1 tiles (64 rows each)
+//   w1-w3   B expanders: chunk masks -> swizzled 0/1 tiles (expander e owns
+//           chunks g = e mod 3, prefetching the next one's masks)
 //   w4-w15  three producer sets of four warps (one per TMEM lane quarter);
 //           set j fills the X' stages of chunks g = j mod 3
 //   w16-w19 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
@@ -42,6 +43,7 @@ namespace {
 
 constexpr int kStages = 4;
 constexpr int kSets = 3;
+constexpr int kExpanders = 3;
 constexpr int kWarps = 20;
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kTmemCols = 512;
@@ -152,6 +154,47 @@ __device__ __forceinline__ uint4 unit_tile(const DenseParams& p, uint32_t u, uin
   return p.tiles[u / p.n_fb];
 }
 
+// The CTA's chunk sequence (units b, b + G, ...; their chunks in order),
+// restricted to the chunks g with g % stride == phase: lets a role that owns
+// every stride-th chunk look one chunk ahead (prefetch) without replaying the
+// unit walk by hand.
+struct ChunkIter {
+  uint32_t u, j, g;      // current unit, chunk within it, global chunk counter
+  uint4 t;               // current unit's tile record
+  uint32_t fb;
+  bool done;
+  __device__ void load(const DenseParams& p) {
+    done = u >= p.n_units;
+    if (!done) t = unit_tile(p, u, fb);
+  }
+  __device__ void init(const DenseParams& p, uint32_t phase, uint32_t stride) {
+    u = blockIdx.x;
+    j = 0;
+    g = 0;
+    load(p);
+    skip(p, phase, stride);
+  }
+  // advance to the next position whose g matches (phase mod stride)
+  __device__ void skip(const DenseParams& p, uint32_t phase, uint32_t stride) {
+    while (!done) {
+      if (j >= t.w) {
+        u += gridDim.x;
+        j = 0;
+        load(p);
+        continue;
+      }
+      if (g % stride == phase) return;
+      ++j;
+      ++g;
+    }
+  }
+  __device__ void next(const DenseParams& p, uint32_t phase, uint32_t stride) {
+    ++j;
+    ++g;
+    skip(p, phase, stride);
+  }
+};
+
 template <bool NORM>
 __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p) {
   extern __shared__ __align__(1024) unsigned char dsmem[];
@@ -171,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&bars->xfull[s], 4);
       mbar_init(&bars->xempty[s], 1);
-      mbar_init(&bars->bfull[s], 2);
+      mbar_init(&bars->bfull[s], 1);
       mbar_init(&bars->bempty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -220,74 +263,94 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       }
       ++nacc;
     }
-  } else if (warp == 1 || warp == 2) {
+  } else if (warp >= 1 && warp < 1 + kExpanders) {
     // ------------------------------------------------------------ B expanders
-    const uint32_t e = warp - 1;  // rows [64 e, 64 e + 64)
-    uint32_t g = 0;
-    for (uint32_t u = blockIdx.x; u < p.n_units; u += G) {
-      uint32_t fb;
-      const uint4 t = unit_tile(p, u, fb);
-      for (uint32_t j = 0; j < t.w; ++j, ++g) {
-        const uint32_t s = g % kStages, ph = (g / kStages) & 1;
-        const uint32_t* mk = p.masks + size_t(t.z + j) * kDenseRows + 64 * e;
-        const uint32_t m0 = mk[lane], m1 = mk[32 + lane];
-        mbar_wait(&bars->bempty[s], ph ^ 1);
-        unsigned char* bs = bstage + s * kBBytes;
-#pragma unroll 4
-        for (uint32_t it = 0; it < 16; ++it) {
-          const uint32_t item = it * 32 + lane, rl = item >> 3, q = item & 7;
-          const uint32_t mask = __shfl_sync(0xFFFFFFFFu, it < 8 ? m0 : m1, rl & 31);
-          const uint32_t bits = mask >> (4 * q);
-          const float4 v = make_float4((bits & 1) ? 1.f : 0.f, (bits & 2) ? 1.f : 0.f,
-                                       (bits & 4) ? 1.f : 0.f, (bits & 8) ? 1.f : 0.f);
-          const uint32_t r = 64 * e + rl;
-          *reinterpret_cast<float4*>(bs + (r >> 3) * 1024 + (r & 7) * 128 +
-                                     ((q ^ (r & 7)) << 4)) = v;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->bfull[s]);
+    // expander e owns chunks g = e mod kExpanders, all 128 rows; the masks of
+    // its next chunk are loaded before it waits for the current stage
+    const uint32_t e = warp - 1;
+    ChunkIter it;
+    it.init(p, e, kExpanders);
+    uint32_t mk[4];
+    if (!it.done) {
+      const uint32_t* src = p.masks + size_t(it.t.z + it.j) * kDenseRows;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mk[i] = __ldg(src + 32 * i + lane);
+    }
+    while (!it.done) {
+      const uint32_t s = it.g % kStages, ph = (it.g / kStages) & 1;
+      uint32_t cur[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cur[i] = mk[i];
+      it.next(p, e, kExpanders);
+      if (!it.done) {
+        const uint32_t* src = p.masks + size_t(it.t.z + it.j) * kDenseRows;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mk[i] = __ldg(src + 32 * i + lane);
       }
+      mbar_wait(&bars->bempty[s], ph ^ 1);
+      unsigned char* bs = bstage + s * kBBytes;
+#pragma unroll
+      for (uint32_t k = 0; k < 32; ++k) {
+        // item = 32 k + lane: row r = item / 8 (4 rows per k), 16-byte chunk q
+        const uint32_t r = 4 * k + (lane >> 3), q = lane & 7;
+        const uint32_t mask = __shfl_sync(0xFFFFFFFFu, cur[k >> 3], r & 31);
+        const uint32_t bits = mask >> (4 * q);
+        const float4 v = make_float4((bits & 1) ? 1.f : 0.f, (bits & 2) ? 1.f : 0.f,
+                                     (bits & 4) ? 1.f : 0.f, (bits & 8) ? 1.f : 0.f);
+        *reinterpret_cast<float4*>(bs + (r >> 3) * 1024 + (r & 7) * 128 +
+                                   ((q ^ (r & 7)) << 4)) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->bfull[s]);
     }
   } else if (warp >= 4 && warp < 4 + 4 * kSets) {
     // ------------------------------------------------------------ X' producers
+    // set j owns chunks g = j mod kSets; the next chunk's column list (and
+    // scales) is fetched before the current chunk's X' rows are converted
     const uint32_t set = (warp - 4) / 4, quarter = warp & 3;
-    uint32_t g = 0;
-    for (uint32_t u = blockIdx.x; u < p.n_units; u += G) {
-      uint32_t fb;
-      const uint4 t = unit_tile(p, u, fb);
-      const uint32_t f = fb * kDenseFeat + quarter * 32 + lane;
+    ChunkIter it;
+    it.init(p, set, kSets);
+    uint32_t ncol = 0;
+    float nsc = 1.f;
+    if (!it.done) {
+      ncol = __ldg(p.cols + size_t(it.t.z + it.j) * kDenseK + lane);
+      if constexpr (NORM) nsc = __ldg(p.scale + ncol);
+    }
+    while (!it.done) {
+      const uint32_t s = it.g % kStages, ph = (it.g / kStages) & 1;
+      const uint32_t f = it.fb * kDenseFeat + quarter * 32 + lane;
       const bool live = f < p.d;
-      for (uint32_t j = 0; j < t.w; ++j, ++g) {
-        if (g % kSets != set) continue;
-        const uint32_t s = g % kStages, ph = (g / kStages) & 1;
-        const uint32_t mycol = p.cols[size_t(t.z + j) * kDenseK + lane];
-        float mysc = 1.f;
-        if constexpr (NORM) mysc = p.scale[mycol];
-        uint32_t hi[32], lo[32];
-        float v[32];
+      const uint32_t mycol = ncol;
+      const float mysc = nsc;
+      float v[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycol, k);
-          v[k] = live ? __ldg(p.x + (long long)c * p.ldx + f) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          float w = v[k];
-          if constexpr (NORM) w = __fmul_rn(w, __shfl_sync(0xFFFFFFFFu, mysc, k));
-          hi[k] = __float_as_uint(w) & 0xFFFFE000u;
-          lo[k] = __float_as_uint(__fsub_rn(w, __uint_as_float(hi[k])));
-        }
-        mbar_wait(&bars->xempty[s], ph ^ 1);
-        tc_fence_after();
-        const uint32_t taddr = tb + ((quarter * 32) << 16) + kStageCol + 64 * s;
-        tmem_st32(taddr, hi);
-        tmem_st32(taddr + 32, lo);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->xfull[s]);
+      for (int k = 0; k < 32; ++k) {
+        const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycol, k);
+        v[k] = live ? __ldg(p.x + (long long)c * p.ldx + f) : 0.f;
       }
+      it.next(p, set, kSets);
+      if (!it.done) {
+        ncol = __ldg(p.cols + size_t(it.t.z + it.j) * kDenseK + lane);
+        if constexpr (NORM) nsc = __ldg(p.scale + ncol);
+      }
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        float w = v[k];
+        if constexpr (NORM) w = __fmul_rn(w, __shfl_sync(0xFFFFFFFFu, mysc, k));
+        hi[k] = __float_as_uint(w) & 0xFFFFE000u;
+        lo[k] = __float_as_uint(__fsub_rn(w, __uint_as_float(hi[k])));
+      }
+      mbar_wait(&bars->xempty[s], ph ^ 1);
+      tc_fence_after();
+      const uint32_t taddr = tb + ((quarter * 32) << 16) + kStageCol + 64 * s;
+      tmem_st32(taddr, hi);
+      tmem_st32(taddr + 32, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->xfull[s]);
     }
   } else if (warp >= 16) {
     // ------------------------------------------------------------ epilogue

@@ -75,6 +75,14 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
       dense.clear();
       for (uint32_t c : touched)
         if (cnt[c] >= mc) dense.push_back(c);
+      if (dense.size() > size_t(kDenseMaxChunks) * kDenseK) {
+        // a tile holding a hub row shares thousands of columns with it: keep
+        // the most shared ones (one CTA multiplies a whole unit, so a long
+        // unit would serialise the launch), the rest stay cold
+        std::stable_sort(dense.begin(), dense.end(),
+                         [&](uint32_t a, uint32_t b) { return cnt[a] > cnt[b]; });
+        dense.resize(size_t(kDenseMaxChunks) * kDenseK);
+      }
       std::sort(dense.begin(), dense.end());
       const uint32_t nch = uint32_t((dense.size() + kDenseK - 1) / kDenseK);
       P.cols.assign(size_t(nch) * kDenseK, 0);

@@ -16,6 +16,7 @@ namespace cbmb {
 inline constexpr uint32_t kDenseRows = 128;  // rows per tile (the MMA's N)
 inline constexpr uint32_t kDenseK = 32;      // columns per chunk (4 tf32 K-steps of 8)
 inline constexpr uint32_t kDenseFeat = 128;  // features per work unit (the MMA's M)
+inline constexpr uint32_t kDenseMaxChunks = 64;  // chunks per tile at most (load balance)
 
 struct DenseLayout {
   bool ok = false;                // planned (consistent rows, not order-faithful)

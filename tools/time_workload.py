@@ -39,12 +39,21 @@ def main():
                                                    c.row_scale)).spmm(x_np, os.cpu_count())
     s = torch.cuda.current_stream()
     for opts in sets:
+        opts = dict(opts)
+        slab = int(opts.pop("_slab", 0))   # > 0: one launch per column slab of this width
         t0 = time.time()
         op = P.DeviceCbm(c, device=0, **opts)
+
+        def mult():
+            if slab <= 0:
+                op.spmm_into(x, y, s)
+            else:
+                for lo in range(0, wl.d, slab):
+                    op.spmm_into(x[:, lo:lo + slab], y[:, lo:lo + slab], s)
         t_up = time.time() - t0
-        op.spmm_into(x, y, s)
+        mult()
         torch.cuda.synchronize()
-        out = {"workload": name, "opts": opts, "build_s": t_build, "upload_s": t_up}
+        out = {"workload": name, "opts": opts, "slab": slab, "build_s": t_build, "upload_s": t_up}
         if want is not None:
             out["parity"] = O.judge_parity(
                 y.cpu().numpy(), want, 1e-5,
@@ -56,7 +65,7 @@ def main():
             flush.fill_(float(i))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            op.spmm_into(x, y, s)
+            mult()
             e1.record(s)
             torch.cuda.synchronize()
             if i >= 2:
