@@ -57,7 +57,9 @@ struct Vec<1> {
   static __device__ __forceinline__ T zero() { return 0.0f; }
   static __device__ __forceinline__ T ldg(const float* p) { return __ldg(p); }
   static __device__ __forceinline__ T ldcg(const float* p) { return __ldcg(p); }
+  static __device__ __forceinline__ T ldcs(const float* p) { return __ldcs(p); }
   static __device__ __forceinline__ void st(float* p, T v) { *p = v; }
+  static __device__ __forceinline__ void stcs(float* p, T v) { __stcs(p, v); }
   static __device__ __forceinline__ T add(T a, T b) { return __fadd_rn(a, b); }
   static __device__ __forceinline__ T sub(T a, T b) { return __fsub_rn(a, b); }
   static __device__ __forceinline__ T mul(T a, float s) { return __fmul_rn(a, s); }
@@ -73,6 +75,12 @@ struct Vec<2> {
     return __ldcg(reinterpret_cast<const float2*>(p));
   }
   static __device__ __forceinline__ void st(float* p, T v) { *reinterpret_cast<float2*>(p) = v; }
+  static __device__ __forceinline__ T ldcs(const float* p) {
+    return __ldcs(reinterpret_cast<const float2*>(p));
+  }
+  static __device__ __forceinline__ void stcs(float* p, T v) {
+    __stcs(reinterpret_cast<float2*>(p), v);
+  }
   static __device__ __forceinline__ T add(T a, T b) {
     return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
   }
@@ -94,6 +102,12 @@ struct Vec<4> {
     return __ldcg(reinterpret_cast<const float4*>(p));
   }
   static __device__ __forceinline__ void st(float* p, T v) { *reinterpret_cast<float4*>(p) = v; }
+  static __device__ __forceinline__ T ldcs(const float* p) {
+    return __ldcs(reinterpret_cast<const float4*>(p));
+  }
+  static __device__ __forceinline__ void stcs(float* p, T v) {
+    __stcs(reinterpret_cast<float4*>(p), v);
+  }
   static __device__ __forceinline__ T add(T a, T b) {
     return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
                        __fadd_rn(a.w, b.w));
@@ -709,7 +723,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
       T4 bv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        bv[u] = col + uint32_t(u) * kSeg < p.d ? W::ldcg(src + col + u * kSeg) : W::zero();
+        bv[u] = col + uint32_t(u) * kSeg < p.d ? W::ldcs(src + col + u * kSeg) : W::zero();
 #pragma unroll
       for (int u = 0; u < U; ++u) acc[u] = W::add(acc[u], bv[u]);
     }
@@ -729,13 +743,17 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
         if (writer && col + uint32_t(u) * kSeg < p.d) {
           T4 yv = W::mul(acc[u], sr);
           if (p.relu) yv = relu_v<V>(yv);
-          W::st(yrow + col + u * kSeg, yv);
+          // (dense-block path: Y is final here and X should keep its L2 lines)
+          if (p.base) W::stcs(yrow + col + u * kSeg, yv);
+          else W::st(yrow + col + u * kSeg, yv);
         }
     } else {
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (writer && col + uint32_t(u) * kSeg < p.d)
-          W::st(yrow + col + u * kSeg, p.relu ? relu_v<V>(acc[u]) : acc[u]);
+        if (writer && col + uint32_t(u) * kSeg < p.d) {
+          if (p.base) W::stcs(yrow + col + u * kSeg, p.relu ? relu_v<V>(acc[u]) : acc[u]);
+          else W::st(yrow + col + u * kSeg, p.relu ? relu_v<V>(acc[u]) : acc[u]);
+        }
       if (is_parent) publish(flag_base + t, p.epoch);
     }
   }

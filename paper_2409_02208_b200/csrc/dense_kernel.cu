@@ -33,6 +33,7 @@
 // (128 TMEM columns each): 4 * 64 + 2 * 128 = 512 columns.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "cuda_common.hpp"
 #include "dense_layout.hpp"
@@ -63,6 +64,7 @@ struct DenseParams {
   uint32_t n_units;                    // tiles x feature blocks
   uint32_t n_fb;                       // feature blocks of kDenseFeat
   uint32_t d;
+  uint32_t dbg;  // dev A/B only (CBM_B200_DENSE_DBG): 1 no X loads, 2 no MMAs, 4 no B fill
 };
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
         mbar_wait(&bars->xfull[s], ph);
         mbar_wait(&bars->bfull[s], ph);
         tc_fence_after();
-        if (lane == 0) {
+        if (lane == 0 && !(p.dbg & 2)) {
           const uint64_t bdesc = sw128_desc(saddr(bstage + s * kBBytes));
 #pragma unroll
           for (uint32_t piece = 0; piece < 2; ++piece)
@@ -258,6 +260,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
           tc_commit(&bars->xempty[s]);
           tc_commit(&bars->bempty[s]);
           if (j + 1 == t.w) tc_commit(&bars->accfull[a]);
+        } else if (lane == 0) {
+          mbar_arrive(&bars->xempty[s]);
+          mbar_arrive(&bars->bempty[s]);
+          if (j + 1 == t.w) mbar_arrive(&bars->accfull[a]);
         }
         __syncwarp();
       }
@@ -290,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       mbar_wait(&bars->bempty[s], ph ^ 1);
       unsigned char* bs = bstage + s * kBBytes;
 #pragma unroll
-      for (uint32_t k = 0; k < 32; ++k) {
+      for (uint32_t k = 0; k < (p.dbg & 4 ? 0u : 32u); ++k) {
         // item = 32 k + lane: row r = item / 8 (4 rows per k), 16-byte chunk q
         const uint32_t r = 4 * k + (lane >> 3), q = lane & 7;
         const uint32_t mask = __shfl_sync(0xFFFFFFFFu, cur[k >> 3], r & 31);
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycol, k);
-        v[k] = live ? __ldg(p.x + (long long)c * p.ldx + f) : 0.f;
+        v[k] = live && !(p.dbg & 1) ? __ldg(p.x + (long long)c * p.ldx + f) : 0.f;
       }
       it.next(p, set, kSets);
       if (!it.done) {
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       float* ybase = p.y + (long long)t.x * p.ldy + f;
       if (t.w == 0) {  // no shared columns: the dense part is zero
         if (live)
-          for (uint32_t r = 0; r < t.y; ++r) ybase[(long long)r * p.ldy] = 0.f;
+          for (uint32_t r = 0; r < t.y; ++r) __stcs(ybase + (long long)r * p.ldy, 0.f);
         continue;
       }
       const uint32_t a = nacc & 1;
@@ -382,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
         if (live) {
 #pragma unroll
           for (uint32_t j = 0; j < 32; ++j)
-            if (c0 + j < t.y) ybase[(long long)(c0 + j) * p.ldy] = __uint_as_float(r[j]);
+            if (c0 + j < t.y) __stcs(ybase + (long long)(c0 + j) * p.ldy, __uint_as_float(r[j]));
         }
       }
       ++nacc;
@@ -414,6 +420,8 @@ void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float*
   p.masks = h->dmasks;
   p.n_fb = (d + kDenseFeat - 1) / kDenseFeat;
   p.d = d;
+  p.dbg = 0;
+  if (const char* e = std::getenv("CBM_B200_DENSE_DBG")) p.dbg = uint32_t(std::atoi(e));
   const uint64_t units = uint64_t(D.n_tiles) * p.n_fb;
   if (units >= 0xFFFFFFFFull) throw invalid_argument("spmm: too many dense-block units");
   p.n_units = uint32_t(units);

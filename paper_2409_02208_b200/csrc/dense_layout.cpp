@@ -118,12 +118,22 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
   std::vector<uint32_t>().swap(fcol);
   std::vector<uint64_t>().swap(fptr);
 
-  // tiles in schedule order: most chunks first (static round-robin over CTAs)
+  // tiles in schedule order (static round-robin over CTAs): the heavy tiles
+  // (more than twice the mean chunk count) first, then the rest in row
+  // order, so that neighbouring tiles, which share X rows, run at the same
+  // time and meet those rows in L2
   std::vector<uint32_t> order(D.n_tiles);
   std::iota(order.begin(), order.end(), 0u);
-  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-    return plans[a].cols.size() > plans[b].cols.size();
-  });
+  {
+    uint64_t total = 0;
+    for (const auto& P : plans) total += P.cols.size();
+    const double heavy = 2.0 * double(total) / double(std::max<uint32_t>(1, D.n_tiles));
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+      const bool ha = double(plans[a].cols.size()) > heavy, hb = double(plans[b].cols.size()) > heavy;
+      if (ha != hb) return ha;
+      return ha ? plans[a].cols.size() > plans[b].cols.size() : false;
+    });
+  }
   D.tiles.reserve(size_t(D.n_tiles) * 4);
   for (uint32_t t : order) {
     const TilePlan& P = plans[t];

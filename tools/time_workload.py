@@ -41,6 +41,8 @@ def main():
     for opts in sets:
         opts = dict(opts)
         slab = int(opts.pop("_slab", 0))   # > 0: one launch per column slab of this width
+        for k, v in opts.pop("_env", {}).items():   # dev env switches read per launch
+            os.environ[k] = str(v)
         t0 = time.time()
         op = P.DeviceCbm(c, device=0, **opts)
 
