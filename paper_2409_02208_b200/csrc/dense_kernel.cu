@@ -21,13 +21,16 @@
 // Sums run in a different order than the reference (default mode: bit-exact
 // on integer X, <= 1e-5 normwise otherwise).
 //
-// Warp roles (20 warps, one CTA per SM, persistent over the units):
+// Warp roles (24 warps, one CTA per SM, persistent over the units):
 //   w0      MMA issuer (one elected lane) and TMEM owner (512 columns)
-//   w1-w3   B expanders: chunk masks -> swizzled 0/1 tiles (expander e owns
-//           chunks g = e mod 3, prefetching the next one's masks)
-//   w4-w15  three producer sets of four warps (one per TMEM lane quarter);
-//           set j fills the X' stages of chunks g = j mod 3
-//   w16-w19 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
+//   w1      metadata loader: each chunk's record (32 columns, their scales,
+//           128 row masks; 768 B) copied into an 8-deep shared-memory ring
+//           with cp.async, completion tracked by an mbarrier, so no other role
+//           waits on a dependent global load
+//   w2, w3  B expanders: row masks -> swizzled 0/1 tiles (chunks g = e mod 2)
+//   w4-w19  four producer sets of four warps (one per TMEM lane quarter);
+//           set j gathers the X' rows of chunks g = j mod 4 into stage j
+//   w20-w23 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
 //           adds the cold entries and applies the row scale on top)
 // Stages: 4 X'/B stages (64 TMEM columns + 16 KB smem each), 2 accumulators
 // (128 TMEM columns each): 4 * 64 + 2 * 128 = 512 columns.
@@ -43,9 +46,12 @@ namespace cbmb {
 namespace {
 
 constexpr int kStages = 4;
-constexpr int kSets = 3;
-constexpr int kExpanders = 3;
-constexpr int kWarps = 20;
+constexpr int kSets = 4;       // producer sets (set j owns stage j)
+constexpr int kExpanders = 2;
+constexpr int kMeta = 8;       // metadata ring depth (chunks)
+constexpr int kWarps = 24;
+constexpr int kProd0 = 4;      // first producer warp
+constexpr int kEpi0 = kProd0 + 4 * kSets;  // first epilogue warp
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAccCol = 0;       // two accumulators: columns [0,128), [128,256)
@@ -59,8 +65,7 @@ struct DenseParams {
   long long ldy;
   const float* __restrict__ scale;     // normalized: per-column scale, else null
   const uint4* __restrict__ tiles;     // row0, rows, first chunk, chunks
-  const uint32_t* __restrict__ cols;   // kDenseK per chunk
-  const uint32_t* __restrict__ masks;  // kDenseRows per chunk
+  const uint32_t* __restrict__ meta;   // kDenseMetaWords per chunk (dense_layout.hpp)
   uint32_t n_units;                    // tiles x feature blocks
   uint32_t n_fb;                       // feature blocks of kDenseFeat
   uint32_t d;
@@ -144,11 +149,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-struct __align__(8) DenseBars {
+struct __align__(16) DenseBars {
   uint64_t xfull[kStages], xempty[kStages], bfull[kStages], bempty[kStages];
   uint64_t accfull[2], accempty[2];
+  uint64_t mfull[kMeta], mempty[kMeta];
   uint32_t tmem_base;
 };
+constexpr uint32_t kMetaBytes = kDenseMetaWords * 4;
 
 // Units are walked identically by every role: CTA b takes b, b + G, b + 2G...
 __device__ __forceinline__ uint4 unit_tile(const DenseParams& p, uint32_t u, uint32_t& fb) {
@@ -203,7 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
   // B stages at the first 1024-byte boundary (the swizzle is address-based)
   unsigned char* bstage = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
-  DenseBars* bars = reinterpret_cast<DenseBars*>(bstage + kStages * kBBytes);
+  const uint32_t* meta_ring = reinterpret_cast<const uint32_t*>(bstage + kStages * kBBytes);
+  DenseBars* bars =
+      reinterpret_cast<DenseBars*>(bstage + kStages * kBBytes + kMeta * kMetaBytes);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0) {
@@ -222,6 +231,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&bars->accfull[a], 1);
       mbar_init(&bars->accempty[a], 4);
+    }
+    for (int m = 0; m < kMeta; ++m) {
+      mbar_init(&bars->mfull[m], 32);           // one cp.async arrive per loader lane
+      mbar_init(&bars->mempty[m], 4 + 1);       // the owning producer set + its expander
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -269,30 +282,40 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       }
       ++nacc;
     }
-  } else if (warp >= 1 && warp < 1 + kExpanders) {
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ metadata loader
+    ChunkIter it;
+    it.init(p, 0, 1);
+    while (!it.done) {
+      const uint32_t m = it.g % kMeta, ph = (it.g / kMeta) & 1;
+      mbar_wait(&bars->mempty[m], ph ^ 1);
+      const unsigned char* src =
+          reinterpret_cast<const unsigned char*>(p.meta + size_t(it.t.z + it.j) * kDenseMetaWords);
+      const uint32_t dst = saddr(meta_ring) + m * kMetaBytes;
+      for (uint32_t o = 16 * lane; o < kMetaBytes; o += 512)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + o), "l"(src + o)
+                     : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                       saddr(&bars->mfull[m]))
+                   : "memory");
+      it.next(p, 0, 1);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp >= 2 && warp < 2 + kExpanders) {
     // ------------------------------------------------------------ B expanders
-    // expander e owns chunks g = e mod kExpanders, all 128 rows; the masks of
-    // its next chunk are loaded before it waits for the current stage
-    const uint32_t e = warp - 1;
+    const uint32_t e = warp - 2;
     ChunkIter it;
     it.init(p, e, kExpanders);
-    uint32_t mk[4];
-    if (!it.done) {
-      const uint32_t* src = p.masks + size_t(it.t.z + it.j) * kDenseRows;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) mk[i] = __ldg(src + 32 * i + lane);
-    }
     while (!it.done) {
       const uint32_t s = it.g % kStages, ph = (it.g / kStages) & 1;
+      const uint32_t m = it.g % kMeta, mph = (it.g / kMeta) & 1;
+      mbar_wait(&bars->mfull[m], mph);
+      const uint32_t* mk = meta_ring + m * kDenseMetaWords + 2 * kDenseK;
       uint32_t cur[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) cur[i] = mk[i];
-      it.next(p, e, kExpanders);
-      if (!it.done) {
-        const uint32_t* src = p.masks + size_t(it.t.z + it.j) * kDenseRows;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) mk[i] = __ldg(src + 32 * i + lane);
-      }
+      for (int i = 0; i < 4; ++i) cur[i] = mk[32 * i + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->mempty[m]);
       mbar_wait(&bars->bempty[s], ph ^ 1);
       unsigned char* bs = bstage + s * kBBytes;
 #pragma unroll
@@ -309,56 +332,51 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->bfull[s]);
+      it.next(p, e, kExpanders);
     }
-  } else if (warp >= 4 && warp < 4 + 4 * kSets) {
+  } else if (warp >= kProd0 && warp < kEpi0) {
     // ------------------------------------------------------------ X' producers
-    // set j owns chunks g = j mod kSets; the next chunk's column list (and
-    // scales) is fetched before the current chunk's X' rows are converted
-    const uint32_t set = (warp - 4) / 4, quarter = warp & 3;
+    // set j owns the chunks g = j mod 4 (and so always stage j)
+    const uint32_t set = (warp - kProd0) / 4, quarter = warp & 3;
     ChunkIter it;
     it.init(p, set, kSets);
-    uint32_t ncol = 0;
-    float nsc = 1.f;
-    if (!it.done) {
-      ncol = __ldg(p.cols + size_t(it.t.z + it.j) * kDenseK + lane);
-      if constexpr (NORM) nsc = __ldg(p.scale + ncol);
-    }
     while (!it.done) {
       const uint32_t s = it.g % kStages, ph = (it.g / kStages) & 1;
+      const uint32_t m = it.g % kMeta, mph = (it.g / kMeta) & 1;
       const uint32_t f = it.fb * kDenseFeat + quarter * 32 + lane;
-      const bool live = f < p.d;
-      const uint32_t mycol = ncol;
-      const float mysc = nsc;
+      const bool live = f < p.d && !(p.dbg & 1);
+      mbar_wait(&bars->mfull[m], mph);
+      const uint32_t* rec = meta_ring + m * kDenseMetaWords;
       float v[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycol, k);
-        v[k] = live && !(p.dbg & 1) ? __ldg(p.x + (long long)c * p.ldx + f) : 0.f;
+      for (int k = 0; k < 32; ++k) v[k] = live ? __ldg(p.x + (long long)rec[k] * p.ldx + f) : 0.f;
+      float sc[NORM ? 32 : 1];
+      if constexpr (NORM) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) sc[k] = __uint_as_float(rec[kDenseK + k]);
       }
-      it.next(p, set, kSets);
-      if (!it.done) {
-        ncol = __ldg(p.cols + size_t(it.t.z + it.j) * kDenseK + lane);
-        if constexpr (NORM) nsc = __ldg(p.scale + ncol);
-      }
-      uint32_t hi[32], lo[32];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->mempty[m]);
+      uint32_t hi[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         float w = v[k];
-        if constexpr (NORM) w = __fmul_rn(w, __shfl_sync(0xFFFFFFFFu, mysc, k));
+        if constexpr (NORM) w = __fmul_rn(w, sc[k]);
         hi[k] = __float_as_uint(w) & 0xFFFFE000u;
-        lo[k] = __float_as_uint(__fsub_rn(w, __uint_as_float(hi[k])));
+        v[k] = __fsub_rn(w, __uint_as_float(hi[k]));   // lo, in place
       }
       mbar_wait(&bars->xempty[s], ph ^ 1);
       tc_fence_after();
       const uint32_t taddr = tb + ((quarter * 32) << 16) + kStageCol + 64 * s;
       tmem_st32(taddr, hi);
-      tmem_st32(taddr + 32, lo);
+      tmem_st32(taddr + 32, reinterpret_cast<const uint32_t(&)[32]>(v));
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->xfull[s]);
+      it.next(p, set, kSets);
     }
-  } else if (warp >= 16) {
+  } else if (warp >= kEpi0) {
     // ------------------------------------------------------------ epilogue
     const uint32_t quarter = warp & 3;
     uint32_t nacc = 0;
@@ -416,8 +434,7 @@ void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float*
   p.ldy = ldy;
   p.scale = h->info.normalized ? h->scale : nullptr;
   p.tiles = reinterpret_cast<const uint4*>(h->dtiles);
-  p.cols = h->dcols;
-  p.masks = h->dmasks;
+  p.meta = h->dmeta;
   p.n_fb = (d + kDenseFeat - 1) / kDenseFeat;
   p.d = d;
   p.dbg = 0;
@@ -425,7 +442,7 @@ void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float*
   const uint64_t units = uint64_t(D.n_tiles) * p.n_fb;
   if (units >= 0xFFFFFFFFull) throw invalid_argument("spmm: too many dense-block units");
   p.n_units = uint32_t(units);
-  const size_t smem = 1024 + kStages * kBBytes + sizeof(DenseBars);
+  const size_t smem = 1024 + kStages * kBBytes + kMeta * kMetaBytes + sizeof(DenseBars);
   const int grid = int(std::min<uint64_t>(units, uint64_t(h->num_sms)));
   if (grid == 0) return;
   if (h->info.normalized) {

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <cstring>
 #include <numeric>
 #include <thread>
 
@@ -143,8 +144,18 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
     D.tiles.push_back(uint32_t(D.n_chunks));
     D.tiles.push_back(uint32_t(P.cols.size() / kDenseK));
     D.n_chunks += P.cols.size() / kDenseK;
-    D.cols.insert(D.cols.end(), P.cols.begin(), P.cols.end());
-    D.masks.insert(D.masks.end(), P.masks.begin(), P.masks.end());
+    for (size_t q = 0; q < P.cols.size() / kDenseK; ++q) {
+      const uint32_t* cc = P.cols.data() + q * kDenseK;
+      D.meta.insert(D.meta.end(), cc, cc + kDenseK);
+      for (uint32_t k = 0; k < kDenseK; ++k) {
+        const float sc = v.is_normalized ? v.row_scale[cc[k]] : 1.0f;
+        uint32_t bits;
+        std::memcpy(&bits, &sc, 4);
+        D.meta.push_back(bits);
+      }
+      const uint32_t* mm = P.masks.data() + q * kDenseRows;
+      D.meta.insert(D.meta.end(), mm, mm + kDenseRows);
+    }
     D.dense_entries += P.dense;
     D.padded_slots += uint64_t(P.cols.size()) * kDenseRows;
   }

@@ -17,6 +17,8 @@ inline constexpr uint32_t kDenseRows = 128;  // rows per tile (the MMA's N)
 inline constexpr uint32_t kDenseK = 32;      // columns per chunk (4 tf32 K-steps of 8)
 inline constexpr uint32_t kDenseFeat = 128;  // features per work unit (the MMA's M)
 inline constexpr uint32_t kDenseMaxChunks = 64;  // chunks per tile at most (load balance)
+inline constexpr uint32_t kDenseMetaWords = 2 * kDenseK + kDenseRows;  // 768 B per chunk
+inline constexpr double kDenseChunkCost = 150.0;  // gathers one chunk's time is worth (auto mode)
 
 struct DenseLayout {
   bool ok = false;                // planned (consistent rows, not order-faithful)
@@ -28,8 +30,10 @@ struct DenseLayout {
   uint32_t min_count = 0;         // a column is dense in a tile with >= this many entries
   // per tile, in schedule order (heaviest first): row0, rows, first chunk, chunks
   std::vector<uint32_t> tiles;    // 4 x n_tiles
-  std::vector<uint32_t> cols;     // kDenseK per chunk (padding repeats a real column)
-  std::vector<uint32_t> masks;    // kDenseRows per chunk: bit k = row has chunk column k
+  // per chunk, kDenseMetaWords u32: its kDenseK columns (padding repeats a
+  // real column), their scales (f32 bits; 1.0 for a binary matrix) and
+  // kDenseRows row masks (bit k = the row has chunk column k)
+  std::vector<uint32_t> meta;
   // the cold part as a CBM view: every parent virtual, values +1 or +s_col
   std::vector<uint32_t> cold_parent;
   std::vector<uint64_t> cold_row_ptr;

@@ -62,16 +62,15 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       if (opt.dense == 1 && !D.ok)
         throw invalid_argument("upload: the dense-block path needs delta rows consistent "
                                "with their parents' rows");
-      // cost in gather-equivalents (one X row slice per gathered entry): a
-      // chunk loads its 32 X rows once and runs 8 MMAs (~45 gathers' time),
-      // the cold entries are gathered; the streaming kernel gathers every
-      // effective entry
-      const double dense_cost = double(D.cold_entries) + 45.0 * double(D.n_chunks);
+      // cost in gather-equivalents (one X row per gathered entry): measured on
+      // cfg[3] (profiles/r02_dense_*), a chunk of the dense kernel costs about
+      // as much as 150 gathers of the streaming kernel; the cold entries are
+      // gathered on top, the streaming kernel alone gathers every effective entry
+      const double dense_cost = double(D.cold_entries) + kDenseChunkCost * double(D.n_chunks);
       h->dense_on = D.ok && (opt.dense == 1 || dense_cost < 0.85 * double(L.nnz_effective));
       if (h->dense_on) {
         put(h->dtiles, D.tiles, "upload dense tiles");
-        put(h->dcols, D.cols, "upload dense cols");
-        put(h->dmasks, D.masks, "upload dense masks");
+        put(h->dmeta, D.meta, "upload dense chunk records");
         cbm_b200_cbm_view cv{v.n_rows, v.n_cols, D.cold_entries, v.alpha, v.is_normalized,
                              D.cold_parent.data(), nullptr, D.cold_row_ptr.data(),
                              D.cold_col.data(), D.cold_val.data(), v.row_scale};
@@ -84,8 +83,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
         h->device_bytes += h->cold->device_bytes;
       }
       D.tiles = {};
-      D.cols = {};
-      D.masks = {};
+      D.meta = {};
       D.cold_parent = {};
       D.cold_row_ptr = {};
       D.cold_col = {};
@@ -167,7 +165,7 @@ void device_free(DeviceMatrix* h) {
   for (auto& kv : h->ws)
     if (kv.second.tinterior) cudaFree(kv.second.tinterior);
   if (h->cold) device_free(h->cold);
-  for (void* p : {(void*)h->dtiles, (void*)h->dcols, (void*)h->dmasks})
+  for (void* p : {(void*)h->dtiles, (void*)h->dmeta})
     if (p) cudaFree(p);
   for (void* p : {(void*)h->dcol, (void*)h->dval, (void*)h->rec, (void*)h->srow, (void*)h->scale,
                   (void*)h->xstage, (void*)h->ystage, (void*)h->tdcol, (void*)h->tdval,

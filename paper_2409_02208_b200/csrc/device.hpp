@@ -47,8 +47,7 @@ struct DeviceMatrix {
   bool dense_on = false;
   DenseLayout dense;
   uint32_t* dtiles = nullptr;
-  uint32_t* dcols = nullptr;
-  uint32_t* dmasks = nullptr;
+  uint32_t* dmeta = nullptr;
   struct DeviceMatrix* cold = nullptr;
   // per-call workspace, one per stream (concurrent calls on distinct streams
   // never share flags or scratch); grown on demand, or by cbm_b200_reserve
