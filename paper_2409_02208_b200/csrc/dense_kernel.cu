@@ -21,16 +21,17 @@
 // Sums run in a different order than the reference (default mode: bit-exact
 // on integer X, <= 1e-5 normwise otherwise).
 //
-// Warp roles (24 warps, one CTA per SM, persistent over the units):
+// Warp roles (22 warps, one CTA per SM, persistent over the units):
 //   w0      MMA issuer (one elected lane) and TMEM owner (512 columns)
 //   w1      metadata loader: each chunk's record (32 columns, their scales,
-//           128 row masks; 768 B) copied into an 8-deep shared-memory ring
-//           with cp.async, completion tracked by an mbarrier, so no other role
+//           128 row masks; 768 B) copied into a shared-memory ring
+//           with cp.async (32 deep), completion tracked by an mbarrier, so no other role
 //           waits on a dependent global load
-//   w2, w3  B expanders: row masks -> swizzled 0/1 tiles (chunks g = e mod 2)
-//   w4-w19  four producer sets of four warps (one per TMEM lane quarter);
-//           set j gathers the X' rows of chunks g = j mod 4 into stage j
-//   w20-w23 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
+//   w2-w5   B expanders: row masks -> swizzled 0/1 tiles (chunks g = e mod 4;
+//           a 16-entry nibble table, one st.shared.v4 per 16 bytes)
+//   w6-w17  three producer sets of four warps (one per TMEM lane quarter);
+//           set j gathers the X' rows of chunks g = j mod 3
+//   w18-w21 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
 //           adds the cold entries and applies the row scale on top)
 // Stages: 4 X'/B stages (64 TMEM columns + 16 KB smem each), 2 accumulators
 // (128 TMEM columns each): 4 * 64 + 2 * 128 = 512 columns.
@@ -46,11 +47,11 @@ namespace cbmb {
 namespace {
 
 constexpr int kStages = 4;
-constexpr int kSets = 4;       // producer sets (set j owns stage j)
-constexpr int kExpanders = 2;
-constexpr int kMeta = 8;       // metadata ring depth (chunks)
-constexpr int kWarps = 24;
-constexpr int kProd0 = 4;      // first producer warp
+constexpr int kSets = 3;       // producer sets (set j owns chunks g = j mod 3)
+constexpr int kExpanders = 4;
+constexpr int kMeta = 32;      // metadata ring depth (chunks)
+constexpr int kWarps = 2 + kExpanders + 4 * kSets + 4;
+constexpr int kProd0 = 2 + kExpanders;  // first producer warp
 constexpr int kEpi0 = kProd0 + 4 * kSets;  // first epilogue warp
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kTmemCols = 512;
@@ -154,6 +155,8 @@ struct __align__(16) DenseBars {
   uint64_t accfull[2], accempty[2];
   uint64_t mfull[kMeta], mempty[kMeta];
   uint32_t tmem_base;
+  uint32_t pad[3];
+  uint4 lut[16];   // the 4 floats (0.0 / 1.0) of each 4-bit mask nibble
 };
 constexpr uint32_t kMetaBytes = kDenseMetaWords * 4;
 
@@ -236,6 +239,9 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       mbar_init(&bars->mfull[m], 32);           // one cp.async arrive per loader lane
       mbar_init(&bars->mempty[m], 4 + 1);       // the owning producer set + its expander
     }
+    for (uint32_t q = 0; q < 16; ++q)
+      bars->lut[q] = make_uint4(q & 1 ? 0x3F800000u : 0u, q & 2 ? 0x3F800000u : 0u,
+                                q & 4 ? 0x3F800000u : 0u, q & 8 ? 0x3F800000u : 0u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -317,17 +323,19 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->mempty[m]);
       mbar_wait(&bars->bempty[s], ph ^ 1);
-      unsigned char* bs = bstage + s * kBBytes;
+      // item = 32 k + lane: tile row r = 4 k + lane / 8, 16-byte chunk q of its
+      // 128-byte line, stored at chunk q ^ (r & 7) (the 128-byte swizzle)
+      const uint32_t q = lane & 7, rsub = lane >> 3;
+      const uint32_t bs = saddr(bstage) + s * kBBytes;
 #pragma unroll
       for (uint32_t k = 0; k < (p.dbg & 4 ? 0u : 32u); ++k) {
-        // item = 32 k + lane: row r = item / 8 (4 rows per k), 16-byte chunk q
-        const uint32_t r = 4 * k + (lane >> 3), q = lane & 7;
+        const uint32_t r = 4 * k + rsub;
         const uint32_t mask = __shfl_sync(0xFFFFFFFFu, cur[k >> 3], r & 31);
-        const uint32_t bits = mask >> (4 * q);
-        const float4 v = make_float4((bits & 1) ? 1.f : 0.f, (bits & 2) ? 1.f : 0.f,
-                                     (bits & 4) ? 1.f : 0.f, (bits & 8) ? 1.f : 0.f);
-        *reinterpret_cast<float4*>(bs + (r >> 3) * 1024 + (r & 7) * 128 +
-                                   ((q ^ (r & 7)) << 4)) = v;
+        const uint4 v = bars->lut[(mask >> (4 * q)) & 15];
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                         bs + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4)),
+                     "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                     : "memory");
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -336,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
     }
   } else if (warp >= kProd0 && warp < kEpi0) {
     // ------------------------------------------------------------ X' producers
-    // set j owns the chunks g = j mod 4 (and so always stage j)
+    // set j owns the chunks g = j mod kSets
     const uint32_t set = (warp - kProd0) / 4, quarter = warp & 3;
     ChunkIter it;
     it.init(p, set, kSets);
