@@ -21,17 +21,20 @@
 // Sums run in a different order than the reference (default mode: bit-exact
 // on integer X, <= 1e-5 normwise otherwise).
 //
-// Warp roles (22 warps, one CTA per SM, persistent over the units):
+// Warp roles (20 warps, one CTA per SM, persistent over the units):
 //   w0      MMA issuer (one elected lane) and TMEM owner (512 columns)
 //   w1      metadata loader: each chunk's record (32 columns, their scales,
-//           128 row masks; 768 B) copied into a shared-memory ring
-//           with cp.async (32 deep), completion tracked by an mbarrier, so no other role
-//           waits on a dependent global load
+//           128 row masks; 768 B) copied into a 32-deep shared-memory ring
+//           with cp.async, completion tracked by an mbarrier, so no role waits
+//           on a dependent global load
 //   w2-w5   B expanders: row masks -> swizzled 0/1 tiles (chunks g = e mod 4;
 //           a 16-entry nibble table, one st.shared.v4 per 16 bytes)
-//   w6-w17  three producer sets of four warps (one per TMEM lane quarter);
-//           set j gathers the X' rows of chunks g = j mod 3
-//   w18-w21 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
+//   w6, w7  X gatherers: the chunk's 32 X row slices (512 B each) into one of 6
+//           shared-memory slots with cp.async (latency hidden by 6 chunks in
+//           flight without holding registers)
+//   w8-w15  two converter sets of four warps (one per TMEM lane quarter):
+//           staged slice -> scale -> hi/lo split -> tcgen05.st into TMEM
+//   w16-w19 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
 //           adds the cold entries and applies the row scale on top)
 // Stages: 4 X'/B stages (64 TMEM columns + 16 KB smem each), 2 accumulators
 // (128 TMEM columns each): 4 * 64 + 2 * 128 = 512 columns.
@@ -47,17 +50,21 @@ namespace cbmb {
 namespace {
 
 constexpr int kStages = 4;
-constexpr int kSets = 3;       // producer sets (set j owns chunks g = j mod 3)
+constexpr int kSets = 2;       // converter sets (set j owns chunks g = j mod 2)
 constexpr int kExpanders = 4;
+constexpr int kGatherers = 2;  // cp.async gatherers (chunks g = j mod 2)
 constexpr int kMeta = 32;      // metadata ring depth (chunks)
-constexpr int kWarps = 2 + kExpanders + 4 * kSets + 4;
-constexpr int kProd0 = 2 + kExpanders;  // first producer warp
-constexpr int kEpi0 = kProd0 + 4 * kSets;  // first epilogue warp
+constexpr int kXSlots = 6;     // staged X' slices in shared memory (chunks in flight)
+constexpr int kGath0 = 2 + kExpanders;       // first gatherer warp
+constexpr int kProd0 = kGath0 + kGatherers;  // first converter warp
+constexpr int kEpi0 = kProd0 + 4 * kSets;    // first epilogue warp
+constexpr int kWarps = kEpi0 + 4;
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAccCol = 0;       // two accumulators: columns [0,128), [128,256)
 constexpr uint32_t kStageCol = 256;   // stage s: [256 + 64 s, 256 + 64 s + 64): hi | lo
 constexpr uint32_t kBBytes = kDenseRows * kDenseK * 4;  // 16 KB per B stage
+constexpr uint32_t kXBytes = kDenseK * kDenseFeat * 4;   // 16 KB per staged X slice
 
 struct DenseParams {
   const float* __restrict__ x;
@@ -154,6 +161,7 @@ struct __align__(16) DenseBars {
   uint64_t xfull[kStages], xempty[kStages], bfull[kStages], bempty[kStages];
   uint64_t accfull[2], accempty[2];
   uint64_t mfull[kMeta], mempty[kMeta];
+  uint64_t sfull[kXSlots], sempty[kXSlots];
   uint32_t tmem_base;
   uint32_t pad[3];
   uint4 lut[16];   // the 4 floats (0.0 / 1.0) of each 4-bit mask nibble
@@ -213,9 +221,12 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
   // B stages at the first 1024-byte boundary (the swizzle is address-based)
   unsigned char* bstage = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
-  const uint32_t* meta_ring = reinterpret_cast<const uint32_t*>(bstage + kStages * kBBytes);
-  DenseBars* bars =
-      reinterpret_cast<DenseBars*>(bstage + kStages * kBBytes + kMeta * kMetaBytes);
+  unsigned char* xslot = bstage + kStages * kBBytes;  // kXSlots x [32 columns][128 features]
+  const uint32_t* meta_ring =
+      reinterpret_cast<const uint32_t*>(xslot + kXSlots * kXBytes);
+  DenseBars* bars = reinterpret_cast<DenseBars*>(reinterpret_cast<unsigned char*>(
+                                                     const_cast<uint32_t*>(meta_ring)) +
+                                                 kMeta * kMetaBytes);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0) {
@@ -237,7 +248,11 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
     }
     for (int m = 0; m < kMeta; ++m) {
       mbar_init(&bars->mfull[m], 32);           // one cp.async arrive per loader lane
-      mbar_init(&bars->mempty[m], 4 + 1);       // the owning producer set + its expander
+      mbar_init(&bars->mempty[m], 1 + 1 + 4);   // its expander, gatherer, converter set
+    }
+    for (int q = 0; q < kXSlots; ++q) {
+      mbar_init(&bars->sfull[q], 32);           // one cp.async arrive per gatherer lane
+      mbar_init(&bars->sempty[q], 4);           // the converter set's four warps
     }
     for (uint32_t q = 0; q < 16; ++q)
       bars->lut[q] = make_uint4(q & 1 ? 0x3F800000u : 0u, q & 2 ? 0x3F800000u : 0u,
@@ -342,29 +357,78 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       if (lane == 0) mbar_arrive(&bars->bfull[s]);
       it.next(p, e, kExpanders);
     }
+  } else if (warp >= kGath0 && warp < kProd0) {
+    // ------------------------------------------------------------ X gatherers
+    // chunk g's 32 X row slices (128 features = 512 B each) copied into slot
+    // g mod kXSlots with cp.async, one row slice per warp instruction; the
+    // slot's mbarrier completes when every lane's copies have landed
+    const uint32_t gi = warp - kGath0;
+    ChunkIter it;
+    it.init(p, gi, kGatherers);
+    while (!it.done) {
+      const uint32_t q = it.g % kXSlots, qph = (it.g / kXSlots) & 1;
+      const uint32_t m = it.g % kMeta, mph = (it.g / kMeta) & 1;
+      mbar_wait(&bars->mfull[m], mph);
+      const uint32_t mycol = meta_ring[m * kDenseMetaWords + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->mempty[m]);
+      mbar_wait(&bars->sempty[q], qph ^ 1);
+      const uint32_t f0 = it.fb * kDenseFeat + 4 * lane;      // this lane's 4 features
+      const uint32_t dst = saddr(xslot) + q * kXBytes + 16 * lane;
+      const bool full = f0 + 4 <= p.d && (p.ldx & 3) == 0 &&
+                        (reinterpret_cast<uintptr_t>(p.x) & 15) == 0;
+#pragma unroll 4
+      for (uint32_t k = 0; k < kDenseK; ++k) {
+        const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycol, k);
+        const float* src = p.x + (long long)c * p.ldx + f0;
+        if (p.dbg & 1) {
+        } else if (full) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + k * 512),
+                       "l"(src)
+                       : "memory");
+        } else {  // ragged feature edge or unaligned X: element copies, zeros past d
+#pragma unroll
+          for (uint32_t e = 0; e < 4; ++e) {
+            const uint32_t sz = f0 + e < p.d ? 4u : 0u;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + k * 512 + 4 * e),
+                         "l"(sz ? src + e : p.x), "r"(sz)
+                         : "memory");
+          }
+        }
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                       saddr(&bars->sfull[q]))
+                   : "memory");
+      it.next(p, gi, kGatherers);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp >= kProd0 && warp < kEpi0) {
-    // ------------------------------------------------------------ X' producers
-    // set j owns the chunks g = j mod kSets
+    // ------------------------------------------------------------ X' converters
+    // set j owns chunks g = j mod kSets: staged slice -> (scale) -> hi/lo split
+    // -> TMEM (lane = feature)
     const uint32_t set = (warp - kProd0) / 4, quarter = warp & 3;
     ChunkIter it;
     it.init(p, set, kSets);
     while (!it.done) {
       const uint32_t s = it.g % kStages, ph = (it.g / kStages) & 1;
       const uint32_t m = it.g % kMeta, mph = (it.g / kMeta) & 1;
-      const uint32_t f = it.fb * kDenseFeat + quarter * 32 + lane;
-      const bool live = f < p.d && !(p.dbg & 1);
-      mbar_wait(&bars->mfull[m], mph);
-      const uint32_t* rec = meta_ring + m * kDenseMetaWords;
-      float v[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) v[k] = live ? __ldg(p.x + (long long)rec[k] * p.ldx + f) : 0.f;
+      const uint32_t q = it.g % kXSlots, qph = (it.g / kXSlots) & 1;
       float sc[NORM ? 32 : 1];
+      mbar_wait(&bars->mfull[m], mph);
       if constexpr (NORM) {
+        const uint32_t* rec = meta_ring + m * kDenseMetaWords;
 #pragma unroll
         for (int k = 0; k < 32; ++k) sc[k] = __uint_as_float(rec[kDenseK + k]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->mempty[m]);
+      mbar_wait(&bars->sfull[q], qph);
+      const float* xs = reinterpret_cast<const float*>(xslot + q * kXBytes) + quarter * 32 + lane;
+      float v[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[k] = xs[k * kDenseFeat];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->sempty[q]);
       uint32_t hi[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
@@ -450,7 +514,8 @@ void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float*
   const uint64_t units = uint64_t(D.n_tiles) * p.n_fb;
   if (units >= 0xFFFFFFFFull) throw invalid_argument("spmm: too many dense-block units");
   p.n_units = uint32_t(units);
-  const size_t smem = 1024 + kStages * kBBytes + kMeta * kMetaBytes + sizeof(DenseBars);
+  const size_t smem =
+      1024 + kStages * kBBytes + kXSlots * kXBytes + kMeta * kMetaBytes + sizeof(DenseBars);
   const int grid = int(std::min<uint64_t>(units, uint64_t(h->num_sms)));
   if (grid == 0) return;
   if (h->info.normalized) {
