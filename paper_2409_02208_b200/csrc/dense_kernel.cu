@@ -21,20 +21,21 @@
 // Sums run in a different order than the reference (default mode: bit-exact
 // on integer X, <= 1e-5 normwise otherwise).
 //
-// Warp roles (20 warps, one CTA per SM, persistent over the units):
+// Warp roles (28 warps, one CTA per SM, persistent over the units):
 //   w0      MMA issuer (one elected lane) and TMEM owner (512 columns)
 //   w1      metadata loader: each chunk's record (32 columns, their scales,
 //           128 row masks; 768 B) copied into a 32-deep shared-memory ring
 //           with cp.async, completion tracked by an mbarrier, so no role waits
 //           on a dependent global load
-//   w2-w5   B expanders: row masks -> swizzled 0/1 tiles (chunks g = e mod 4;
+//   w2, w3  B expanders: row masks -> swizzled 0/1 tiles (chunks g = e mod 2;
 //           a 16-entry nibble table, one st.shared.v4 per 16 bytes)
-//   w6, w7  X gatherers: the chunk's 32 X row slices (512 B each) into one of 6
-//           shared-memory slots with cp.async (latency hidden by 6 chunks in
-//           flight without holding registers)
-//   w8-w15  two converter sets of four warps (one per TMEM lane quarter):
-//           staged slice -> scale -> hi/lo split -> tcgen05.st into TMEM
-//   w16-w19 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
+//   w4-w19  X gatherers: warp i copies X row slices 2i, 2i+1 (512 B each) of
+//           every chunk into one of 6 shared-memory slots with cp.async; a
+//           warp sustains only a few rows in flight, so the gather bandwidth
+//           comes from the number of gathering warps
+//   w20-w23 converters (one per TMEM lane quarter): staged slice -> scale ->
+//           hi/lo split -> tcgen05.st into TMEM
+//   w24-w27 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
 //           adds the cold entries and applies the row scale on top)
 // Stages: 4 X'/B stages (64 TMEM columns + 16 KB smem each), 2 accumulators
 // (128 TMEM columns each): 4 * 64 + 2 * 128 = 512 columns.
@@ -50,9 +51,10 @@ namespace cbmb {
 namespace {
 
 constexpr int kStages = 4;
-constexpr int kSets = 2;       // converter sets (set j owns chunks g = j mod 2)
-constexpr int kExpanders = 4;
-constexpr int kGatherers = 2;  // cp.async gatherers (chunks g = j mod 2)
+constexpr int kSets = 1;       // converter sets (set j owns chunks g = j mod kSets)
+constexpr int kExpanders = 2;
+constexpr int kGatherers = 16; // cp.async gatherers: warp i copies rows 2i, 2i+1 of every chunk
+constexpr int kRowsPerGatherer = kDenseK / kGatherers;
 constexpr int kMeta = 32;      // metadata ring depth (chunks)
 constexpr int kXSlots = 6;     // staged X' slices in shared memory (chunks in flight)
 constexpr int kGath0 = 2 + kExpanders;       // first gatherer warp
@@ -145,6 +147,15 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint32_t a_tmem, uint6
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], " ARGS32 ";" ::"r"(taddr), R32(r)
                : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -248,10 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
     }
     for (int m = 0; m < kMeta; ++m) {
       mbar_init(&bars->mfull[m], 32);           // one cp.async arrive per loader lane
-      mbar_init(&bars->mempty[m], 1 + 1 + 4);   // its expander, gatherer, converter set
+      mbar_init(&bars->mempty[m], 1 + kGatherers + 4);  // expander, gatherers, converter set
     }
     for (int q = 0; q < kXSlots; ++q) {
-      mbar_init(&bars->sfull[q], 32);           // one cp.async arrive per gatherer lane
+      mbar_init(&bars->sfull[q], 32 * kGatherers);  // one cp.async arrive per gatherer lane
       mbar_init(&bars->sempty[q], 4);           // the converter set's four warps
     }
     for (uint32_t q = 0; q < 16; ++q)
@@ -364,12 +375,15 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
     // slot's mbarrier completes when every lane's copies have landed
     const uint32_t gi = warp - kGath0;
     ChunkIter it;
-    it.init(p, gi, kGatherers);
+    it.init(p, 0, 1);
     while (!it.done) {
       const uint32_t q = it.g % kXSlots, qph = (it.g / kXSlots) & 1;
       const uint32_t m = it.g % kMeta, mph = (it.g / kMeta) & 1;
       mbar_wait(&bars->mfull[m], mph);
-      const uint32_t mycol = meta_ring[m * kDenseMetaWords + lane];
+      uint32_t cols[kRowsPerGatherer];
+#pragma unroll
+      for (int r = 0; r < kRowsPerGatherer; ++r)
+        cols[r] = meta_ring[m * kDenseMetaWords + kRowsPerGatherer * gi + r];
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->mempty[m]);
       mbar_wait(&bars->sempty[q], qph ^ 1);
@@ -377,10 +391,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       const uint32_t dst = saddr(xslot) + q * kXBytes + 16 * lane;
       const bool full = f0 + 4 <= p.d && (p.ldx & 3) == 0 &&
                         (reinterpret_cast<uintptr_t>(p.x) & 15) == 0;
-#pragma unroll 4
-      for (uint32_t k = 0; k < kDenseK; ++k) {
-        const uint32_t c = __shfl_sync(0xFFFFFFFFu, mycol, k);
-        const float* src = p.x + (long long)c * p.ldx + f0;
+#pragma unroll
+      for (int r = 0; r < kRowsPerGatherer; ++r) {
+        const uint32_t k = kRowsPerGatherer * gi + r;
+        const float* src = p.x + (long long)cols[r] * p.ldx + f0;
         if (p.dbg & 1) {
         } else if (full) {
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + k * 512),
@@ -399,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
                        saddr(&bars->sfull[q]))
                    : "memory");
-      it.next(p, gi, kGatherers);
+      it.next(p, 0, 1);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp >= kProd0 && warp < kEpi0) {
@@ -413,35 +427,31 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       const uint32_t s = it.g % kStages, ph = (it.g / kStages) & 1;
       const uint32_t m = it.g % kMeta, mph = (it.g / kMeta) & 1;
       const uint32_t q = it.g % kXSlots, qph = (it.g / kXSlots) & 1;
-      float sc[NORM ? 32 : 1];
       mbar_wait(&bars->mfull[m], mph);
-      if constexpr (NORM) {
-        const uint32_t* rec = meta_ring + m * kDenseMetaWords;
-#pragma unroll
-        for (int k = 0; k < 32; ++k) sc[k] = __uint_as_float(rec[kDenseK + k]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->mempty[m]);
+      const float* sc = reinterpret_cast<const float*>(meta_ring + m * kDenseMetaWords + kDenseK);
       mbar_wait(&bars->sfull[q], qph);
       const float* xs = reinterpret_cast<const float*>(xslot + q * kXBytes) + quarter * 32 + lane;
-      float v[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) v[k] = xs[k * kDenseFeat];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->sempty[q]);
-      uint32_t hi[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        float w = v[k];
-        if constexpr (NORM) w = __fmul_rn(w, sc[k]);
-        hi[k] = __float_as_uint(w) & 0xFFFFE000u;
-        v[k] = __fsub_rn(w, __uint_as_float(hi[k]));   // lo, in place
-      }
       mbar_wait(&bars->xempty[s], ph ^ 1);
       tc_fence_after();
       const uint32_t taddr = tb + ((quarter * 32) << 16) + kStageCol + 64 * s;
-      tmem_st32(taddr, hi);
-      tmem_st32(taddr + 32, reinterpret_cast<const uint32_t(&)[32]>(v));
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {   // 16 columns at a time (register budget)
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          float w = xs[(16 * half + k) * kDenseFeat];
+          if constexpr (NORM) w = __fmul_rn(w, sc[16 * half + k]);
+          hi[k] = __float_as_uint(w) & 0xFFFFE000u;
+          lo[k] = __float_as_uint(__fsub_rn(w, __uint_as_float(hi[k])));
+        }
+        tmem_st16(taddr + 16 * half, hi);
+        tmem_st16(taddr + 32 + 16 * half, lo);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bars->sempty[q]);
+        mbar_arrive(&bars->mempty[m]);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
