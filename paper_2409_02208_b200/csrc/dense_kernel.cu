@@ -21,27 +21,29 @@
 // Sums run in a different order than the reference (default mode: bit-exact
 // on integer X, <= 1e-5 normwise otherwise).
 //
-// Warp roles (28 warps, one CTA per SM, persistent over the units):
+// Warp roles (30 warps, one CTA per SM, persistent over the units):
 //   w0      MMA issuer (one elected lane) and TMEM owner (512 columns)
 //   w1      metadata loader: each chunk's record (32 columns, their scales,
 //           128 row masks; 768 B) copied into a 32-deep shared-memory ring
 //           with cp.async, completion tracked by an mbarrier, so no role waits
 //           on a dependent global load
-//   w2, w3  B expanders: row masks -> swizzled 0/1 tiles (chunks g = e mod 2;
+//   w2-w5   B expanders: row masks -> swizzled 0/1 tiles (chunks g = e mod 4;
 //           a 16-entry nibble table, one st.shared.v4 per 16 bytes)
-//   w4-w19  X gatherers: warp i copies X row slices 2i, 2i+1 (512 B each) of
-//           every chunk into one of 6 shared-memory slots with cp.async; a
+//   w6-w17  X gatherers: warp i copies X row slices i, i+12, i+24 (512 B each)
+//           of every chunk into one of 6 shared-memory slots with cp.async; a
 //           warp sustains only a few rows in flight, so the gather bandwidth
 //           comes from the number of gathering warps
-//   w20-w23 converters (one per TMEM lane quarter): staged slice -> scale ->
-//           hi/lo split -> tcgen05.st into TMEM
-//   w24-w27 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
+//   w18-w25 two converter sets of four warps (one per TMEM lane quarter):
+//           staged slice -> scale -> hi/lo split -> tcgen05.st into TMEM
+//   w26-w29 epilogue: TMEM -> registers -> Y (unscaled; the streaming kernel
 //           adds the cold entries and applies the row scale on top)
 // Stages: 4 X'/B stages (64 TMEM columns + 16 KB smem each), 2 accumulators
 // (128 TMEM columns each): 4 * 64 + 2 * 128 = 512 columns.
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "cuda_common.hpp"
 #include "dense_layout.hpp"
@@ -51,10 +53,10 @@ namespace cbmb {
 namespace {
 
 constexpr int kStages = 4;
-constexpr int kSets = 1;       // converter sets (set j owns chunks g = j mod kSets)
-constexpr int kExpanders = 2;
-constexpr int kGatherers = 16; // cp.async gatherers: warp i copies rows 2i, 2i+1 of every chunk
-constexpr int kRowsPerGatherer = kDenseK / kGatherers;
+constexpr int kSets = 2;       // converter sets (set j owns chunks g = j mod kSets)
+constexpr int kExpanders = 4;
+constexpr int kGatherers = 12; // cp.async gatherers: warp i copies rows i, i+12, i+24 of every chunk
+constexpr int kRowsPerGatherer = (kDenseK + kGatherers - 1) / kGatherers;
 constexpr int kMeta = 32;      // metadata ring depth (chunks)
 constexpr int kXSlots = 6;     // staged X' slices in shared memory (chunks in flight)
 constexpr int kGath0 = 2 + kExpanders;       // first gatherer warp
@@ -79,7 +81,9 @@ struct DenseParams {
   uint32_t n_units;                    // tiles x feature blocks
   uint32_t n_fb;                       // feature blocks of kDenseFeat
   uint32_t d;
-  uint32_t dbg;  // dev A/B only (CBM_B200_DENSE_DBG): 1 no X loads, 2 no MMAs, 4 no B fill
+  unsigned long long* trace;  // dev only (CBM_B200_DENSE_TRACE): CTA 0's MMA-warp timeline
+  uint32_t dbg;  // dev A/B only (CBM_B200_DENSE_DBG): 1 no X loads, 2 no MMAs, 4 no B fill,
+                 // 8 no Y stores
 };
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
@@ -146,6 +150,13 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint32_t a_tmem, uint6
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], " ARGS32 ";" ::"r"(taddr), R32(r)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
+                   taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+               "r"(r[7])
                : "memory");
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -291,8 +302,16 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       tc_fence_after();
       for (uint32_t j = 0; j < t.w; ++j, ++g) {
         const uint32_t s = g % kStages, ph = (g / kStages) & 1;
+        unsigned long long t0 = 0, t1 = 0;
+        if (p.trace) t0 = clock64();
         mbar_wait(&bars->xfull[s], ph);
+        if (p.trace) t1 = clock64();
         mbar_wait(&bars->bfull[s], ph);
+        if (p.trace && blockIdx.x == 0 && lane == 0 && g < 4096) {
+          p.trace[3 * g] = t0;
+          p.trace[3 * g + 1] = t1;
+          p.trace[3 * g + 2] = clock64();
+        }
         tc_fence_after();
         if (lane == 0 && !(p.dbg & 2)) {
           const uint64_t bdesc = sw128_desc(saddr(bstage + s * kBBytes));
@@ -353,11 +372,15 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       // 128-byte line, stored at chunk q ^ (r & 7) (the 128-byte swizzle)
       const uint32_t q = lane & 7, rsub = lane >> 3;
       const uint32_t bs = saddr(bstage) + s * kBBytes;
+      const uint32_t lut = saddr(&bars->lut[0]);
 #pragma unroll
       for (uint32_t k = 0; k < (p.dbg & 4 ? 0u : 32u); ++k) {
         const uint32_t r = 4 * k + rsub;
         const uint32_t mask = __shfl_sync(0xFFFFFFFFu, cur[k >> 3], r & 31);
-        const uint4 v = bars->lut[(mask >> (4 * q)) & 15];
+        uint4 v;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(lut + 16 * ((mask >> (4 * q)) & 15)));
         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
                          bs + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4)),
                      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -383,7 +406,8 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       uint32_t cols[kRowsPerGatherer];
 #pragma unroll
       for (int r = 0; r < kRowsPerGatherer; ++r)
-        cols[r] = meta_ring[m * kDenseMetaWords + kRowsPerGatherer * gi + r];
+        cols[r] = gi + kGatherers * r < kDenseK
+                      ? meta_ring[m * kDenseMetaWords + gi + kGatherers * r] : 0u;
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->mempty[m]);
       mbar_wait(&bars->sempty[q], qph ^ 1);
@@ -393,7 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
                         (reinterpret_cast<uintptr_t>(p.x) & 15) == 0;
 #pragma unroll
       for (int r = 0; r < kRowsPerGatherer; ++r) {
-        const uint32_t k = kRowsPerGatherer * gi + r;
+        const uint32_t k = gi + kGatherers * r;
+        if (k >= kDenseK) break;
         const float* src = p.x + (long long)cols[r] * p.ldx + f0;
         if (p.dbg & 1) {
         } else if (full) {
@@ -435,17 +460,17 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       tc_fence_after();
       const uint32_t taddr = tb + ((quarter * 32) << 16) + kStageCol + 64 * s;
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {   // 16 columns at a time (register budget)
-        uint32_t hi[16], lo[16];
+      for (int part = 0; part < 4; ++part) {   // 8 columns at a time (register budget)
+        uint32_t hi[8], lo[8];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          float w = xs[(16 * half + k) * kDenseFeat];
-          if constexpr (NORM) w = __fmul_rn(w, sc[16 * half + k]);
+        for (int k = 0; k < 8; ++k) {
+          float w = xs[(8 * part + k) * kDenseFeat];
+          if constexpr (NORM) w = __fmul_rn(w, sc[8 * part + k]);
           hi[k] = __float_as_uint(w) & 0xFFFFE000u;
           lo[k] = __float_as_uint(__fsub_rn(w, __uint_as_float(hi[k])));
         }
-        tmem_st16(taddr + 16 * half, hi);
-        tmem_st16(taddr + 32 + 16 * half, lo);
+        tmem_st8(taddr + 8 * part, hi);
+        tmem_st8(taddr + 32 + 8 * part, lo);
       }
       __syncwarp();
       if (lane == 0) {
@@ -485,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars->accempty[a]);
         }
-        if (live) {
+        if (live && !(p.dbg & 8)) {
 #pragma unroll
           for (uint32_t j = 0; j < 32; ++j)
             if (c0 + j < t.y) __stcs(ybase + (long long)(c0 + j) * p.ldy, __uint_as_float(r[j]));
@@ -521,6 +546,12 @@ void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float*
   p.d = d;
   p.dbg = 0;
   if (const char* e = std::getenv("CBM_B200_DENSE_DBG")) p.dbg = uint32_t(std::atoi(e));
+  p.trace = nullptr;
+  const char* trace_path = std::getenv("CBM_B200_DENSE_TRACE");
+  if (trace_path) {
+    ck(cudaMalloc(&p.trace, 3 * 4096 * 8), "trace");
+    ck(cudaMemsetAsync(p.trace, 0, 3 * 4096 * 8, s), "trace");
+  }
   const uint64_t units = uint64_t(D.n_tiles) * p.n_fb;
   if (units >= 0xFFFFFFFFull) throw invalid_argument("spmm: too many dense-block units");
   p.n_units = uint32_t(units);
@@ -538,6 +569,18 @@ void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float*
     dense_kernel<false><<<grid, kThreads, smem, s>>>(p);
   }
   ck(cudaGetLastError(), "dense_kernel launch");
+  if (trace_path) {  // dev tool: per chunk of CTA 0: before xfull, after xfull, after bfull
+    std::vector<unsigned long long> t(3 * 4096);
+    ck(cudaStreamSynchronize(s), "trace");
+    ck(cudaMemcpy(t.data(), p.trace, t.size() * 8, cudaMemcpyDeviceToHost), "trace");
+    cudaFree(p.trace);
+    if (FILE* f = std::fopen(trace_path, "a")) {
+      std::fprintf(f, "call\n");
+      for (int g = 0; g < 4096 && t[3 * g]; ++g)
+        std::fprintf(f, "%d %llu %llu %llu\n", g, t[3 * g], t[3 * g + 1], t[3 * g + 2]);
+      std::fclose(f);
+    }
+  }
 }
 
 }  // namespace cbmb
