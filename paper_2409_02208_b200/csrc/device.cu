@@ -67,7 +67,11 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       // as much as 150 gathers of the streaming kernel; the cold entries are
       // gathered on top, the streaming kernel alone gathers every effective entry
       const double dense_cost = double(D.cold_entries) + kDenseChunkCost * double(D.n_chunks);
-      h->dense_on = D.ok && (opt.dense == 1 || dense_cost < 0.85 * double(L.nnz_effective));
+      // (and enough chunks to fill the SMs: two launches and a persistent
+      // pipeline do not pay on small matrices, cfg[0]: 23.6 vs 13.3 us tiled)
+      h->dense_on = D.ok && (opt.dense == 1 ||
+                             (dense_cost < 0.85 * double(L.nnz_effective) &&
+                              D.n_chunks >= 8ull * uint64_t(std::max(1, h->num_sms))));
       if (h->dense_on) {
         put(h->dtiles, D.tiles, "upload dense tiles");
         put(h->dmeta, D.meta, "upload dense chunk records");

@@ -99,14 +99,22 @@ def test_dense_min_threshold_moves_entries():
 
 
 def test_auto_picks_dense_on_community_blocks_and_falls_back_narrow():
-    a = community(4096, 256, 0.6, 0.001, 25)
+    # enough 128-row tiles with shared columns to fill the SMs (auto rule)
+    a = community(24000, 400, 0.5, 1e-4, 25)
     c = P.build_cbm_normalized(a, 0, 4)
     op = P.DeviceCbm(c, device=0)
     assert op.info()["dense_active"]
+    assert op.info()["dense_chunks"] >= 8 * 148
     x = P.generate_dense("normal", a.n_cols, 16, 11)     # d < 32: streaming kernel
     got = op.spmm(torch.from_numpy(x).cuda()).cpu().numpy()
     assert normwise_err(got, O.oracle_spmm(oracle_arrays(c), x)) <= TOL
     assert op.info()["launches_per_call"] == 1
+
+
+def test_auto_keeps_small_matrices_off_the_dense_path():
+    a = community(4096, 256, 0.6, 0.001, 27)
+    c = P.build_cbm_normalized(a, 0, 4)
+    assert not P.DeviceCbm(c, device=0).info()["dense_active"]
 
 
 def test_order_faithful_never_takes_the_dense_path():

@@ -1,0 +1,98 @@
+// Dev probe (not product code): tcgen05.mma issue rate from one thread with A in
+// TMEM and B in 128B-swizzled shared memory, for the shapes the dense-block
+// kernel could use. Prints cycles per MMA for kind::tf32 and kind::f16 (bf16)
+// at N = 128 and 256 (M = 128, cta_group::1).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/umma_rate tools/umma_rate.cu
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t desc(uint32_t saddr) {
+  return uint64_t((saddr & 0x3FFFF) >> 4) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+template <int KIND, int N>   // KIND 0 = tf32, 1 = f16 (bf16)
+__global__ void rate(unsigned long long* out, int iters) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* b = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < N * 32; i += blockDim.x) reinterpret_cast<uint32_t*>(b)[i] = 0;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tb = tbase;
+  if (threadIdx.x == 0) {
+    const uint32_t fmt = KIND == 0 ? 2u : 1u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+    const uint64_t bd = desc(smem_u32(b));
+    const uint32_t acol = N == 256 ? 256 : 384;   // A columns after the accumulator
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint32_t acc = (i | ks) != 0;
+        if (KIND == 0)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tb),
+                       "r"(tb + acol + 8 * ks), "l"(bd + 2 * ks), "r"(idesc), "r"(acc));
+        else
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tb),
+                       "r"(tb + acol + 8 * ks), "l"(bd + 2 * ks), "r"(idesc), "r"(acc));
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+    unsigned long long t1 = clock64();
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(smem_u32(&bar)), "r"(0));
+    unsigned long long t2 = clock64();
+    out[blockIdx.x * 2] = t1 - t0;
+    out[blockIdx.x * 2 + 1] = t2 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512));
+}
+
+template <int KIND, int N>
+void run(const char* name, int blocks) {
+  unsigned long long* d;
+  cudaMalloc(&d, 2 * blocks * 8);
+  const int iters = 2000;
+  const size_t smem = 1024 + N * 128 + 64;
+  cudaFuncSetAttribute(rate<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  rate<KIND, N><<<blocks, 128, smem>>>(d, iters);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[2 * 148];
+  cudaMemcpy(h, d, 2 * blocks * 8, cudaMemcpyDeviceToHost);
+  const double macs = 128.0 * N * (KIND == 0 ? 8 : 16);
+  printf("%s blocks=%d err=%s: issue %.1f cyc/mma, complete %.1f cyc/mma, %.0f MAC/clk/SM\n", name, blocks,
+         cudaGetErrorString(e), double(h[0]) / (iters * 4), double(h[1]) / (iters * 4),
+         macs * iters * 4 / double(h[1]));
+  cudaFree(d);
+}
+
+int main() {
+  run<0, 128>("tf32 M128 N128 K8 ", 1);
+  run<0, 256>("tf32 M128 N256 K8 ", 1);
+  run<1, 128>("bf16 M128 N128 K16", 1);
+  run<1, 256>("bf16 M128 N256 K16", 1);
+  run<0, 128>("tf32 M128 N128 K8 ", 148);
+  run<1, 256>("bf16 M128 N256 K16", 148);
+  return 0;
+}
