@@ -57,7 +57,8 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
     }
     // dense-block path (default mode): the tensor cores take the columns each
     // 128-row tile shares, a streaming operator the rest
-    if (!L.order_faithful && opt.dense != 0 && v.n_rows > 0) {
+    if (!L.order_faithful && (opt.dense == 1 || (opt.dense == -1 && opt.tile != 1)) &&
+        v.n_rows > 0) {
       DenseLayout D = plan_dense(v, opt.dense_min);
       if (opt.dense == 1 && !D.ok)
         throw invalid_argument("upload: the dense-block path needs delta rows consistent "

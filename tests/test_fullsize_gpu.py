@@ -88,10 +88,13 @@ def test_cfg3_full_size_default_and_faithful(cfg3):
     assert a.n_rows == 132534 and c.is_normalized
     x = wl.operand(a.n_cols)                       # N(0,1), d = 256
     want = ref_cbm(c).spmm(x, THREADS)
-    got, info = run(c, x)                          # auto: the tiled path on cfg3
-    assert info["tile_active"]
+    got, info = run(c, x)                          # auto: the dense-block path on cfg3
+    assert info["dense_active"]
     assert normwise_err(got, want) <= TOL
-    got_s, _ = run(c, x, tile=0)                   # streaming kernel, default mode
+    got_t, info_t = run(c, x, dense=0)             # the tiled path
+    assert info_t["tile_active"]
+    assert normwise_err(got_t, want) <= TOL
+    got_s, _ = run(c, x, dense=0, tile=0)          # streaming kernel, default mode
     assert normwise_err(got_s, want) <= TOL
     got_f, _ = run(c, x, order_faithful=True)
     assert_bitwise(got_f, want, "cfg3 order-faithful vs reference spmm_into")
