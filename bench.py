@@ -494,7 +494,7 @@ def run_ours(args, wl, WL):
     from paper_2409_02208_b200.sharding import (auto_row_groups, column_slab, grid_position,
                                                 row_partition)
     if args.row_groups < 0:
-        args.row_groups = 1 if wl.normalized else auto_row_groups(wl.d, world)
+        args.row_groups = auto_row_groups(wl.d, world)
     group, slab_rank, n_slabs = grid_position(world, rank, args.row_groups)
     c_local, n_out, rows_g = c, a.n_rows, None
     if args.row_groups > 1:
@@ -534,13 +534,15 @@ def run_ours(args, wl, WL):
     if args.no_parity:
         gate = {"ok": False, "why": "--no-parity"}
     elif O is not None and O.ref_available():
-        ref_cbm = O.RefCbm.from_arrays(O.RefCbmArrays(c_local.n_rows, c_local.n_cols,
-                                                      c_local.alpha, c_local.is_normalized,
-                                                      c_local.parent, c_local.row_ptr,
-                                                      c_local.col_idx, c_local.values,
-                                                      c_local.row_scale))
+        # the reference multiplies the WHOLE matrix (a row block of a normalized
+        # CBM is not a container it accepts); this rank's rows are taken from it
+        ref_cbm = O.RefCbm.from_arrays(O.RefCbmArrays(c.n_rows, c.n_cols, c.alpha,
+                                                      c.is_normalized, c.parent, c.row_ptr,
+                                                      c.col_idx, c.values, c.row_scale))
         threads = max(1, args.threads // max(1, world))
         want = ref_cbm.spmm(x_host.numpy(), threads) if d_local else np.zeros((n_out, 0))
+        if rows_g is not None:
+            want = want[rows_g]
         if wl.x_kind == "int" and not wl.normalized:
             gate = parity(y.cpu().numpy(), want, exact=True)
         else:

@@ -59,6 +59,12 @@ typedef struct cbm_b200_cbm_view {
   const uint32_t* col_idx;     /* delta_matrix.col_idx[nnz] */
   const float* values;         /* delta_matrix.values[nnz] */
   const float* row_scale;      /* row_scale[n_rows] (normalized) or NULL */
+  /* normalized only, optional: the per-COLUMN scale (n_cols entries) the
+   * delta values are checked against (values = +-col_scale[col]) when the view
+   * is a row block of a normalized matrix (a rectangular sub-CBM of the 2-D
+   * multi-GPU partition); row_scale then scales the block's own
+   * rows. NULL: square container, row_scale serves both (io.cpp:369-380). */
+  const float* col_scale;
 } cbm_b200_cbm_view;
 
 /* ------------------------------------------------------------------------

@@ -68,7 +68,8 @@ class _CbmView(C.Structure):
     _fields_ = [("n_rows", C.c_uint32), ("n_cols", C.c_uint32), ("nnz", C.c_uint64),
                 ("alpha", C.c_uint64), ("is_normalized", C.c_int32),
                 ("parent", C.c_void_p), ("topo_order", C.c_void_p), ("row_ptr", C.c_void_p),
-                ("col_idx", C.c_void_p), ("values", C.c_void_p), ("row_scale", C.c_void_p)]
+                ("col_idx", C.c_void_p), ("values", C.c_void_p), ("row_scale", C.c_void_p),
+                ("col_scale", C.c_void_p)]
 
 
 class _Options(C.Structure):
@@ -223,6 +224,9 @@ class CbmMatrix:
     topo_order: np.ndarray | None = None
     branch_ptr: np.ndarray | None = None
     build_stats: dict | None = None
+    # normalized row block of a larger matrix (sharding.row_partition): the
+    # per-column scale of the delta values; row_scale then scales its own rows
+    col_scale: np.ndarray | None = None
 
     def __post_init__(self):
         self.parent = np.ascontiguousarray(self.parent, np.uint32)
@@ -231,6 +235,8 @@ class CbmMatrix:
         self.values = np.ascontiguousarray(self.values, np.float32)
         if self.row_scale is not None:
             self.row_scale = np.ascontiguousarray(self.row_scale, np.float32)
+        if self.col_scale is not None:
+            self.col_scale = np.ascontiguousarray(self.col_scale, np.float32)
 
     @property
     def nnz(self) -> int:
@@ -242,7 +248,9 @@ class CbmMatrix:
                         self.topo_order.ctypes.data if self.topo_order is not None else None,
                         self.row_ptr.ctypes.data, self.col_idx.ctypes.data,
                         self.values.ctypes.data,
-                        self.row_scale.ctypes.data if self.is_normalized else None)
+                        self.row_scale.ctypes.data if self.is_normalized else None,
+                        self.col_scale.ctypes.data
+                        if self.is_normalized and self.col_scale is not None else None)
 
 
 def _copy(ptr, n, dtype):

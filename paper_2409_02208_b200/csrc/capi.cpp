@@ -142,6 +142,7 @@ int cbm_b200_host_view(const cbm_b200_host_cbm* h, cbm_b200_cbm_view* v) {
     v->col_idx = c.col_idx.data();
     v->values = c.values.data();
     v->row_scale = c.normalized ? c.row_scale.data() : nullptr;
+    v->col_scale = nullptr;
   });
 }
 
@@ -185,6 +186,8 @@ int cbm_b200_load_cbm1(const char* path, cbm_b200_host_cbm** out) {
 int cbm_b200_save_cbm1(const cbm_b200_cbm_view* v, const char* path) {
   return guard([&] {
     need(v && path, "save_cbm1: null argument");
+    need(!(v->is_normalized && v->col_scale),
+         "save_cbm1: a row block of a normalized matrix is not a CBM1 container");
     cbmb::HostCbm c;
     c.n_rows = v->n_rows;
     c.n_cols = v->n_cols;
@@ -248,7 +251,7 @@ int cbm_b200_upload_cbm1(const char* path, const cbm_b200_options* opt,
     cbm_b200_cbm_view v{c.n_rows, c.n_cols, c.row_ptr.back(), c.alpha, c.normalized ? 1 : 0,
                         c.parent.data(), c.topo_order.data(), c.row_ptr.data(),
                         c.col_idx.data(), c.values.data(),
-                        c.normalized ? c.row_scale.data() : nullptr};
+                        c.normalized ? c.row_scale.data() : nullptr, nullptr};
     *out = upload_view(v, opt);
   });
 }

@@ -32,6 +32,7 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
   if (const char* e = std::getenv("CBM_B200_DENSE_MIN"))  // dev tool (threshold sweeps)
     D.min_count = std::max(1, std::atoi(e));
   if (m == 0) return D;
+  const float* colscale = v.col_scale ? v.col_scale : v.row_scale;  // (normalized)
 
   // full rows of the represented matrix (parents first)
   std::vector<uint32_t> bfs;
@@ -148,7 +149,7 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
       const uint32_t* cc = P.cols.data() + q * kDenseK;
       D.meta.insert(D.meta.end(), cc, cc + kDenseK);
       for (uint32_t k = 0; k < kDenseK; ++k) {
-        const float sc = v.is_normalized ? v.row_scale[cc[k]] : 1.0f;
+        const float sc = v.is_normalized ? colscale[cc[k]] : 1.0f;
         uint32_t bits;
         std::memcpy(&bits, &sc, 4);
         D.meta.push_back(bits);
@@ -174,7 +175,7 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
   D.cold_val.resize(D.cold_entries);
   const bool norm = v.is_normalized != 0;
   for (uint64_t k = 0; k < D.cold_entries; ++k)
-    D.cold_val[k] = norm ? v.row_scale[D.cold_col[k]] : 1.0f;
+    D.cold_val[k] = norm ? colscale[D.cold_col[k]] : 1.0f;
   D.cold_parent.assign(m, kNoItem);
   D.ok = true;
   return D;

@@ -78,7 +78,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
         put(h->dmeta, D.meta, "upload dense chunk records");
         cbm_b200_cbm_view cv{v.n_rows, v.n_cols, D.cold_entries, v.alpha, v.is_normalized,
                              D.cold_parent.data(), nullptr, D.cold_row_ptr.data(),
-                             D.cold_col.data(), D.cold_val.data(), v.row_scale};
+                             D.cold_col.data(), D.cold_val.data(), v.row_scale, v.col_scale};
         cbm_b200_options co = opt;
         co.order_faithful = 0;
         co.tile = 0;
@@ -96,7 +96,9 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       h->dense = std::move(D);
     }
     // tiled path (default mode): planned here, kept only when it pays
-    if (!L.order_faithful && opt.tile != 0 && v.n_rows > 0 && !h->dense_on) {
+    // (the tiled kernel scales rows and staged columns from one array: square only)
+    if (!L.order_faithful && opt.tile != 0 && v.n_rows > 0 && !h->dense_on &&
+        !(L.normalized && v.col_scale)) {
       TileLayout T;
       bool planned = true;
       try {
@@ -145,6 +147,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
     L.rec = {};  // item_beg and item_dep stay: they drive the ticket schedule
     L.srow = {};
     L.scale = {};
+    L.row_scale = {};
     h->info = std::move(L);
   } catch (...) {
     device_free(h);

@@ -76,13 +76,16 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   if (nnz && (!v.col_idx || !v.values)) throw invalid_argument("upload: null array in view");
   L.nnz = nnz;
   if (L.normalized) {
-    if (v.n_rows != v.n_cols)
+    if (v.n_rows != v.n_cols && !v.col_scale)
       throw invalid_argument("normalized container must be square");
     if (!v.row_scale && m) throw invalid_argument("upload: normalized view without row_scale");
-    L.scale.assign(v.row_scale, v.row_scale + m);
-    for (float s : L.scale)
-      if (!std::isfinite(s) || s <= 0.0f)
-        throw invalid_argument("row_scale entries must be positive and finite");
+    L.row_scale.assign(v.row_scale, v.row_scale + m);
+    if (v.col_scale) L.scale.assign(v.col_scale, v.col_scale + v.n_cols);
+    else L.scale = L.row_scale;
+    for (const auto* vec : {&L.scale, &L.row_scale})
+      for (float s : *vec)
+        if (!std::isfinite(s) || s <= 0.0f)
+          throw invalid_argument("row_scale entries must be positive and finite");
   }
   // delta rows: monotone offsets, strictly increasing in-range columns, value pattern
   for (uint32_t r = 0; r < m; ++r) {
@@ -367,7 +370,7 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
     R(t)[4] = p == kVirtual ? 0u : (L.normalized ? slot[p] : p);
     if (L.normalized) {
       R(t)[7] = slot[r];
-      L.srow[t] = L.scale[r];
+      L.srow[t] = L.row_scale[r];
     }
   }
   return L;

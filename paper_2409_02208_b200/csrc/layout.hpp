@@ -55,7 +55,8 @@ struct Layout {
   //   [7] slot  : own interior scratch slot (normalized parents) or kNoItem
   std::vector<uint32_t> rec;
   std::vector<float> srow;      // per item: row_scale[row] (normalized)
-  std::vector<float> scale;     // row_scale (normalized), indexed by column
+  std::vector<float> scale;     // column scale (normalized): row_scale, or the view's col_scale
+  std::vector<float> row_scale; // the rows' own scale (normalized)
   std::vector<uint32_t> item_beg;  // n_items + 1: delta prefix by item (kept on the host)
   std::vector<uint32_t> level_ptr;  // ROW-item offsets of each level (relative to the ROW block)
 };

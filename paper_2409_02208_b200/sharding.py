@@ -70,11 +70,28 @@ def _max_group(cost, cuts):
     return int(np.max(cum[cuts[1:]] - cum[cuts[:-1]]))
 
 
+def _with_identity(a):
+    """Row pointers and columns of A + I (the pattern a normalized CBM
+    represents, normalized_adjacency_csr, gcn.cpp:48-89)."""
+    import numpy as np
+    n = a.n_rows
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.row_ptr.astype(np.int64)))
+    r = np.concatenate([rows, np.arange(n, dtype=np.int64)])
+    cc = np.concatenate([a.col_idx.astype(np.int64), np.arange(n, dtype=np.int64)])
+    order = np.lexsort((cc, r))
+    r, cc = r[order], cc[order]
+    keep = np.ones(r.size, bool)
+    keep[1:] = (r[1:] != r[:-1]) | (cc[1:] != cc[:-1])
+    r, cc = r[keep], cc[keep]
+    ptr = np.concatenate([[0], np.cumsum(np.bincount(r, minlength=n))]).astype(np.uint64)
+    return ptr, cc.astype(np.uint32)
+
+
 def row_partition(a, c, parts: int):
-    """Row groups of a 2-D (row group x column slab) partition of a BINARY CBM
+    """Row groups of a 2-D (row group x column slab) partition of a CBM
     (DESIGN.md §7): contiguous row ranges balanced by stored length (delta
-    count, refined to count flattened rows at their A length). A row whose
-    parent lies in another range is flattened (its deltas become its row of A
+    count, refined to count flattened rows at their full length). A row whose
+    parent lies in another range is flattened (its deltas become its full row
     with a virtual parent, as the tiled path does for cut trees), so a group
     never waits on another and no collective is needed. Returns
     [(global row ids, sub-CBM of those rows x all columns)], one per group;
@@ -82,24 +99,29 @@ def row_partition(a, c, parts: int):
     multiply; otherwise the flattened rows sum in a different order (within
     the default mode's tolerance).
 
-    A normalized CBM cannot be cut this way: its delta values are +-row_scale
-    of the COLUMN and the container ties row_scale to square matrices
-    (io.cpp:369-380), so a row subset is not a valid CbmMatrix."""
+    Normalized CBMs: the full rows are those of A + I, the delta values stay
+    +-s[col] (the column scale), and each block carries the column scale of
+    the whole matrix (col_scale) beside its own rows' scale (row_scale): a
+    rectangular row block the reference's square container cannot hold
+    (io.cpp:369-380), uploaded through the view's col_scale."""
     import numpy as np
     from . import VIRTUAL_PARENT, CbmMatrix
-    if c.is_normalized:
-        raise ValueError("row_partition: binary CBMs only")
     if parts < 1:
         raise ValueError("row_partition: parts must be >= 1")
     if a.n_rows != c.n_rows or a.n_cols != c.n_cols:
         raise ValueError("row_partition: A and its CBM differ in shape")
+    norm = bool(c.is_normalized)
+    if norm:
+        a_ptr, a_col = _with_identity(a)
+    else:
+        a_ptr, a_col = a.row_ptr, a.col_idx
     m = c.n_rows
     clen = np.diff(c.row_ptr.astype(np.int64))
-    alen_all = np.diff(a.row_ptr.astype(np.int64))
+    alen_all = np.diff(a_ptr.astype(np.int64))
     par_all = c.parent.astype(np.int64)
     cuts = _balanced_cuts(clen, parts)
     # refine: balance the lengths AFTER flattening (a flattened row costs its
-    # A row, not its deltas); keep whichever cut has the lightest heaviest group
+    # full row, not its deltas); keep whichever cut has the lightest heaviest group
     best = (_max_group(_group_cost(cuts, par_all, clen, alen_all), cuts), cuts)
     for _ in range(4):
         cuts = _balanced_cuts(_group_cost(cuts, par_all, clen, alen_all), parts)
@@ -123,12 +145,14 @@ def row_partition(a, c, parts: int):
         fpos = flat[row_of]
         col_idx = np.empty(int(row_ptr[-1]), np.uint32)
         values = np.empty(int(row_ptr[-1]), np.float32)
-        col_idx[fpos] = _gather_rows(a.row_ptr, a.col_idx, rows[flat])
-        values[fpos] = 1.0
+        col_idx[fpos] = _gather_rows(a_ptr, a_col, rows[flat])
+        values[fpos] = c.row_scale[col_idx[fpos]] if norm else 1.0
         col_idx[~fpos] = _gather_rows(c.row_ptr, c.col_idx, rows[~flat])
         values[~fpos] = _gather_rows(c.row_ptr, c.values, rows[~flat])
-        out.append((rows, CbmMatrix(hi - lo, c.n_cols, c.alpha, False, parent, row_ptr, col_idx,
-                                    values)))
+        out.append((rows, CbmMatrix(hi - lo, c.n_cols, c.alpha, norm, parent, row_ptr, col_idx,
+                                    values,
+                                    row_scale=c.row_scale[lo:hi] if norm else None,
+                                    col_scale=c.row_scale if norm else None)))
     return out
 
 

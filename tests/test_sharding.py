@@ -196,11 +196,27 @@ def test_row_partition_reassembles_exactly(parts):
     assert heavy <= _max_group(_group_cost(plain, par, clen, alen), plain)
 
 
-def test_row_partition_rejects_normalized():
+@pytest.mark.parametrize("parts", [2, 3, 5])
+def test_row_partition_normalized_row_blocks(parts):
+    """Normalized CBMs cut into row blocks: each block keeps the whole matrix's
+    column scale (col_scale) and its own rows' scale (row_scale); flattened
+    rows become rows of A + I with values s[col]. Reassembled through the
+    oracle, the blocks give the full multiply within the default-mode bar."""
     from paper_2409_02208_b200.sharding import row_partition
-    a = P.generate_graph("community", [200, 20, 0.5, 0.01], 5)
-    with pytest.raises(ValueError, match="binary CBMs only"):
-        row_partition(a, P.build_cbm_normalized(a, 0), 2)
+    from helpers import normwise_err
+    a = P.generate_graph("community", [1200, 80, 0.4, 0.01], 0xC0F60000 + 93)
+    c = P.build_cbm_normalized(a, 0, 4)
+    x = P.generate_dense("normal", a.n_cols, 24, 0xC0F61000 + 93)
+    want = O.oracle_spmm(oracle_arrays(c), x)
+    got = np.empty_like(want)
+    for rows, sub in row_partition(a, c, parts):
+        assert sub.is_normalized and sub.n_cols == c.n_cols
+        assert np.array_equal(sub.row_scale, c.row_scale[rows])
+        assert np.array_equal(sub.col_scale, c.row_scale)
+        # every delta value is +-col_scale[col] (load_cbm's rule, per column)
+        assert np.array_equal(np.abs(sub.values), sub.col_scale[sub.col_idx])
+        got[rows] = O.oracle_spmm(oracle_arrays(sub), x)
+    assert normwise_err(got, want) <= 1e-6
 
 
 @pytest.mark.parametrize("world,row_groups", [(4, 1), (4, 2), (4, 4), (6, 3)])
@@ -265,3 +281,24 @@ def test_auto_row_groups_matches_the_projection_choice():
     assert [auto_row_groups(64, n) for n in (1, 2, 4, 8)] == [1, 2, 4, 8]
     assert [auto_row_groups(256, n) for n in (1, 2, 4, 8)] == [1, 1, 2, 4]
     assert auto_row_groups(512, 6) == 2
+
+
+@pytest.mark.gpu
+def test_device_multiplies_normalized_row_blocks():
+    """Each normalized row block uploads through the view's col_scale (a
+    rectangular normalized CBM) and multiplies like the oracle on the block."""
+    import torch
+    from paper_2409_02208_b200.sharding import row_partition
+    from helpers import normwise_err
+    a = P.generate_graph("community", [3000, 150, 0.4, 0.005], 0xC0F60000 + 94)
+    c = P.build_cbm_normalized(a, 0, 4)
+    x = P.generate_dense("normal", a.n_cols, 64, 0xC0F61000 + 94)
+    for rows, sub in row_partition(a, c, 3):
+        want = O.oracle_spmm(oracle_arrays(sub), x)
+        for faithful in (True, False):
+            got = P.DeviceCbm(sub, device=0, order_faithful=faithful).spmm(
+                torch.from_numpy(x).cuda()).cpu().numpy()
+            if faithful:
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+            else:
+                assert normwise_err(got, want) <= 1e-5

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -q --durations=8 > gpurun_out/r16_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r16_pytest.log
+timeout 1200 python bench.py > gpurun_out/r16_bench.json 2> gpurun_out/r16_bench.err; echo "bench rc=$?" >> gpurun_out/r16_bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/r16_ref.json 2> gpurun_out/r16_ref.err; echo "ref rc=$?" >> gpurun_out/r16_ref.err
+BENCH_DEV_SHARE_GPU=1 timeout 600 python bench.py --gpus 2 --config cfg2 --steps 5 --no-cpu-baseline --no-north-star > gpurun_out/r16_share2.json 2> gpurun_out/r16_share2.err; echo "share2 rc=$?" >> gpurun_out/r16_share2.err
