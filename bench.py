@@ -400,15 +400,21 @@ def roofline_for(info, ms, n_out, n_cols, d_local, normalized, workload):
     peak, peak_src = peaks()
     b_alg = b_alg_bytes(info["nnz_delta"], n_out, n_cols, d_local, normalized)
     achieved = b_alg / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-    tiled = bool(info["tile_active"]) and d_local >= 32
-    if tiled:
+    dense = bool(info["dense_active"]) and d_local >= 32
+    tiled = not dense and bool(info["tile_active"]) and d_local >= 32
+    if dense:
+        # the tensor-core part loads one X row slice per chunk column, the cold
+        # part gathers one per entry
+        l2_bytes = (int(info["dense_chunks"]) * 32 + int(info["cold_entries"])) * d_local * 4
+    elif tiled:
         l2_bytes = (int(info["tile_staged_rows"]) + int(info["tile_deltas"])
                     - int(info["tile_staged_deltas"])) * d_local * 4
     else:
         l2_bytes = int(info["nnz_effective"]) * d_local * 4
     r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
          "frac": achieved / peak, "traffic": traffic_for(workload), "b_alg_bytes": b_alg,
-         "kernel": "tile_kernel" if tiled else "cbm_kernel", "peak_source": peak_src,
+         "kernel": ("dense_kernel (tcgen05) + cbm_kernel (cold entries)" if dense else
+                    "tile_kernel" if tiled else "cbm_kernel"), "peak_source": peak_src,
          # what bounds the gather: X rows moved L2 -> SM per step (one row per
          # summed delta)
          "l2_gather": {"bytes": l2_bytes,

@@ -14,7 +14,9 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr) {
          (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
 
-template <int KIND, int N>   // KIND 0 = tf32, 1 = f16 (bf16)
+__device__ volatile int g_stop;
+
+template <int KIND, int N, int CONT>   // KIND 0 = tf32, 1 = f16 (bf16); CONT 1 smem, 2 tmem traffic
 __global__ void rate(unsigned long long* out, int iters) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* b = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
@@ -35,6 +37,29 @@ __global__ void rate(unsigned long long* out, int iters) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tb = tbase;
+  __shared__ __align__(16) float junk[4][32 * 64];
+  __shared__ volatile int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  if (warp >= 4 && CONT == 1) {           // other warps: smem read/write traffic
+    float acc = 0;
+    const int w = warp & 3, l = threadIdx.x & 31;
+    for (int it = 0; !stop && it < 1000000; ++it) {
+      float4* q = reinterpret_cast<float4*>(junk[w]) + (it & 15) * 32 + l;
+      float4 v = *q;
+      acc += v.x;
+      *q = make_float4(acc, v.y, v.z, v.w);
+    }
+    if (acc == 12345.f) out[0] = 1;
+  } else if (warp >= 4 && CONT == 2) {    // other warps: TMEM stores into unused columns
+    const int q = warp & 3;
+    uint32_t r[8] = {1, 2, 3, 4, 5, 6, 7, 8};
+    for (int it = 0; !stop && it < 1000000; ++it)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
+                       tb + ((32 * q) << 16) + 480 + 8 * (it & 3)),
+                   "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+  }
   if (threadIdx.x == 0) {
     const uint32_t fmt = KIND == 0 ? 2u : 1u;
     const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
@@ -63,20 +88,21 @@ __global__ void rate(unsigned long long* out, int iters) {
     unsigned long long t2 = clock64();
     out[blockIdx.x * 2] = t1 - t0;
     out[blockIdx.x * 2 + 1] = t2 - t0;
+    stop = 1;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512));
 }
 
-template <int KIND, int N>
-void run(const char* name, int blocks) {
+template <int KIND, int N, int CONT = 0>
+void run(const char* name, int blocks, int threads = 128) {
   unsigned long long* d;
   cudaMalloc(&d, 2 * blocks * 8);
   const int iters = 2000;
   const size_t smem = 1024 + N * 128 + 64;
-  cudaFuncSetAttribute(rate<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  rate<KIND, N><<<blocks, 128, smem>>>(d, iters);
+  cudaFuncSetAttribute(rate<KIND, N, CONT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  rate<KIND, N, CONT><<<blocks, threads, smem>>>(d, iters);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[2 * 148];
   cudaMemcpy(h, d, 2 * blocks * 8, cudaMemcpyDeviceToHost);
@@ -94,5 +120,7 @@ int main() {
   run<1, 256>("bf16 M128 N256 K16", 1);
   run<0, 128>("tf32 M128 N128 K8 ", 148);
   run<1, 256>("bf16 M128 N256 K16", 148);
+  run<0, 128, 1>("tf32 N128 + smem traffic (12 warps)", 1, 512);
+  run<0, 128, 2>("tf32 N128 + tmem st traffic (12 warps)", 1, 512);
   return 0;
 }
