@@ -313,6 +313,13 @@ int cbm_b200_gen_graph(const char* kind, const double* params, int32_t n_params,
                        uint64_t seed, cbm_b200_csr** out);
 int cbm_b200_csr_get(const cbm_b200_csr* a, cbm_b200_csr_view* out);
 void cbm_b200_csr_free(cbm_b200_csr* a);
+/* Host-only plan of the dense-block layout (no device): what an upload with
+ * options.dense = 1 would multiply on the tensor cores. stats:
+ * tiles, chunks, dense entries, cold entries, padded slots (tile rows x chunk
+ * columns, zeros included), rows of the tallest tile. Validates the view like
+ * load_cbm (io.cpp:346-380). */
+int cbm_b200_plan_dense(const cbm_b200_cbm_view* c, uint32_t dense_min, uint64_t stats[6]);
+
 /* Dense fills: kind 0 = uniform [lo,hi) (random_dense, dense.cpp:56-62),
  * 1 = integers below(hi-lo+1)+lo, 2 = N(0,1) Box-Muller (lo/hi unused),
  * 3 = Glorot-uniform for a lo x hi (fan_in x fan_out) weight. */

@@ -30,7 +30,7 @@ import numpy as np
 
 __all__ = [
     "CsrBinaryMatrix", "CbmMatrix", "DeviceCbm", "build_cbm", "build_cbm_normalized",
-    "count_scalar_ops", "generate_graph", "generate_dense", "CbmError", "FormatError",
+    "count_scalar_ops", "plan_dense", "generate_graph", "generate_dense", "CbmError", "FormatError",
     "load_cbm", "save_cbm", "dense_matmul", "csr_operator", "VIRTUAL_PARENT",
     "library_path", "gemm_parts", "ipc_handle", "ipc_open", "ipc_close",
 ]
@@ -132,6 +132,7 @@ _sig = {
     "cbm_b200_spmm_host": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp]),
     "cbm_b200_spmv": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp]),
     "cbm_b200_get_info": (C.c_int, [_vp, C.POINTER(_Info)]),
+    "cbm_b200_plan_dense": (C.c_int, [C.POINTER(_CbmView), C.c_uint32, C.POINTER(_u64)]),
     "cbm_b200_dense_matmul": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp]),
     "cbm_b200_gcn_forward": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "cbm_b200_gemm_parts": (C.c_int, [C.POINTER(_vp), C.POINTER(_i64), _i32, _i64, _vp, _i64,
@@ -354,6 +355,16 @@ def count_scalar_ops(c: CbmMatrix) -> tuple[int, int]:
     v = c._view()
     _check(_lib.cbm_b200_count_ops(C.byref(v), C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def plan_dense(c: CbmMatrix, dense_min: int = 0) -> dict:
+    """Host-only plan of the dense-block layout: what an upload
+    with dense=1 would put on the tensor cores."""
+    st = (_u64 * 6)()
+    v = c._view()
+    _check(_lib.cbm_b200_plan_dense(C.byref(v), dense_min, st))
+    keys = ("tiles", "chunks", "dense_entries", "cold_entries", "padded_slots", "max_tile_rows")
+    return dict(zip(keys, (int(x) for x in st)))
 
 
 def generate_graph(kind: str, params, seed: int) -> CsrBinaryMatrix:

@@ -11,7 +11,9 @@
 
 #include "../../include/cbm_b200.h"
 #include "cbm_host.hpp"
+#include "dense_layout.hpp"
 #include "device.hpp"
+#include "layout.hpp"
 
 struct cbm_b200_host_cbm {
   cbmb::HostCbm c;
@@ -491,6 +493,26 @@ int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* o) {
     o->dense_chunks = D.n_chunks;
     o->dense_entries = D.dense_entries;
     o->cold_entries = D.cold_entries;
+  });
+}
+
+// Host-only plan of the dense-block layout (no device needed): what an upload
+// with dense = 1 would multiply on the tensor cores. stats: tiles, chunks,
+// dense entries, cold entries, padded slots, max tile rows.
+int cbm_b200_plan_dense(const cbm_b200_cbm_view* c, uint32_t dense_min, uint64_t stats[6]) {
+  return guard([&] {
+    need(c && stats, "plan_dense: null argument");
+    (void)cbmb::plan_layout(*c, true, 0, 0, 0, 148 * 20);  // validates like load_cbm
+    const cbmb::DenseLayout D = cbmb::plan_dense(*c, dense_min);
+    need(D.ok, "plan_dense: delta rows inconsistent with their parents");
+    uint64_t max_rows = 0;
+    for (uint32_t t = 0; t < D.n_tiles; ++t) max_rows = std::max<uint64_t>(max_rows, D.tiles[4 * t + 1]);
+    stats[0] = D.n_tiles;
+    stats[1] = D.n_chunks;
+    stats[2] = D.dense_entries;
+    stats[3] = D.cold_entries;
+    stats[4] = D.padded_slots;
+    stats[5] = max_rows;
   });
 }
 

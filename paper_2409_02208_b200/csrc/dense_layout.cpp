@@ -23,6 +23,39 @@ struct TilePlan {
   uint64_t dense = 0;
 };
 
+// Row ranges of the tiles (ascending, bounds[0] = 0, bounds.back() = m).
+std::vector<uint32_t> tile_bounds(uint32_t m, uint32_t n, const std::vector<uint64_t>& fptr,
+                                  const std::vector<uint32_t>& fcol) {
+  std::vector<uint32_t> fixed;
+  for (uint32_t r = 0; r < m; r += kDenseRows) fixed.push_back(r);
+  fixed.push_back(m);
+  if (const char* e = std::getenv("CBM_B200_DENSE_FIXED_TILES"))  // dev A/B
+    if (std::atoi(e)) return fixed;
+  std::vector<uint32_t> b{0};
+  std::vector<uint8_t> in_tile(n, 0);
+  uint32_t r0 = 0;
+  for (uint32_t r = 0; r < m; ++r) {
+    const uint64_t len = fptr[r + 1] - fptr[r];
+    bool cut = r - r0 >= kDenseRows;
+    if (!cut && r > r0 && len >= 8) {
+      uint64_t hit = 0;
+      for (uint64_t k = fptr[r]; k < fptr[r + 1]; ++k) hit += in_tile[fcol[k]];
+      cut = 2 * hit < len;
+    }
+    if (cut) {
+      for (uint32_t q = r0; q < r; ++q)
+        for (uint64_t k = fptr[q]; k < fptr[q + 1]; ++k) in_tile[fcol[k]] = 0;
+      b.push_back(r);
+      r0 = r;
+    }
+    for (uint64_t k = fptr[r]; k < fptr[r + 1]; ++k) in_tile[fcol[k]] = 1;
+  }
+  b.push_back(m);
+  // structure-free matrices: the scan cuts almost every row; keep the grid
+  if (b.size() - 1 > fixed.size() - 1 + (fixed.size() - 1) / 2) return fixed;
+  return b;
+}
+
 }  // namespace
 
 DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
@@ -56,7 +89,14 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
   if (!reconstruct_full_rows(v, bfs, fptr, fcol)) return D;   // no full-row form
   std::vector<uint32_t>().swap(bfs);
 
-  D.n_tiles = (m + kDenseRows - 1) / kDenseRows;
+  // Tile boundaries. A tile is <= kDenseRows consecutive rows; a fixed grid
+  // of 128 cuts communities in two, and a tile straddling two communities
+  // carries both column sets half empty. The greedy scan closes a tile when
+  // the next row places under half of its entries on columns the tile already
+  // holds (a new community starts); matrices without that structure (the
+  // scan would shred them into slivers) keep the fixed grid.
+  std::vector<uint32_t> bounds = tile_bounds(m, n, fptr, fcol);
+  D.n_tiles = uint32_t(bounds.size() - 1);
   std::vector<TilePlan> plans(D.n_tiles);
   const int threads = int(std::max(1u, std::thread::hardware_concurrency()));
   std::atomic<uint32_t> next{0};
@@ -67,7 +107,7 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
     std::vector<uint32_t> touched, dense;
     for (uint32_t t; (t = next.fetch_add(1)) < D.n_tiles;) {
       TilePlan& P = plans[t];
-      const uint32_t r0 = t * kDenseRows, r1 = std::min(m, r0 + kDenseRows);
+      const uint32_t r0 = bounds[t], r1 = bounds[t + 1];
       touched.clear();
       for (uint32_t r = r0; r < r1; ++r)
         for (uint64_t k = fptr[r]; k < fptr[r + 1]; ++k) {
@@ -139,9 +179,9 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
   D.tiles.reserve(size_t(D.n_tiles) * 4);
   for (uint32_t t : order) {
     const TilePlan& P = plans[t];
-    const uint32_t r0 = t * kDenseRows;
+    const uint32_t r0 = bounds[t];
     D.tiles.push_back(r0);
-    D.tiles.push_back(std::min(m, r0 + kDenseRows) - r0);
+    D.tiles.push_back(bounds[t + 1] - r0);
     D.tiles.push_back(uint32_t(D.n_chunks));
     D.tiles.push_back(uint32_t(P.cols.size() / kDenseK));
     D.n_chunks += P.cols.size() / kDenseK;
@@ -165,13 +205,13 @@ DenseLayout plan_dense(const cbm_b200_cbm_view& v, uint32_t min_count) {
   D.cold_row_ptr.assign(size_t(m) + 1, 0);
   for (uint32_t t = 0; t < D.n_tiles; ++t)
     for (uint32_t i = 0; i < plans[t].cold_cnt.size(); ++i)
-      D.cold_row_ptr[size_t(t) * kDenseRows + i + 1] = plans[t].cold_cnt[i];
+      D.cold_row_ptr[size_t(bounds[t]) + i + 1] = plans[t].cold_cnt[i];
   std::partial_sum(D.cold_row_ptr.begin(), D.cold_row_ptr.end(), D.cold_row_ptr.begin());
   D.cold_entries = D.cold_row_ptr[m];
   D.cold_col.resize(D.cold_entries);
   for (uint32_t t = 0; t < D.n_tiles; ++t)
     std::copy(plans[t].cold.begin(), plans[t].cold.end(),
-              D.cold_col.begin() + D.cold_row_ptr[size_t(t) * kDenseRows]);
+              D.cold_col.begin() + D.cold_row_ptr[bounds[t]]);
   D.cold_val.resize(D.cold_entries);
   const bool norm = v.is_normalized != 0;
   for (uint64_t k = 0; k < D.cold_entries; ++k)

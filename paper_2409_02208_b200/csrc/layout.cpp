@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <numeric>
 #include <string>
 
@@ -254,15 +255,48 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   }
   if (chunk == 0) chunk = std::max<uint32_t>(32, split_threshold / 4);
   if (chunk > split_threshold) chunk = split_threshold;
+  // Column bands (default mode): when X is far larger than L2, the pieces of
+  // the long rows are cut at band boundaries and summed band by band (every
+  // long row's piece of band 0, then band 1, ...), so a band of X rows is
+  // read from DRAM once and then met in L2 by every long row that references
+  // it. Row-major pieces sweep all of X once per long row instead (cfg[4]:
+  // 54 GB of DRAM reads per multiply, 10x the compulsory bytes). A band holds
+  // 48 MB of 1 KB X row slices; rows too sparse to leave >= 16 entries per
+  // band keep plain pieces (still taken in band order of their first column).
+  uint32_t band_cols = 0;
+  if (!order_faithful) {
+    const uint64_t budget = (48ull << 20) / 1024;
+    if (const char* e = std::getenv("CBM_B200_BAND_COLS")) band_cols = uint32_t(std::atoll(e));
+    else if (uint64_t(v.n_cols) > budget + budget / 3) band_cols = uint32_t(budget);
+  }
+  const uint32_t n_bands = band_cols ? (v.n_cols + band_cols - 1) / band_cols : 1;
+  L.band_cols = band_cols;
   std::vector<uint32_t> pieces(m, 1);  // per ROW position i
+  std::vector<uint64_t> cut_ptr(size_t(m) + 1, 0);
+  std::vector<uint32_t> cuts;  // piece start offsets inside the split rows (first = 0)
   uint64_t n_leaf = 0;
   if (!order_faithful) {
     for (uint32_t i = 0; i < m; ++i) {
       const uint32_t r = rows[i];
       const uint64_t len = eptr[r + 1] - eptr[r];
-      if (len <= split_threshold) continue;
-      pieces[i] = uint32_t((len + chunk - 1) / chunk);
-      n_leaf += pieces[i] - 1;
+      if (len > split_threshold) {
+        const uint32_t* e = ecol.data() + eptr[r];
+        const bool banded = band_cols && len >= 16ull * n_bands;
+        auto band = [&](uint32_t w) { return (w & ~kSignBit) / band_cols; };
+        uint32_t start = 0;
+        cuts.push_back(0);
+        for (uint32_t k = 1; k < len; ++k) {
+          bool cut = k - start >= chunk;
+          if (!cut && banded && k - start >= 16 && band(e[k]) != band(e[start])) cut = true;
+          if (cut) {
+            cuts.push_back(k);
+            start = k;
+          }
+        }
+        pieces[i] = uint32_t(cuts.size() - cut_ptr[i]);
+        n_leaf += pieces[i] - 1;
+      }
+      cut_ptr[i + 1] = cuts.size();
     }
   }
   // merge tree per split row: level 0 = the row's leaf chunks; a level with
@@ -329,12 +363,13 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
       own_hi[t_row] = hi;
       continue;
     }
+    const uint32_t* cq = cuts.data() + cut_ptr[i];
     own_lo[t_row] = lo;  // piece 0 stays with the ROW item
-    own_hi[t_row] = lo + chunk;
+    own_hi[t_row] = lo + cq[1];
     for (uint32_t q = 1; q < pieces[i]; ++q) {
       const uint32_t t = first_at[0][i] + q - 1;
-      own_lo[t] = lo + uint64_t(q) * chunk;
-      own_hi[t] = std::min<uint64_t>(hi, own_lo[t] + chunk);
+      own_lo[t] = lo + cq[q];
+      own_hi[t] = q + 1 < pieces[i] ? lo + cq[q + 1] : hi;
       R(t)[2] = r;
     }
     // merge levels: node j at level lv sums nodes [j*F, min((j+1)*F, n_prev)) of lv-1
@@ -357,6 +392,19 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
     for (uint64_t k = own_lo[t]; k < own_hi[t]; ++k)
       L.dcol[o++] = ecol[k];
     R(t)[1] = uint32_t(o);
+  }
+  // processing order of the items (schedule.cu): leaf pieces by the band of
+  // their first column (stable: row order inside a band), then everything
+  // else in item order. Leaf pieces wait on nothing, so every dependency
+  // still points to an earlier position.
+  if (band_cols && n_leaf) {
+    L.order.resize(L.n_items);
+    std::iota(L.order.begin(), L.order.end(), 0u);
+    std::vector<uint32_t> key(n_leaf);
+    for (uint64_t t = 0; t < n_leaf; ++t)
+      key[t] = (ecol[own_lo[t]] & ~kSignBit) / band_cols;
+    std::stable_sort(L.order.begin(), L.order.begin() + n_leaf,
+                     [&](uint32_t a, uint32_t b) { return key[a] < key[b]; });
   }
   L.item_beg.resize(size_t(L.n_items) + 1);
   for (uint32_t t = 0; t < L.n_items; ++t) L.item_beg[t] = R(t)[0];

@@ -58,6 +58,8 @@ struct Layout {
   std::vector<float> scale;     // column scale (normalized): row_scale, or the view's col_scale
   std::vector<float> row_scale; // the rows' own scale (normalized)
   std::vector<uint32_t> item_beg;  // n_items + 1: delta prefix by item (kept on the host)
+  uint32_t band_cols = 0;       // columns per band (0: the long rows' pieces are not banded)
+  std::vector<uint32_t> order;  // processing order of the items (empty: item order)
   std::vector<uint32_t> level_ptr;  // ROW-item offsets of each level (relative to the ROW block)
 };
 

@@ -37,12 +37,14 @@ __global__ void build_ticket_stream(const uint4* __restrict__ rec, const float* 
 }  // namespace
 
 // Static list schedule of the tickets over the resident warps (cbm_kernel).
-// Tickets are taken in order and each goes to the warp that an estimated
+// Tickets are taken in processing order (slab-major, then Layout::order: item
+// order, with the long rows' leaf pieces band by band) and each goes to the warp that an estimated
 // clock frees first (ties: lowest warp), starting no earlier than its
 // parent / partial producers are estimated to finish; cost ~ per-ticket
-// overhead + deltas + partial rows + parent row. Every warp's list is
-// increasing, which is all the deadlock argument needs (the smallest
-// unfinished ticket is always being worked on). Balancing by work instead of
+// overhead + deltas + partial rows + parent row. Every warp's list follows
+// the processing order and every wait targets an earlier position, which is
+// all the deadlock argument needs (the earliest unfinished ticket is always
+// being worked on). Balancing by work instead of
 // round-robin by count removes the tail where warps holding several 32-delta
 // chunks finish long after the rest.
 const DeviceMatrix::Schedule& schedule_for(DeviceMatrix* h, uint32_t warps, uint32_t slabs,
@@ -67,7 +69,8 @@ const DeviceMatrix::Schedule& schedule_for(DeviceMatrix* h, uint32_t warps, uint
   auto later = [](const Slot& a, const Slot& b) { return a > b; };  // min-heap
   std::make_heap(heap.begin(), heap.end(), later);
   for (uint32_t sl = 0; sl < slabs; ++sl) {
-    for (uint32_t t = 0; t < n; ++t) {
+    for (uint32_t idx = 0; idx < n; ++idx) {
+      const uint32_t t = L.order.empty() ? idx : L.order[idx];
       std::pop_heap(heap.begin(), heap.end(), later);
       Slot& top = heap.back();
       const uint32_t* dp = &h->item_dep[size_t(t) * 3];
@@ -93,7 +96,11 @@ const DeviceMatrix::Schedule& schedule_for(DeviceMatrix* h, uint32_t warps, uint
   std::vector<uint32_t> list(total);
   {
     std::vector<uint32_t> pos(count.begin(), count.end() - 1);
-    for (uint64_t T = 0; T < total; ++T) list[pos[owner[T]]++] = uint32_t(T);
+    for (uint32_t sl = 0; sl < slabs; ++sl)
+      for (uint32_t idx = 0; idx < n; ++idx) {  // each warp's list in processing order
+        const uint64_t T = uint64_t(sl) * n + (L.order.empty() ? idx : L.order[idx]);
+        list[pos[owner[T]]++] = uint32_t(T);
+      }
   }
   // the ticket stream: warp w's records at [w * stride, w * stride + count_w),
   // zero records after them and 64 more after the last region
