@@ -424,6 +424,49 @@ def roofline_for(info, ms, n_out, n_cols, d_local, normalized, workload):
     return r
 
 
+def cusparse_comparator(a, x, normalized, flops, ms, steps, stream, flush, dev):
+    """The vendor bar: cuSPARSE CSR SpMM (fp32, through
+    torch.sparse's CSR @ dense) on the same represented matrix and X. A reported
+    comparator only: the product path never calls it."""
+    import torch
+    try:
+        rp = np.asarray(a.row_ptr, np.int64)
+        ci = np.asarray(a.col_idx, np.int64)
+        if normalized:
+            n = a.n_rows
+            rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+            has_diag = np.zeros(n, bool)
+            has_diag[rows[rows == ci]] = True
+            add = np.nonzero(~has_diag)[0]
+            rows = np.concatenate([rows, add])
+            ci = np.concatenate([ci, add])
+            o = np.lexsort((ci, rows))
+            rows, ci = rows[o], ci[o]
+            rp = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=n))]).astype(np.int64)
+            s = (np.float32(1.0) / np.sqrt(np.diff(rp).astype(np.float64)).astype(np.float32))
+            vals = (s[rows] * s[ci]).astype(np.float32)
+        else:
+            vals = np.ones(ci.size, np.float32)
+        A = torch.sparse_csr_tensor(torch.from_numpy(rp).to(dev).to(torch.int32),
+                                    torch.from_numpy(ci).to(dev).to(torch.int32),
+                                    torch.from_numpy(vals).to(dev),
+                                    size=(a.n_rows, a.n_cols))
+        for _ in range(3):
+            yy = torch.sparse.mm(A, x)
+        torch.cuda.synchronize()
+        holder = [yy]
+
+        def fn():
+            holder[0] = torch.sparse.mm(A, x)
+        cs_ms = float(statistics.mean(time_steps(fn, steps, stream, flush)))
+        return {"ms_per_step": cs_ms, "value": flops / (cs_ms * 1e-3) / 1e9,
+                "ours_over_cusparse": cs_ms / ms if ms > 0 else None,
+                "note": "cuSPARSE CSR SpMM fp32 via torch.sparse.mm (allocates its output "
+                        "inside the timed call); reported comparator, not on the product path"}
+    except Exception as e:  # the comparator must never take the bench line down
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+
+
 def run_north_star(args, P, O, WL, dev, stream, flush):
     """configs[3] (north_star "config 3"): normalized A_hat.X at d=256 on one
     GPU, parity-gated like the headline, same timing rules."""
@@ -630,6 +673,11 @@ def run_ours(args, wl, WL):
                    "note": "uncompressed matrix through the same kernels (every parent virtual)"}
         csr_op.close()
 
+    cusparse = None
+    if not args.no_csr_comparator and args.row_groups == 1 and world == 1 and d_local:
+        cusparse = cusparse_comparator(a, x, wl.normalized, flops, ms, min(args.steps, 20),
+                                       stream, flush, dev)
+
     spmv = None
     if rank == 0 and world == 1:
         # spmv (d = 1, the lane-per-delta kernel) on the same whole matrix
@@ -695,6 +743,7 @@ def run_ours(args, wl, WL):
            "roofline": roofline,
            "cpu_baseline": cpu,
            "gpu_csr_comparator": gpu_csr,
+           "cusparse_comparator": cusparse,
            "spmv": spmv,
            "e2e": {"value": e2e_value, "unit": UNIT,
                    "h2d_bytes_per_step": int(a.n_cols * d_local * 4),

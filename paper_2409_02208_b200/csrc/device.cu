@@ -50,7 +50,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       // values: +-row_scale[col], validated by plan_layout)
       std::vector<float> dval(L.dcol.size());
       for (size_t k = 0; k < dval.size(); ++k) {
-        const float sc = L.scale[L.dcol[k] & 0x7FFFFFFFu];
+        const float sc = L.scale[L.dcol[k] & L.col_mask];
         dval[k] = (L.dcol[k] >> 31) ? -sc : sc;
       }
       put(h->dval, dval, "upload dval");

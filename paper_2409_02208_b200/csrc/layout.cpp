@@ -228,6 +228,39 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   if (L.nnz_effective >= 0xFFFFFFFFull)  // dcol offsets are 32-bit on the device
     throw invalid_argument("upload: more than 2^32-1 deltas after flattening "
                            "(upload with flatten_gain = 0)");
+  // Cache-residency marks (layout.hpp). Power-law matrices reference a few
+  // thousand columns from most rows (cfg[4]: the top 32 columns take 11% of the
+  // entries, the top 40k 61%) while the bulk of X is touched a handful of
+  // times. The marks let the kernel keep the shared rows in L1 / L2 and stream
+  // the rest past them. Only when X (at 1 KB per row) is well beyond L2.
+  {
+    uint32_t k1 = 0, k2 = 0;
+    if (v.n_cols < kHotL2Bit && uint64_t(v.n_cols) > (96ull << 10)) {
+      k1 = 24;
+      k2 = 32u << 10;
+    }
+    if (const char* e = std::getenv("CBM_B200_HOT_L1")) k1 = uint32_t(std::atoll(e));  // dev A/B
+    if (const char* e = std::getenv("CBM_B200_HOT_L2")) k2 = uint32_t(std::atoll(e));
+    if (v.n_cols >= kHotL2Bit) k1 = k2 = 0;
+    k1 = std::min(k1, v.n_cols);
+    k2 = std::min(k2, v.n_cols);
+    if ((k1 || k2) && !ecol.empty()) {
+      std::vector<uint32_t> cnt(v.n_cols, 0);
+      for (uint32_t w : ecol) ++cnt[w & ~kSignBit];
+      std::vector<uint32_t> by(v.n_cols);
+      std::iota(by.begin(), by.end(), 0u);
+      const uint32_t top = std::max(k1, k2);
+      auto more = [&](uint32_t a, uint32_t b) { return cnt[a] != cnt[b] ? cnt[a] > cnt[b] : a < b; };
+      std::partial_sort(by.begin(), by.begin() + top, by.end(), more);
+      std::vector<uint32_t> mark(v.n_cols, 0);
+      for (uint32_t i = 0; i < k2; ++i)
+        if (cnt[by[i]] >= 2) mark[by[i]] |= kHotL2Bit, ++L.hot_l2;
+      for (uint32_t i = 0; i < k1; ++i)
+        if (cnt[by[i]] >= 2) mark[by[i]] |= kHotL1Bit, ++L.hot_l1;
+      for (uint32_t& w : ecol) w |= mark[w & ~kSignBit];
+      if (L.hot_l1 || L.hot_l2) L.col_mask = kColMask;
+    }
+  }
 
   // ROW items: by depth, ascending row id inside a level (stable counting sort)
   uint32_t max_depth = 0;
@@ -282,7 +315,7 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
       if (len > split_threshold) {
         const uint32_t* e = ecol.data() + eptr[r];
         const bool banded = band_cols && len >= 16ull * n_bands;
-        auto band = [&](uint32_t w) { return (w & ~kSignBit) / band_cols; };
+        auto band = [&](uint32_t w) { return (w & L.col_mask) / band_cols; };
         uint32_t start = 0;
         cuts.push_back(0);
         for (uint32_t k = 1; k < len; ++k) {
@@ -402,7 +435,7 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
     std::iota(L.order.begin(), L.order.end(), 0u);
     std::vector<uint32_t> key(n_leaf);
     for (uint64_t t = 0; t < n_leaf; ++t)
-      key[t] = (ecol[own_lo[t]] & ~kSignBit) / band_cols;
+      key[t] = (ecol[own_lo[t]] & L.col_mask) / band_cols;
     std::stable_sort(L.order.begin(), L.order.begin() + n_leaf,
                      [&](uint32_t a, uint32_t b) { return key[a] < key[b]; });
   }
