@@ -160,6 +160,12 @@ typedef struct cbm_b200_options {
                                 cost model favours it), 0 off, 1 force */
   uint32_t dense_min;        /* entries per column per tile to count as shared
                                 (0 = auto, 3) */
+  int32_t hub;               /* default mode only: hub-row panel:
+                                the longest rows of a power-law matrix (up to 128)
+                                leave the streaming kernel and are multiplied as
+                                one tile on the tensor cores, each X row loaded
+                                once for all of them. -1 auto (when the cost rule
+                                favours it), 0 off, 1 force */
 } cbm_b200_options;
 
 void cbm_b200_default_options(cbm_b200_options* opt);
@@ -293,6 +299,10 @@ typedef struct cbm_b200_info {
   uint64_t dense_chunks;       /* 32-column chunks multiplied on the tensor cores */
   uint64_t dense_entries;      /* entries summed by the tensor cores */
   uint64_t cold_entries;       /* entries summed by the streaming kernel */
+  int32_t hub_active;          /* the hub-row panel takes the longest rows */
+  uint32_t hub_rows;           /* rows in the panel */
+  uint64_t hub_entries;        /* entries of those rows (summed by the tensor cores) */
+  uint64_t hub_chunks;         /* 32-column chunks over the union of their columns */
 } cbm_b200_info;
 int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* out);
 
@@ -319,6 +329,10 @@ void cbm_b200_csr_free(cbm_b200_csr* a);
  * columns, zeros included), rows of the tallest tile. Validates the view like
  * load_cbm (io.cpp:346-380). */
 int cbm_b200_plan_dense(const cbm_b200_cbm_view* c, uint32_t dense_min, uint64_t stats[6]);
+/* Host-only: the hub-row panel an upload with options.hub = mode would build
+ * (DESIGN.md §6). stats: active (0/1), rows in the panel, their entries, 32-column
+ * chunks over the union of their columns, pieces, deltas left to the rest. */
+int cbm_b200_plan_hub(const cbm_b200_cbm_view* c, int32_t mode, uint64_t stats[6]);
 
 /* Dense fills: kind 0 = uniform [lo,hi) (random_dense, dense.cpp:56-62),
  * 1 = integers below(hi-lo+1)+lo, 2 = N(0,1) Box-Muller (lo/hi unused),

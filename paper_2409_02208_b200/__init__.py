@@ -78,7 +78,7 @@ class _Options(C.Structure):
                 ("kernel", C.c_int32), ("max_segments", C.c_int32),
                 ("flatten_gain", C.c_int32), ("prefetch", C.c_int32), ("tile", C.c_int32),
                 ("tile_rows", C.c_uint32), ("tile_stage", C.c_uint32), ("tile_vec", C.c_int32),
-                ("dense", C.c_int32), ("dense_min", C.c_uint32)]
+                ("dense", C.c_int32), ("dense_min", C.c_uint32), ("hub", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -94,7 +94,9 @@ class _Info(C.Structure):
                 ("tile_deltas", C.c_uint64), ("tile_staged_deltas", C.c_uint64),
                 ("tile_staged_rows", C.c_uint64), ("dense_active", C.c_int32),
                 ("dense_tiles", C.c_uint32), ("dense_chunks", C.c_uint64),
-                ("dense_entries", C.c_uint64), ("cold_entries", C.c_uint64)]
+                ("dense_entries", C.c_uint64), ("cold_entries", C.c_uint64),
+                ("hub_active", C.c_int32), ("hub_rows", C.c_uint32),
+                ("hub_entries", C.c_uint64), ("hub_chunks", C.c_uint64)]
 
 
 class _Stats(C.Structure):
@@ -133,6 +135,7 @@ _sig = {
     "cbm_b200_spmv": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp]),
     "cbm_b200_get_info": (C.c_int, [_vp, C.POINTER(_Info)]),
     "cbm_b200_plan_dense": (C.c_int, [C.POINTER(_CbmView), C.c_uint32, C.POINTER(_u64)]),
+    "cbm_b200_plan_hub": (C.c_int, [C.POINTER(_CbmView), C.c_int32, C.POINTER(_u64)]),
     "cbm_b200_dense_matmul": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp]),
     "cbm_b200_gcn_forward": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "cbm_b200_gemm_parts": (C.c_int, [C.POINTER(_vp), C.POINTER(_i64), _i32, _i64, _vp, _i64,
@@ -367,6 +370,16 @@ def plan_dense(c: CbmMatrix, dense_min: int = 0) -> dict:
     return dict(zip(keys, (int(x) for x in st)))
 
 
+def plan_hub(c: CbmMatrix, mode: int = -1) -> dict:
+    """Host-only plan of the hub-row panel: what an upload with
+    hub=mode would take off the streaming kernel."""
+    st = (_u64 * 6)()
+    v = c._view()
+    _check(_lib.cbm_b200_plan_hub(C.byref(v), mode, st))
+    keys = ("active", "rows", "entries", "chunks", "pieces", "rest_deltas")
+    return dict(zip(keys, (int(x) for x in st)))
+
+
 def generate_graph(kind: str, params, seed: int) -> CsrBinaryMatrix:
     """Seeded synthetic graph (see include/cbm_b200.h and DESIGN.md §Workloads)."""
     p = (C.c_double * len(params))(*[float(x) for x in params])
@@ -492,7 +505,7 @@ class DeviceCbm:
                  prescale: int = -1, kernel: str = "auto", max_segments: int = 0,
                  flatten_gain: int = -1, prefetch: bool = False, tile: int = -1,
                  tile_rows: int = 0, tile_stage: int = 0, tile_vec: int = 0,
-                 dense: int = -1, dense_min: int = 0, _cbm1_path=None):
+                 dense: int = -1, dense_min: int = 0, hub: int = -1, _cbm1_path=None):
         opt = _Options()
         _lib.cbm_b200_default_options(C.byref(opt))
         opt.device = -1 if device is None else int(device)
@@ -512,6 +525,7 @@ class DeviceCbm:
         opt.tile_vec = tile_vec
         opt.dense = int(dense)
         opt.dense_min = dense_min
+        opt.hub = int(hub)
         self._h = _vp()
         if _cbm1_path is not None:
             _check(_lib.cbm_b200_upload_cbm1(str(_cbm1_path).encode(), C.byref(opt),

@@ -12,6 +12,7 @@
 #include "../../include/cbm_b200.h"
 #include "cbm_host.hpp"
 #include "dense_layout.hpp"
+#include "hub_layout.hpp"
 #include "device.hpp"
 #include "layout.hpp"
 
@@ -233,6 +234,7 @@ void cbm_b200_default_options(cbm_b200_options* o) {
   o->tile_vec = 0;
   o->dense = -1;
   o->dense_min = 0;
+  o->hub = -1;
 }
 
 int cbm_b200_upload(const cbm_b200_cbm_view* c, const cbm_b200_options* opt,
@@ -465,7 +467,7 @@ int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* o) {
     const auto& L = h->d->info;
     o->n_rows = L.n_rows;
     o->n_cols = L.n_cols;
-    o->nnz_delta = L.nnz;
+    o->nnz_delta = h->d->hub_on ? h->d->hub_nnz : L.nnz;   // (the uploaded CBM's count)
     o->nnz_effective = L.nnz_effective;
     o->n_flattened = L.n_flattened;
     o->n_levels = L.n_levels;
@@ -493,6 +495,10 @@ int cbm_b200_get_info(const cbm_b200_matrix* h, cbm_b200_info* o) {
     o->dense_chunks = D.n_chunks;
     o->dense_entries = D.dense_entries;
     o->cold_entries = D.cold_entries;
+    o->hub_active = h->d->hub_on ? 1 : 0;
+    o->hub_rows = h->d->hub_n_rows;
+    o->hub_entries = h->d->hub_entries;
+    o->hub_chunks = h->d->hub_chunks;
   });
 }
 
@@ -513,6 +519,22 @@ int cbm_b200_plan_dense(const cbm_b200_cbm_view* c, uint32_t dense_min, uint64_t
     stats[3] = D.cold_entries;
     stats[4] = D.padded_slots;
     stats[5] = max_rows;
+  });
+}
+
+// Host-only: the hub-row panel an upload with hub = mode would build
+// (hub_layout.hpp). stats: active, rows, entries, chunks, pieces, rest deltas.
+int cbm_b200_plan_hub(const cbm_b200_cbm_view* c, int32_t mode, uint64_t stats[6]) {
+  return guard([&] {
+    need(c && stats, "plan_hub: null argument");
+    cbmb::validate_view(*c);
+    const cbmb::HubPlan H = cbmb::plan_hub(*c, mode, 148);
+    stats[0] = H.on ? 1 : 0;
+    stats[1] = H.rows.size();
+    stats[2] = H.entries;
+    stats[3] = H.n_chunks;
+    stats[4] = H.n_pieces;
+    stats[5] = H.on ? H.rest_row_ptr.back() : c->nnz;
   });
 }
 

@@ -173,8 +173,6 @@ struct Params {
   uint32_t ldxb;              // ldx in bytes (< 2^32): one IMAD.WIDE per gathered row
   const float* base;          // optional addend per output row (unscaled), may alias y
   long long ldbase;
-  uint32_t cmask;             // column bits of a dcol word (layout.hpp: kColMask when marked)
-  uint32_t hot;               // bit 0: L1 marks honoured, bit 1: L2 marks honoured
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -256,34 +254,6 @@ __device__ __forceinline__ void cp_async_n(float* dst, const float* src, uint32_
 template <int V>
 __device__ __forceinline__ void cp_async_z(float* dst, const float* src, bool on) {
   cp_async_n<V>(dst, src, on ? uint32_t(V * 4) : 0u);
-}
-// 16-byte copy with the residency the layout marked for the row (layout.hpp):
-// through L1 when `l1` (cp.async.ca: the row stays in the SM's L1 for its other
-// warps), else L2 only; `policy` is the row's L2 eviction priority.
-__device__ __forceinline__ void cp_async_hot(float* dst, const float* src, uint32_t n,
-                                             uint32_t l1, uint64_t policy) {
-  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
-      "@p cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2, %4;\n\t"
-      "@!p cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %4;\n\t}"
-      ::"r"(d), "l"(src), "r"(n), "r"(l1), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_normal() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-  return p;
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -540,11 +510,6 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
   const char* ixb = reinterpret_cast<const char*>(p.x);  // this ticket's column slab of X row 0
   bool ifull = true;  // warp-uniform: every segment of every lane inside the matrix
   Wd win = window(0), wn1 = window(1), wn2 = window(2), wlong{0u, 0.0f};
-  // residency marks (V = 4 rows only): policies made once per warp
-  const bool hot_on = V == 4 && p.hot != 0;
-  const uint64_t pol_keep = (p.hot & 2u) ? l2_policy_evict_last() : l2_policy_normal();
-  const uint64_t pol_pass = (p.hot & 2u) ? l2_policy_evict_first() : l2_policy_normal();
-  const uint32_t l1_bit = (p.hot & 1u) ? 0x40000000u : 0u;
   uint32_t iseq = 0;     // ring slots issued (B per group)
   uint32_t icommit = 0;  // ring groups committed; the consumer's k-th group is the k-th
   uint32_t cgroup = 0;   // groups consumed
@@ -610,21 +575,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
         else val = __int_as_float(0x3F800000u | (win.c & 0x80000000u));
         if (q < kGroup) sm.val[(q % H) * D + s0 + q / H] = q < n ? val : 0.0f;
       }
-      if (V == 4 && ifull && hot_on) {  // marked layouts: per-row cache residency
-        if constexpr (V == 4) {
-#pragma unroll
-          for (int b = 0; b < B; ++b) {
-            const bool on = uint32_t(b) * H + hl < n;
-            const uint32_t cw = cwb[b];
-            const float* src = reinterpret_cast<const float*>(ixb + (uint64_t)(cw & p.cmask) * p.ldxb);
-            const uint32_t sz = on ? 16u : 0u;
-            const uint64_t pol = (cw & 0x20000000u) ? pol_keep : pol_pass;
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-              cp_async_hot(&sm.ring[s0 + b][u][lane * V], src + u * kSeg, sz, cw & l1_bit, pol);
-          }
-        }
-      } else if (ifull) {  // straight-line copies: one size for all segments, immediate
+      if (ifull) {  // straight-line copies: one size for all segments, immediate
         // segment offsets, one IMAD.WIDE per row address (byte pitch < 2^32)
 #pragma unroll
         for (int b = 0; b < B; ++b) {
@@ -632,7 +583,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
           // 0 (fetch, or a lane the rotation left in place): a valid row either
           // way, and nothing is read (size 0)
           const bool on = uint32_t(b) * H + hl < n;
-          const uint32_t c = cwb[b] & p.cmask;
+          const uint32_t c = cwb[b] & 0x7FFFFFFFu;
           const float* src = reinterpret_cast<const float*>(ixb + (uint64_t)c * p.ldxb);
           const uint32_t sz = on ? uint32_t(V * 4) : 0u;
 #pragma unroll
@@ -642,7 +593,7 @@ __global__ void CBM_LAUNCH_BOUNDS(U) cbm_kernel(const Params p) {
 #pragma unroll
         for (int b = 0; b < B; ++b) {
           const bool on = uint32_t(b) * H + hl < n;
-          const uint32_t c = on ? (cwb[b] & p.cmask) : 0u;
+          const uint32_t c = on ? (cwb[b] & 0x7FFFFFFFu) : 0u;
           const float* src = reinterpret_cast<const float*>(ixb + (uint64_t)c * p.ldxb);
           if constexpr (U == 1 && H == 1) {  // the matrix edge: a real call keeps
             // the one-segment hot path unpredicated (A/B: cfg[2] 921 -> 838 us; with
@@ -878,7 +829,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) cbm_spmv_kernel(const Param
 #pragma unroll
       for (int q = 0; q < K; ++q) {
         const bool on = k0 + 32u * q + lane < r.end;
-        xv[q] = on ? __ldg(p.x + (uint64_t)(cw[q] & p.cmask) * p.ldx32) : 0.0f;
+        xv[q] = on ? __ldg(p.x + (uint64_t)(cw[q] & 0x7FFFFFFFu) * p.ldx32) : 0.0f;
         if constexpr (SC == 0) val[q] = on ? __int_as_float(0x3F800000u | (cw[q] & 0x80000000u)) : 0.0f;
       }
 #pragma unroll
@@ -1060,8 +1011,39 @@ uint32_t pick_vec(uint32_t d, const float* x, int64_t ldx, const float* y, int64
 }
 }  // namespace
 
+namespace {
+void spmm_rest(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y, int64_t ldy,
+               void* stream, bool relu, const float* base, int64_t ldbase);
+}
+
 void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
                  int64_t ldy, void* stream, bool relu, const float* base, int64_t ldbase) {
+  spmm_rest(h, x, ldx, d, y, ldy, stream, relu, base, ldbase);
+  if (!h->hub_on || h->info.n_rows == 0 || d == 0) return;
+  // hub-row panel: this operator's layout leaves the hub rows empty (zeros in
+  // Y so far); their rows come from the tensor cores, or, for X narrower than
+  // that path takes, from the hub rows' own streaming operator
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint32_t launches = h->last_launches;
+  if (d >= kDenseMinD) {
+    if (ldx >= (int64_t(1) << 30))
+      throw invalid_argument("spmm: leading dimension of X must be below 2^30");
+    auto& ws = h->ws[stream];
+    h->last_launches = launches + 1;  // the panel's tensor kernel; hub_spmm adds its reductions
+    hub_spmm(h, x, ldx, d, y, ldy, relu, ws.hub_part, ws.hub_part_cap, s);
+  } else {
+    const uint32_t dpad = (d + 3) & ~3u;
+    auto& ws = h->ws[stream];
+    grow(ws.hub_part, ws.hub_part_cap, uint64_t(h->hub_n_rows) * dpad, "workspace hub rows");
+    device_spmm(h->hub_op, x, ldx, d, ws.hub_part, dpad, stream, relu);
+    hub_scatter(ws.hub_part, dpad, h->hrows, h->hub_n_rows, d, y, ldy, s);
+    h->last_launches = launches + h->hub_op->last_launches + 1;
+  }
+}
+
+namespace {
+void spmm_rest(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y, int64_t ldy,
+               void* stream, bool relu, const float* base, int64_t ldbase) {
   const Layout& L = h->info;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   h->last_launches = 0;
@@ -1188,11 +1170,6 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
   if (uint64_t(ldin) >= (uint64_t(1) << 30))
     throw invalid_argument("spmm: leading dimension of X must be below 2^30");
   p.ldxb = uint32_t(ldin) * 4u;
-  p.cmask = L.col_mask;
-  p.hot = 0;
-  if (L.hot_l1) p.hot |= 1u;
-  if (L.hot_l2 && uint64_t(L.n_cols) * d * sizeof(float) > uint64_t(h->l2_bytes)) p.hot |= 2u;
-  if (const char* e = std::getenv("CBM_B200_HOT_USE")) p.hot &= uint32_t(std::atoi(e));  // dev A/B
   if (H > 1) {
     if (H == 2) run_groups<2>(p, tickets, n_slabs, norm, scl, h, s);
     else if (H == 4) run_groups<4>(p, tickets, n_slabs, norm, scl, h, s);
@@ -1239,5 +1216,7 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
     }
   }
 }
+
+}  // namespace
 
 }  // namespace cbmb

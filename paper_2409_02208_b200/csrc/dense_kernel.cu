@@ -529,19 +529,121 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
   }
 }
 
+// Hub panel: the pieces' partial rows are combined kHubFanIn at a time in
+// ascending piece order (a fixed tree: deterministic), round-to-nearest adds.
+// Group j of `in` (pieces [j F, j F + F)) becomes piece j of `out`; the last
+// level (one group) writes Y[rows[r], :] = sum (*) row scale, optional ReLU.
+// One thread per (group, hub row, float4).
+__global__ void hub_reduce_kernel(const float* __restrict__ in, uint32_t n_pieces, uint32_t dpad,
+                                  float* __restrict__ out, const uint32_t* __restrict__ rows,
+                                  const float* __restrict__ srow, uint32_t n_rows, uint32_t d,
+                                  float* __restrict__ y, long long ldy, uint32_t relu) {
+  const uint32_t per_row = dpad / 4;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_rows * per_row) return;
+  const uint32_t r = i / per_row, f = (i % per_row) * 4;
+  const uint32_t g = blockIdx.y, p_lo = g * kHubFanIn;
+  const uint32_t p_hi = min(n_pieces, p_lo + kHubFanIn);
+  const size_t pstride = size_t(kDenseRows) * dpad;
+  const float* src = in + size_t(r) * dpad + f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t p0 = p_lo; p0 < p_hi; p0 += 8) {
+    float4 v[8];
+#pragma unroll
+    for (uint32_t q = 0; q < 8; ++q)
+      v[q] = p0 + q < p_hi ? __ldcs(reinterpret_cast<const float4*>(src + (p0 + q) * pstride))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (uint32_t q = 0; q < 8; ++q) {
+      acc.x = __fadd_rn(acc.x, v[q].x);
+      acc.y = __fadd_rn(acc.y, v[q].y);
+      acc.z = __fadd_rn(acc.z, v[q].z);
+      acc.w = __fadd_rn(acc.w, v[q].w);
+    }
+  }
+  if (out) {  // an inner level: piece g of the next level
+    *reinterpret_cast<float4*>(out + (size_t(g) * kDenseRows + r) * dpad + f) = acc;
+    return;
+  }
+  const float sc = srow ? srow[r] : 1.0f;
+  float o[4] = {acc.x, acc.y, acc.z, acc.w};
+  float* dst = y + (long long)rows[r] * ldy + f;
+#pragma unroll
+  for (uint32_t e = 0; e < 4; ++e) {
+    if (f + e >= d) break;
+    float w = srow ? __fmul_rn(o[e], sc) : o[e];
+    if (relu && w < 0.0f) w = 0.0f;
+    dst[e] = w;
+  }
+}
+
+__global__ void hub_scatter_kernel(const float* __restrict__ src, uint32_t ld,
+                                   const uint32_t* __restrict__ rows, uint32_t n, uint32_t d,
+                                   float* __restrict__ y, long long ldy) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= uint64_t(n) * d) return;
+  const uint32_t r = uint32_t(i / d), f = uint32_t(i % d);
+  y[(long long)rows[r] * ldy + f] = src[size_t(r) * ld + f];
+}
+
+void dense_launch(DeviceMatrix* h, const uint32_t* tiles, const uint32_t* meta, uint32_t n_tiles,
+                  const float* x, int64_t ldx, uint32_t d, float* y, int64_t ldy, cudaStream_t s);
+
 }  // namespace
 
 void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
                 int64_t ldy, cudaStream_t s) {
-  const DenseLayout& D = h->dense;
+  dense_launch(h, h->dtiles, h->dmeta, h->dense.n_tiles, x, ldx, d, y, ldy, s);
+}
+
+void hub_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y, int64_t ldy,
+              bool relu, float*& part, uint64_t& part_cap, cudaStream_t s) {
+  const uint32_t dpad = (d + 3) & ~3u;
+  // level 0: one 128-row partial per piece; level k: one per kHubFanIn of level k-1
+  const uint64_t rows0 = uint64_t(h->hub_pieces) * kDenseRows;
+  uint64_t total_rows = 0;
+  for (uint32_t n = h->hub_pieces; n > 1; n = (n + kHubFanIn - 1) / kHubFanIn)
+    total_rows += uint64_t(n) * kDenseRows;
+  total_rows = std::max<uint64_t>(total_rows, rows0);
+  grow(part, part_cap, total_rows * dpad, "workspace hub partials");
+  // the pieces are the dense kernel's tiles: "rows" [128 p, 128 p + 128) of
+  // the partial buffer, leading dimension dpad
+  dense_launch(h, h->htiles, h->hmeta, h->hub_pieces, x, ldx, d, part, dpad, s);
+  const uint32_t threads = h->hub_n_rows * (dpad / 4);
+  float* in = part;
+  for (uint32_t n = h->hub_pieces;;) {
+    const uint32_t groups = (n + kHubFanIn - 1) / kHubFanIn;
+    float* out = groups > 1 ? in + uint64_t(n) * kDenseRows * dpad : nullptr;
+    hub_reduce_kernel<<<dim3((threads + 127) / 128, groups), 128, 0, s>>>(
+        in, n, dpad, out, h->hrows, h->hsrow, h->hub_n_rows, d, y, ldy, relu ? 1u : 0u);
+    ck(cudaGetLastError(), "hub_reduce launch");
+    ++h->last_launches;
+    if (groups == 1) break;
+    in = out;
+    n = groups;
+  }
+}
+
+void hub_scatter(const float* src, uint32_t ld, const uint32_t* rows, uint32_t n, uint32_t d,
+                 float* y, int64_t ldy, cudaStream_t s) {
+  const uint64_t total = uint64_t(n) * d;
+  if (total == 0) return;
+  hub_scatter_kernel<<<unsigned((total + 255) / 256), 256, 0, s>>>(src, ld, rows, n, d, y, ldy);
+  ck(cudaGetLastError(), "hub_scatter launch");
+}
+
+namespace {
+
+void dense_launch(DeviceMatrix* h, const uint32_t* tiles, const uint32_t* meta, uint32_t n_tiles,
+                  const float* x, int64_t ldx, uint32_t d, float* y, int64_t ldy, cudaStream_t s) {
   DenseParams p;
   p.x = x;
   p.ldx = ldx;
   p.y = y;
   p.ldy = ldy;
   p.scale = h->info.normalized ? h->scale : nullptr;
-  p.tiles = reinterpret_cast<const uint4*>(h->dtiles);
-  p.meta = h->dmeta;
+  p.tiles = reinterpret_cast<const uint4*>(tiles);
+  p.meta = meta;
   p.n_fb = (d + kDenseFeat - 1) / kDenseFeat;
   p.d = d;
   p.dbg = 0;
@@ -552,7 +654,7 @@ void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float*
     ck(cudaMalloc(&p.trace, 3 * 4096 * 8), "trace");
     ck(cudaMemsetAsync(p.trace, 0, 3 * 4096 * 8, s), "trace");
   }
-  const uint64_t units = uint64_t(D.n_tiles) * p.n_fb;
+  const uint64_t units = uint64_t(n_tiles) * p.n_fb;
   if (units >= 0xFFFFFFFFull) throw invalid_argument("spmm: too many dense-block units");
   p.n_units = uint32_t(units);
   const size_t smem =
@@ -582,5 +684,7 @@ void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float*
     }
   }
 }
+
+}  // namespace
 
 }  // namespace cbmb

@@ -11,6 +11,62 @@
 
 namespace cbmb {
 
+namespace {
+
+// Hub-row panel (hub_layout.hpp): the operator is uploaded WITHOUT its hub
+// rows (the plan's rest view, through the ordinary upload: streaming, tiled or
+// dense-block as that view deserves) and carries the panel beside it.
+DeviceMatrix* upload_with_hub(const cbm_b200_cbm_view& v, const cbm_b200_options& opt,
+                              HubPlan& H) {
+  cbm_b200_options ro = opt;
+  ro.hub = 0;
+  cbm_b200_cbm_view rv{v.n_rows, v.n_cols, H.rest_row_ptr.back(), v.alpha, v.is_normalized,
+                       H.rest_parent.data(), nullptr, H.rest_row_ptr.data(), H.rest_col.data(),
+                       H.rest_val.data(), v.row_scale, v.col_scale};
+  DeviceMatrix* h = device_upload(rv, ro);
+  try {
+    H.rest_parent = {};
+    H.rest_row_ptr = {};
+    H.rest_col = {};
+    H.rest_val = {};
+    auto put = [&](auto*& dst, const auto& vec, const char* what) {
+      using E = typename std::remove_reference_t<decltype(vec)>::value_type;
+      ck(cudaMalloc(&dst, std::max<size_t>(vec.size(), 1) * sizeof(E)), what);
+      if (!vec.empty()) ck(cudaMemcpy(dst, vec.data(), vec.size() * sizeof(E),
+                                      cudaMemcpyHostToDevice), what);
+      h->device_bytes += vec.size() * sizeof(E);
+    };
+    put(h->htiles, H.tiles, "upload hub pieces");
+    put(h->hmeta, H.meta, "upload hub chunk records");
+    put(h->hrows, H.rows, "upload hub rows");
+    if (v.is_normalized) put(h->hsrow, H.hub_row_scale, "upload hub row scales");
+    h->hub_n_rows = uint32_t(H.rows.size());
+    h->hub_pieces = H.n_pieces;
+    h->hub_entries = H.entries;
+    h->hub_chunks = H.n_chunks;
+    h->hub_nnz = v.nnz;
+    // the hub rows alone, for X narrower than the tensor path takes
+    const float* colscale = v.col_scale ? v.col_scale : v.row_scale;
+    cbm_b200_cbm_view hv{h->hub_n_rows, v.n_cols, H.hub_row_ptr.back(), v.alpha, v.is_normalized,
+                         H.hub_parent.data(), nullptr, H.hub_row_ptr.data(), H.hub_col.data(),
+                         H.hub_val.data(), H.hub_row_scale.data(), colscale};
+    cbm_b200_options ho = ro;
+    ho.tile = 0;
+    ho.dense = 0;
+    ho.flatten_gain = 0;
+    h->hub_op = device_upload(hv, ho);
+    h->device_bytes += h->hub_op->device_bytes;
+    h->opt.hub = opt.hub;
+    h->hub_on = true;
+  } catch (...) {
+    device_free(h);
+    throw;
+  }
+  return h;
+}
+
+}  // namespace
+
 DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& opt) {
   // validate + plan on the host first: malformed input is EINVAL, never a CUDA error
   const uint32_t gain = opt.flatten_gain < 0 ? 16u : uint32_t(opt.flatten_gain);
@@ -22,6 +78,15 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
                              opt.device >= 0 ? opt.device : cur) != cudaSuccess)
     sms = 148;
   cudaGetLastError();  // a failed probe must not leak into later error checks
+  if (!opt.order_faithful && opt.hub != 0 && opt.tile != 1 && opt.dense != 1 && v.n_rows > 0 &&
+      (opt.hub > 0 || (v.n_rows >= (1u << 15) && v.nnz >= (1ull << 22)))) {
+    validate_view(v);
+    HubPlan H = plan_hub(v, opt.hub, uint32_t(sms));
+    if (opt.hub > 0 && !H.on)
+      throw invalid_argument("upload: the hub-row panel needs delta rows consistent with "
+                             "their parents' rows");
+    if (H.on) return upload_with_hub(v, opt, H);
+  }
   Layout L = plan_layout(v, opt.order_faithful != 0, opt.split_threshold, opt.chunk, gain,
                          uint32_t(sms) * 20);
   auto* h = new DeviceMatrix;
@@ -50,7 +115,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
       // values: +-row_scale[col], validated by plan_layout)
       std::vector<float> dval(L.dcol.size());
       for (size_t k = 0; k < dval.size(); ++k) {
-        const float sc = L.scale[L.dcol[k] & L.col_mask];
+        const float sc = L.scale[L.dcol[k] & 0x7FFFFFFFu];
         dval[k] = (L.dcol[k] >> 31) ? -sc : sc;
       }
       put(h->dval, dval, "upload dval");
@@ -173,7 +238,11 @@ void device_free(DeviceMatrix* h) {
   for (auto& kv : h->ws)
     if (kv.second.tinterior) cudaFree(kv.second.tinterior);
   if (h->cold) device_free(h->cold);
-  for (void* p : {(void*)h->dtiles, (void*)h->dmeta})
+  if (h->hub_op) device_free(h->hub_op);
+  for (auto& kv : h->ws)
+    if (kv.second.hub_part) cudaFree(kv.second.hub_part);
+  for (void* p : {(void*)h->dtiles, (void*)h->dmeta, (void*)h->htiles, (void*)h->hmeta,
+                  (void*)h->hrows, (void*)h->hsrow})
     if (p) cudaFree(p);
   for (void* p : {(void*)h->dcol, (void*)h->dval, (void*)h->rec, (void*)h->srow, (void*)h->scale,
                   (void*)h->xstage, (void*)h->ystage, (void*)h->tdcol, (void*)h->tdval,
@@ -203,6 +272,17 @@ void device_reserve(DeviceMatrix* h, uint64_t d, void* stream) {
   if (h->tile_on) grow(ws.tinterior, ws.tinterior_cap, uint64_t(h->tile.n_interior) * dpad,
                        "workspace tile interior");
   if (h->cold) device_reserve(h->cold, d, stream);
+  if (h->hub_on) {
+    if (d >= kDenseMinD) {
+      uint64_t rows = 0;
+      for (uint32_t n = h->hub_pieces; n > 1; n = (n + kHubFanIn - 1) / kHubFanIn)
+        rows += uint64_t(n) * kDenseRows;
+      rows = std::max<uint64_t>(rows, uint64_t(h->hub_pieces) * kDenseRows);
+      grow(ws.hub_part, ws.hub_part_cap, rows * dpad, "workspace hub partials");
+    } else {
+      device_reserve(h->hub_op, d, stream);
+    }
+  }
 }
 
 // Host-buffer entry point. Columns are independent (kernels.cpp:27-62), so X

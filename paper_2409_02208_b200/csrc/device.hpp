@@ -14,6 +14,7 @@
 #include "errors.hpp"
 #include "layout.hpp"
 #include "dense_layout.hpp"
+#include "hub_layout.hpp"
 #include "tile_layout.hpp"
 
 namespace cbmb {
@@ -49,6 +50,17 @@ struct DeviceMatrix {
   uint32_t* dtiles = nullptr;
   uint32_t* dmeta = nullptr;
   struct DeviceMatrix* cold = nullptr;
+  // hub-row panel (hub_layout.hpp): this operator's own layout is then the
+  // matrix WITHOUT its hub rows; the panel adds them after the multiply
+  bool hub_on = false;
+  uint32_t hub_n_rows = 0, hub_pieces = 0;
+  uint64_t hub_entries = 0, hub_chunks = 0;
+  uint64_t hub_nnz = 0;          // deltas of the uploaded CBM (info: the view's own count)
+  uint32_t* htiles = nullptr;    // per piece: piece * 128, 128, first chunk, chunks
+  uint32_t* hmeta = nullptr;     // chunk records (dense_layout.hpp)
+  uint32_t* hrows = nullptr;     // the hub rows' ids
+  float* hsrow = nullptr;        // normalized: their row scales
+  struct DeviceMatrix* hub_op = nullptr;  // the hub rows alone (X narrower than the tensor path)
   // per-call workspace, one per stream (concurrent calls on distinct streams
   // never share flags or scratch); grown on demand, or by cbm_b200_reserve
   struct Workspace {
@@ -64,6 +76,8 @@ struct DeviceMatrix {
     uint64_t xs_cap = 0;
     float* gcn_h = nullptr;      // GCN hidden activations (2 x n x hid)
     uint64_t gcn_h_cap = 0;
+    float* hub_part = nullptr;   // hub panel: per piece, 128 partial rows
+    uint64_t hub_part_cap = 0;
     uint32_t epoch = 0;          // ready-flag stamp of the last call
   };
   std::map<void*, Workspace> ws;
@@ -101,6 +115,13 @@ void device_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float
 inline constexpr uint32_t kDenseMinD = 32;  // narrower X stays on the streaming kernel
 void dense_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y,
                 int64_t ldy, cudaStream_t s);
+// Y[hub rows] = (A X)[hub rows]: the panel's units on the dense-block kernel,
+// then the fixed-order reduction of their partials (row scale / ReLU applied).
+void hub_spmm(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* y, int64_t ldy,
+              bool relu, float*& part, uint64_t& part_cap, cudaStream_t s);
+// out[rows[i], :] = src[i, :] (the narrow-X form of the panel: rows from hub_op)
+void hub_scatter(const float* src, uint32_t ld, const uint32_t* rows, uint32_t n, uint32_t d,
+                 float* y, int64_t ldy, cudaStream_t s);
 void device_dense_matmul(const float* a, uint32_t m, uint32_t k, const float* b, uint32_t n,
                          float* c, void* stream);
 void device_fast_matmul(const float* a, uint32_t m, uint32_t k, const float* b, uint32_t n,

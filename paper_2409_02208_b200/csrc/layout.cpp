@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <numeric>
 #include <string>
 
@@ -57,6 +58,73 @@ bool reconstruct_full_rows(const cbm_b200_cbm_view& v, const std::vector<uint32_
     if (out != end) return false;
   }
   return true;
+}
+
+// load_cbm's structural checks (io.cpp:346-380) on a view, with its messages:
+// what plan_layout verifies before it lays anything out. For callers that
+// must read the view before a layout exists (hub_layout.cpp).
+void validate_view(const cbm_b200_cbm_view& v) {
+  const uint32_t m = v.n_rows;
+  if (m >= kInteriorBit) throw invalid_argument("upload: too many rows for the device layout");
+  if (v.n_cols >= kSignBit) throw invalid_argument("upload: too many columns for the device layout");
+  if (m && (!v.parent || !v.row_ptr)) throw invalid_argument("upload: null array in view");
+  if (v.row_ptr && v.row_ptr[0] != 0) throw invalid_argument("csr: row_ptr[0] must be 0");
+  const uint64_t nnz = m ? v.row_ptr[m] : 0;
+  if (nnz != v.nnz) throw invalid_argument("csr: row_ptr back must equal nnz");
+  if (nnz >= 0xFFFFFFFFull) throw invalid_argument("upload: more than 2^32-1 deltas");
+  if (nnz && (!v.col_idx || !v.values)) throw invalid_argument("upload: null array in view");
+  const bool norm = v.is_normalized != 0;
+  const float* colscale = v.col_scale ? v.col_scale : v.row_scale;
+  if (norm) {
+    if (v.n_rows != v.n_cols && !v.col_scale)
+      throw invalid_argument("normalized container must be square");
+    if (!v.row_scale && m) throw invalid_argument("upload: normalized view without row_scale");
+    for (uint32_t r = 0; r < m; ++r)
+      if (!std::isfinite(v.row_scale[r]) || v.row_scale[r] <= 0.0f)
+        throw invalid_argument("row_scale entries must be positive and finite");
+    if (v.col_scale)
+      for (uint32_t c = 0; c < v.n_cols; ++c)
+        if (!std::isfinite(v.col_scale[c]) || v.col_scale[c] <= 0.0f)
+          throw invalid_argument("row_scale entries must be positive and finite");
+  }
+  for (uint32_t r = 0; r < m; ++r) {
+    const uint64_t lo = v.row_ptr[r], hi = v.row_ptr[r + 1];
+    if (lo > hi) throw invalid_argument("csr: row_ptr must be non-decreasing");
+    if (hi > nnz) throw invalid_argument("csr: row_ptr back must equal nnz");
+    for (uint64_t k = lo; k < hi; ++k) {
+      const uint32_t c = v.col_idx[k];
+      if (c >= v.n_cols)
+        throw invalid_argument("csr: column index out of range in row " + std::to_string(r));
+      if (k + 1 < hi && c >= v.col_idx[k + 1])
+        throw invalid_argument("csr: row " + std::to_string(r) + " is not strictly increasing");
+      const float val = v.values[k];
+      const float mag = norm ? colscale[c] : 1.0f;
+      if (val != mag && val != -mag)
+        throw invalid_argument(norm ? "delta values disagree with the column scales"
+                                    : "delta values must be +1 or -1");
+    }
+  }
+  for (uint32_t x = 0; x < m; ++x) {
+    const uint32_t p = v.parent[x];
+    if (p == kVirtual) continue;
+    if (p >= m || p == x) throw invalid_argument("chain: bad parent link at row " + std::to_string(x));
+  }
+  // acyclic: every row reaches a root in at most m steps (path compression by
+  // marking rows already known to end at a root)
+  std::vector<uint8_t> ok(m, 0);
+  std::vector<uint32_t> path;
+  for (uint32_t x = 0; x < m; ++x) {
+    uint32_t u = x;
+    path.clear();
+    while (u != kVirtual && !ok[u]) {
+      if (path.size() > m) throw invalid_argument("chain: parent links contain a cycle");
+      ok[u] = 2;  // on the current path
+      path.push_back(u);
+      u = v.parent[u];
+      if (u != kVirtual && ok[u] == 2) throw invalid_argument("chain: parent links contain a cycle");
+    }
+    for (uint32_t w : path) ok[w] = 1;
+  }
 }
 
 Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t split_threshold,
@@ -228,39 +296,6 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   if (L.nnz_effective >= 0xFFFFFFFFull)  // dcol offsets are 32-bit on the device
     throw invalid_argument("upload: more than 2^32-1 deltas after flattening "
                            "(upload with flatten_gain = 0)");
-  // Cache-residency marks (layout.hpp). Power-law matrices reference a few
-  // thousand columns from most rows (cfg[4]: the top 32 columns take 11% of the
-  // entries, the top 40k 61%) while the bulk of X is touched a handful of
-  // times. The marks let the kernel keep the shared rows in L1 / L2 and stream
-  // the rest past them. Only when X (at 1 KB per row) is well beyond L2.
-  {
-    uint32_t k1 = 0, k2 = 0;
-    if (v.n_cols < kHotL2Bit && uint64_t(v.n_cols) > (96ull << 10)) {
-      k1 = 24;
-      k2 = 32u << 10;
-    }
-    if (const char* e = std::getenv("CBM_B200_HOT_L1")) k1 = uint32_t(std::atoll(e));  // dev A/B
-    if (const char* e = std::getenv("CBM_B200_HOT_L2")) k2 = uint32_t(std::atoll(e));
-    if (v.n_cols >= kHotL2Bit) k1 = k2 = 0;
-    k1 = std::min(k1, v.n_cols);
-    k2 = std::min(k2, v.n_cols);
-    if ((k1 || k2) && !ecol.empty()) {
-      std::vector<uint32_t> cnt(v.n_cols, 0);
-      for (uint32_t w : ecol) ++cnt[w & ~kSignBit];
-      std::vector<uint32_t> by(v.n_cols);
-      std::iota(by.begin(), by.end(), 0u);
-      const uint32_t top = std::max(k1, k2);
-      auto more = [&](uint32_t a, uint32_t b) { return cnt[a] != cnt[b] ? cnt[a] > cnt[b] : a < b; };
-      std::partial_sort(by.begin(), by.begin() + top, by.end(), more);
-      std::vector<uint32_t> mark(v.n_cols, 0);
-      for (uint32_t i = 0; i < k2; ++i)
-        if (cnt[by[i]] >= 2) mark[by[i]] |= kHotL2Bit, ++L.hot_l2;
-      for (uint32_t i = 0; i < k1; ++i)
-        if (cnt[by[i]] >= 2) mark[by[i]] |= kHotL1Bit, ++L.hot_l1;
-      for (uint32_t& w : ecol) w |= mark[w & ~kSignBit];
-      if (L.hot_l1 || L.hot_l2) L.col_mask = kColMask;
-    }
-  }
 
   // ROW items: by depth, ascending row id inside a level (stable counting sort)
   uint32_t max_depth = 0;
@@ -273,6 +308,42 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   {
     std::vector<uint32_t> cur(L.level_ptr.begin(), L.level_ptr.end() - 1);
     for (uint32_t x = 0; x < m; ++x) rows[cur[depth[x]]++] = x;
+  }
+  // X far beyond L2 (default mode): rows of one level are taken by the
+  // smallest of their own id and their rarely referenced ("tail") columns
+  // instead of by row id. Rows that share tail columns (the members of one
+  // clique of a clique overlay each hold all the others) get the same key and
+  // run at the same time, so a tail X row is read from DRAM once and met in L2
+  // by the others; in row-id order each of them misses (cfg[4]: the short
+  // rows' tail columns alone are ~12 GB of 1 KB misses per multiply). Columns
+  // among the 32k most referenced stay L2-resident anyway and are not keyed.
+  const bool big_x = !order_faithful && uint64_t(v.n_cols) > (64ull << 10) &&
+                     !std::getenv("CBM_B200_NO_ROW_KEYS");
+  if (big_x && m > 1 && !ecol.empty()) {
+    std::vector<uint32_t> cnt(v.n_cols, 0);
+    for (uint32_t w : ecol) ++cnt[w & ~kSignBit];
+    uint32_t thr = 0;  // reference count of the 32k-th most referenced column
+    {
+      std::vector<uint32_t> c2(cnt);
+      const size_t k = std::min<size_t>(c2.size() - 1, 32u << 10);
+      std::nth_element(c2.begin(), c2.begin() + k, c2.end(), std::greater<uint32_t>());
+      thr = c2[k];
+    }
+    std::vector<uint32_t> key(m);
+    for (uint32_t x = 0; x < m; ++x) {
+      uint32_t k = x < v.n_cols ? x : v.n_cols - 1;
+      for (uint64_t j = eptr[x]; j < eptr[x + 1]; ++j) {
+        const uint32_t c = ecol[j] & ~kSignBit;
+        if (cnt[c] <= thr) {  // columns ascend: the first tail column is the smallest
+          k = std::min(k, c);
+          break;
+        }
+      }
+      key[x] = k;
+    }
+    for (uint32_t lv = 0; lv < L.n_levels; ++lv)
+      std::stable_sort(rows.begin() + L.level_ptr[lv], rows.begin() + L.level_ptr[lv + 1],
+                       [&](uint32_t a, uint32_t b) { return key[a] < key[b]; });
   }
 
   // split plan for long rows (default mode only)
@@ -315,7 +386,7 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
       if (len > split_threshold) {
         const uint32_t* e = ecol.data() + eptr[r];
         const bool banded = band_cols && len >= 16ull * n_bands;
-        auto band = [&](uint32_t w) { return (w & L.col_mask) / band_cols; };
+        auto band = [&](uint32_t w) { return (w & ~kSignBit) / band_cols; };
         uint32_t start = 0;
         cuts.push_back(0);
         for (uint32_t k = 1; k < len; ++k) {
@@ -435,7 +506,7 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
     std::iota(L.order.begin(), L.order.end(), 0u);
     std::vector<uint32_t> key(n_leaf);
     for (uint64_t t = 0; t < n_leaf; ++t)
-      key[t] = (ecol[own_lo[t]] & L.col_mask) / band_cols;
+      key[t] = (ecol[own_lo[t]] & ~kSignBit) / band_cols;
     std::stable_sort(L.order.begin(), L.order.begin() + n_leaf,
                      [&](uint32_t a, uint32_t b) { return key[a] < key[b]; });
   }

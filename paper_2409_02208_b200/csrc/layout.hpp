@@ -27,16 +27,6 @@ namespace cbmb {
 inline constexpr uint32_t kInteriorBit = 0x80000000u;
 inline constexpr uint32_t kSignBit = 0x80000000u;
 inline constexpr uint32_t kNoItem = 0xFFFFFFFFu;
-// Cache-residency marks of a delta's column (layouts with n_cols < 2^29; set
-// by plan_layout, read by the streaming kernel's copies):
-//   kHotL1Bit  one of the few most referenced columns: its X row is copied
-//              through L1 (cp.async.ca), where it stays for the SM's other warps
-//   kHotL2Bit  one of the columns whose X rows together fit L2: copied with an
-//              evict_last policy; every other gather is evict_first, so one-time
-//              rows do not push the shared ones out of L2
-inline constexpr uint32_t kHotL1Bit = 0x40000000u;
-inline constexpr uint32_t kHotL2Bit = 0x20000000u;
-inline constexpr uint32_t kColMask = 0x1FFFFFFFu;
 inline constexpr uint32_t kFanIn = 32;  // partials combined per MERGE / ROW item
 
 struct Layout {
@@ -68,8 +58,6 @@ struct Layout {
   std::vector<float> scale;     // column scale (normalized): row_scale, or the view's col_scale
   std::vector<float> row_scale; // the rows' own scale (normalized)
   std::vector<uint32_t> item_beg;  // n_items + 1: delta prefix by item (kept on the host)
-  uint32_t hot_l1 = 0, hot_l2 = 0;  // columns marked kHotL1Bit / kHotL2Bit (0: no marks)
-  uint32_t col_mask = ~kSignBit;    // column bits of a dcol word (kColMask when marked)
   uint32_t band_cols = 0;       // columns per band (0: the long rows' pieces are not banded)
   std::vector<uint32_t> order;  // processing order of the items (empty: item order)
   std::vector<uint32_t> level_ptr;  // ROW-item offsets of each level (relative to the ROW block)
@@ -82,6 +70,9 @@ struct Layout {
 // inconsistent with its parent's row (layout.cpp).
 bool reconstruct_full_rows(const cbm_b200_cbm_view& v, const std::vector<uint32_t>& bfs,
                            std::vector<uint64_t>& fptr, std::vector<uint32_t>& fcol);
+
+// The structural checks alone (throws like plan_layout).
+void validate_view(const cbm_b200_cbm_view& v);
 
 Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t split_threshold,
                    uint32_t chunk, uint32_t flatten_gain, uint32_t warps_hint);
