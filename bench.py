@@ -411,16 +411,26 @@ def roofline_for(info, ms, n_out, n_cols, d_local, normalized, workload):
                     - int(info["tile_staged_deltas"])) * d_local * 4
     else:
         l2_bytes = int(info["nnz_effective"]) * d_local * 4
+    hub = bool(info.get("hub_active")) and d_local >= 32
+    if hub:
+        # the hub-row panel loads one X row slice per chunk column for all of
+        # its rows; nnz_effective above already excludes those rows
+        l2_bytes += int(info["hub_chunks"]) * 32 * d_local * 4
     r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
          "frac": achieved / peak, "traffic": traffic_for(workload), "b_alg_bytes": b_alg,
-         "kernel": ("dense_kernel (tcgen05) + cbm_kernel (cold entries)" if dense else
-                    "tile_kernel" if tiled else "cbm_kernel"), "peak_source": peak_src,
+         "kernel": (("dense_kernel (tcgen05) + cbm_kernel (cold entries)" if dense else
+                     "tile_kernel" if tiled else "cbm_kernel")
+                    + (" + dense_kernel (tcgen05, hub-row panel) + hub_reduce_kernel" if hub else "")),
+         "peak_source": peak_src,
          # what bounds the gather: X rows moved L2 -> SM per step (one row per
          # summed delta)
          "l2_gather": {"bytes": l2_bytes,
                        "achieved_tbps": l2_bytes / (ms * 1e-3) / 1e12 if ms > 0 else 0.0}}
     if tiled:
         r["smem_gather_bytes"] = int(info["tile_staged_deltas"]) * d_local * 4
+    if hub:
+        r["hub_panel"] = {"rows": int(info["hub_rows"]), "entries": int(info["hub_entries"]),
+                          "chunks": int(info["hub_chunks"])}
     return r
 
 

@@ -52,10 +52,20 @@ namespace cbmb {
 
 namespace {
 
+// Role counts (measured defaults; overridable for A/B builds, `make alt`).
+#ifndef DENSE_SETS
+#define DENSE_SETS 2
+#endif
+#ifndef DENSE_EXPANDERS
+#define DENSE_EXPANDERS 4
+#endif
+#ifndef DENSE_GATHERERS
+#define DENSE_GATHERERS 12
+#endif
 constexpr int kStages = 4;
-constexpr int kSets = 2;       // converter sets (set j owns chunks g = j mod kSets)
-constexpr int kExpanders = 4;
-constexpr int kGatherers = 12; // cp.async gatherers: warp i copies rows i, i+12, i+24 of every chunk
+constexpr int kSets = DENSE_SETS;       // converter sets (set j owns chunks g = j mod kSets)
+constexpr int kExpanders = DENSE_EXPANDERS;
+constexpr int kGatherers = DENSE_GATHERERS; // cp.async gatherers: warp i copies rows i, i+G, i+2G... of every chunk
 constexpr int kRowsPerGatherer = (kDenseK + kGatherers - 1) / kGatherers;
 constexpr int kMeta = 32;      // metadata ring depth (chunks)
 constexpr int kXSlots = 6;     // staged X' slices in shared memory (chunks in flight)
@@ -63,6 +73,7 @@ constexpr int kGath0 = 2 + kExpanders;       // first gatherer warp
 constexpr int kProd0 = kGath0 + kGatherers;  // first converter warp
 constexpr int kEpi0 = kProd0 + 4 * kSets;    // first epilogue warp
 constexpr int kWarps = kEpi0 + 4;
+static_assert(kWarps <= 32, "one CTA: at most 1024 threads");
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAccCol = 0;       // two accumulators: columns [0,128), [128,256)

@@ -149,6 +149,7 @@ DeviceMatrix* device_upload(const cbm_b200_cbm_view& v, const cbm_b200_options& 
         co.tile = 0;
         co.dense = 0;
         co.flatten_gain = 0;
+        if (const char* e = std::getenv("CBM_B200_COLD_SEGS")) co.max_segments = std::atoi(e);  // dev A/B
         h->cold = device_upload(cv, co);
         h->device_bytes += h->cold->device_bytes;
       }

@@ -23,7 +23,7 @@
 namespace cbmb {
 
 inline constexpr uint32_t kHubPieceChunks = 32;  // chunks per piece (accumulation length)
-inline constexpr uint32_t kHubFanIn = 32;        // partial rows combined per reduction step
+inline constexpr uint32_t kHubFanIn = 64;        // partial rows combined per reduction step
 
 struct HubPlan {
   bool on = false;

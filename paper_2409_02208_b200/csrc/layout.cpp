@@ -3,7 +3,6 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
-#include <functional>
 #include <numeric>
 #include <string>
 
@@ -308,42 +307,6 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
   {
     std::vector<uint32_t> cur(L.level_ptr.begin(), L.level_ptr.end() - 1);
     for (uint32_t x = 0; x < m; ++x) rows[cur[depth[x]]++] = x;
-  }
-  // X far beyond L2 (default mode): rows of one level are taken by the
-  // smallest of their own id and their rarely referenced ("tail") columns
-  // instead of by row id. Rows that share tail columns (the members of one
-  // clique of a clique overlay each hold all the others) get the same key and
-  // run at the same time, so a tail X row is read from DRAM once and met in L2
-  // by the others; in row-id order each of them misses (cfg[4]: the short
-  // rows' tail columns alone are ~12 GB of 1 KB misses per multiply). Columns
-  // among the 32k most referenced stay L2-resident anyway and are not keyed.
-  const bool big_x = !order_faithful && uint64_t(v.n_cols) > (64ull << 10) &&
-                     !std::getenv("CBM_B200_NO_ROW_KEYS");
-  if (big_x && m > 1 && !ecol.empty()) {
-    std::vector<uint32_t> cnt(v.n_cols, 0);
-    for (uint32_t w : ecol) ++cnt[w & ~kSignBit];
-    uint32_t thr = 0;  // reference count of the 32k-th most referenced column
-    {
-      std::vector<uint32_t> c2(cnt);
-      const size_t k = std::min<size_t>(c2.size() - 1, 32u << 10);
-      std::nth_element(c2.begin(), c2.begin() + k, c2.end(), std::greater<uint32_t>());
-      thr = c2[k];
-    }
-    std::vector<uint32_t> key(m);
-    for (uint32_t x = 0; x < m; ++x) {
-      uint32_t k = x < v.n_cols ? x : v.n_cols - 1;
-      for (uint64_t j = eptr[x]; j < eptr[x + 1]; ++j) {
-        const uint32_t c = ecol[j] & ~kSignBit;
-        if (cnt[c] <= thr) {  // columns ascend: the first tail column is the smallest
-          k = std::min(k, c);
-          break;
-        }
-      }
-      key[x] = k;
-    }
-    for (uint32_t lv = 0; lv < L.n_levels; ++lv)
-      std::stable_sort(rows.begin() + L.level_ptr[lv], rows.begin() + L.level_ptr[lv + 1],
-                       [&](uint32_t a, uint32_t b) { return key[a] < key[b]; });
   }
 
   // split plan for long rows (default mode only)

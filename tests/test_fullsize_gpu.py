@@ -67,8 +67,12 @@ def test_cfg2_full_size_default_and_faithful(cfg2):
     assert a.n_rows == 235868
     x = wl.operand(a.n_cols)                       # N(0,1), d = 128
     want = ref_cbm(c).spmm(x, THREADS)
-    got, info = run(c, x)
+    got, info = run(c, x)                          # auto: hub-row panel + streaming kernel
+    assert info["hub_active"] and info["hub_rows"] == 128
     assert normwise_err(got, want) <= TOL
+    got_s, info_s = run(c, x, hub=0)               # streaming kernel alone
+    assert not info_s["hub_active"]
+    assert normwise_err(got_s, want) <= TOL
     got_f, _ = run(c, x, order_faithful=True)
     assert_bitwise(got_f, want, "cfg2 order-faithful vs reference spmm_into")
     # the restatement agrees with the compiled reference at full size too
@@ -79,8 +83,11 @@ def test_cfg2_full_size_integer_x_bitwise(cfg2):
     wl, a, c = cfg2
     x = P.generate_dense("int", a.n_cols, 64, 0xC0F61102, -8, 8)
     want = ref_cbm(c).spmm(x, THREADS)
-    got, _ = run(c, x)                              # default mode, lane groups at d=64
+    got, info = run(c, x)                           # default mode: hub panel on the tensor cores
+    assert info["hub_active"]
     assert_bitwise(got, want, "cfg2 default mode, integer X")
+    got, _ = run(c, x, hub=0)                       # lane groups at d=64
+    assert_bitwise(got, want, "cfg2 default mode without the hub panel, integer X")
 
 
 def test_cfg3_full_size_default_and_faithful(cfg3):
@@ -136,7 +143,8 @@ def test_cfg4_full_size_binary(cfg4):
     rc = ref_cbm(c)
     x = wl.operand(a.n_cols)
     want = rc.spmm(x, THREADS)
-    got, _ = run(c, x)
+    got, info = run(c, x)
+    assert info["hub_active"] and info["hub_entries"] > 20_000_000
     # the hub row has ~1.4M entries: the reference's sequential f32 sum is
     # itself ~3e-5 (normwise) from the exact product, so the device result is
     # judged against the f64 product on a column sample when it differs from
