@@ -1056,8 +1056,10 @@ void spmm_rest(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, float* 
     // entries to it in place and applies the row scale / ReLU
     if (ldx >= (int64_t(1) << 30))
       throw invalid_argument("spmm: leading dimension of X must be below 2^30");
-    dense_spmm(h, x, ldx, d, y, ldy, s);
-    device_spmm(h->cold, x, ldx, d, y, ldy, stream, relu, y, ldy);
+    uint32_t dbg = 0;  // dev timing only (CBM_B200_DENSE_DBG): 16 no cold kernel, 32 no dense kernel
+    if (const char* e = std::getenv("CBM_B200_DENSE_DBG")) dbg = uint32_t(std::atoi(e));
+    if (!(dbg & 32)) dense_spmm(h, x, ldx, d, y, ldy, s);
+    if (!(dbg & 16)) device_spmm(h->cold, x, ldx, d, y, ldy, stream, relu, y, ldy);
     h->last_launches = 1 + h->cold->last_launches;
     return;
   }

@@ -69,6 +69,8 @@ constexpr int kGatherers = DENSE_GATHERERS; // cp.async gatherers: warp i copies
 constexpr int kRowsPerGatherer = (kDenseK + kGatherers - 1) / kGatherers;
 constexpr int kMeta = 32;      // metadata ring depth (chunks)
 constexpr int kXSlots = 6;     // staged X' slices in shared memory (chunks in flight)
+constexpr int kGatherAhead = 3;  // a gatherer's copy groups in flight behind the signalled chunk
+constexpr int kMetaAhead = 8;    // the loader's record groups in flight
 constexpr int kGath0 = 2 + kExpanders;       // first gatherer warp
 constexpr int kProd0 = kGath0 + kGatherers;  // first converter warp
 constexpr int kEpi0 = kProd0 + 4 * kSets;    // first epilogue warp
@@ -190,8 +192,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// dev tool (CBM_B200_DENSE_TRACE): CTA 0's per-chunk timeline, 8 stamps per
+// (role, chunk): roles 0 MMA, 1 loader, 2 expander 0, 3 gatherer 0, 4 converter
+// set 0 / quarter 0, 5 epilogue quarter 0 (per unit)
+constexpr uint32_t kTraceChunks = 2048;
+#define DTRACE(role, g, k)                                                              \
+  do {                                                                                  \
+    if (p.trace && blockIdx.x == 0 && lane == 0 && (g) < kTraceChunks)                  \
+      p.trace[(size_t(role) * kTraceChunks + (g)) * 8 + (k)] = clock64();               \
+  } while (0)
+
 struct __align__(16) DenseBars {
-  uint64_t xfull[kStages], xempty[kStages], bfull[kStages], bempty[kStages];
+  uint64_t xfull[kStages], xempty[kStages], bfull[kStages];
   uint64_t accfull[2], accempty[2];
   uint64_t mfull[kMeta], mempty[kMeta];
   uint64_t sfull[kXSlots], sempty[kXSlots];
@@ -273,18 +285,17 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       mbar_init(&bars->xfull[s], 4);
       mbar_init(&bars->xempty[s], 1);
       mbar_init(&bars->bfull[s], 1);
-      mbar_init(&bars->bempty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&bars->accfull[a], 1);
       mbar_init(&bars->accempty[a], 4);
     }
     for (int m = 0; m < kMeta; ++m) {
-      mbar_init(&bars->mfull[m], 32);           // one cp.async arrive per loader lane
+      mbar_init(&bars->mfull[m], 1);            // the loader's lane 0, once the record has landed
       mbar_init(&bars->mempty[m], 1 + kGatherers + 4);  // expander, gatherers, converter set
     }
     for (int q = 0; q < kXSlots; ++q) {
-      mbar_init(&bars->sfull[q], 32 * kGatherers);  // one cp.async arrive per gatherer lane
+      mbar_init(&bars->sfull[q], kGatherers);   // one arrive per gatherer warp
       mbar_init(&bars->sempty[q], 4);           // the converter set's four warps
     }
     for (uint32_t q = 0; q < 16; ++q)
@@ -313,16 +324,11 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       tc_fence_after();
       for (uint32_t j = 0; j < t.w; ++j, ++g) {
         const uint32_t s = g % kStages, ph = (g / kStages) & 1;
-        unsigned long long t0 = 0, t1 = 0;
-        if (p.trace) t0 = clock64();
+        DTRACE(0, g, 0);
         mbar_wait(&bars->xfull[s], ph);
-        if (p.trace) t1 = clock64();
+        DTRACE(0, g, 1);
         mbar_wait(&bars->bfull[s], ph);
-        if (p.trace && blockIdx.x == 0 && lane == 0 && g < 4096) {
-          p.trace[3 * g] = t0;
-          p.trace[3 * g + 1] = t1;
-          p.trace[3 * g + 2] = clock64();
-        }
+        DTRACE(0, g, 2);
         tc_fence_after();
         if (lane == 0 && !(p.dbg & 2)) {
           const uint64_t bdesc = sw128_desc(saddr(bstage + s * kBBytes));
@@ -332,37 +338,54 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
             for (uint32_t ks = 0; ks < kDenseK / 8; ++ks)
               mma_tf32(tb + kAccCol + 128 * a, tb + kStageCol + 64 * s + 32 * piece + 8 * ks,
                        bdesc + 2 * ks, idesc, (j | piece | ks) != 0);
+          // one commit frees the stage for both operand producers (each
+          // tcgen05.commit costs the issuing thread ~150 cycles: DESIGN.md §6)
           tc_commit(&bars->xempty[s]);
-          tc_commit(&bars->bempty[s]);
           if (j + 1 == t.w) tc_commit(&bars->accfull[a]);
         } else if (lane == 0) {
           mbar_arrive(&bars->xempty[s]);
-          mbar_arrive(&bars->bempty[s]);
           if (j + 1 == t.w) mbar_arrive(&bars->accfull[a]);
         }
+        DTRACE(0, g, 3);
         __syncwarp();
       }
       ++nacc;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ metadata loader
+    // One arrive per record, not one per lane: hundreds of same-address
+    // mbarrier arrives per chunk were what bounded the kernel.
+    // The warp commits one cp.async group per record and signals record
+    // g - kMetaAhead once at most kMetaAhead newer groups are pending.
     ChunkIter it;
     it.init(p, 0, 1);
+    uint32_t issued = 0;
     while (!it.done) {
       const uint32_t m = it.g % kMeta, ph = (it.g / kMeta) & 1;
+      DTRACE(1, it.g, 0);
       mbar_wait(&bars->mempty[m], ph ^ 1);
+      DTRACE(1, it.g, 1);
       const unsigned char* src =
           reinterpret_cast<const unsigned char*>(p.meta + size_t(it.t.z + it.j) * kDenseMetaWords);
       const uint32_t dst = saddr(meta_ring) + m * kMetaBytes;
       for (uint32_t o = 16 * lane; o < kMetaBytes; o += 512)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + o), "l"(src + o)
                      : "memory");
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
-                       saddr(&bars->mfull[m]))
-                   : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      ++issued;
+      if (issued > kMetaAhead) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kMetaAhead) : "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->mfull[(issued - 1 - kMetaAhead) % kMeta]);
+      }
+      DTRACE(1, it.g, 2);
       it.next(p, 0, 1);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    if (lane == 0)
+      for (uint32_t k = issued > kMetaAhead ? issued - kMetaAhead : 0; k < issued; ++k)
+        mbar_arrive(&bars->mfull[k % kMeta]);
   } else if (warp >= 2 && warp < 2 + kExpanders) {
     // ------------------------------------------------------------ B expanders
     const uint32_t e = warp - 2;
@@ -371,14 +394,17 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
     while (!it.done) {
       const uint32_t s = it.g % kStages, ph = (it.g / kStages) & 1;
       const uint32_t m = it.g % kMeta, mph = (it.g / kMeta) & 1;
+      if (e == 0) DTRACE(2, it.g, 0);
       mbar_wait(&bars->mfull[m], mph);
+      if (e == 0) DTRACE(2, it.g, 1);
       const uint32_t* mk = meta_ring + m * kDenseMetaWords + 2 * kDenseK;
       uint32_t cur[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) cur[i] = mk[32 * i + lane];
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->mempty[m]);
-      mbar_wait(&bars->bempty[s], ph ^ 1);
+      mbar_wait(&bars->xempty[s], ph ^ 1);   // the stage's MMAs are done: B may be overwritten
+      if (e == 0) DTRACE(2, it.g, 2);
       // item = 32 k + lane: tile row r = 4 k + lane / 8, 16-byte chunk q of its
       // 128-byte line, stored at chunk q ^ (r & 7) (the 128-byte swizzle)
       const uint32_t q = lane & 7, rsub = lane >> 3;
@@ -400,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->bfull[s]);
+      if (e == 0) DTRACE(2, it.g, 3);
       it.next(p, e, kExpanders);
     }
   } else if (warp >= kGath0 && warp < kProd0) {
@@ -410,10 +437,13 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
     const uint32_t gi = warp - kGath0;
     ChunkIter it;
     it.init(p, 0, 1);
+    uint32_t issued = 0;   // chunks whose copies this warp has committed (= it.g)
     while (!it.done) {
       const uint32_t q = it.g % kXSlots, qph = (it.g / kXSlots) & 1;
       const uint32_t m = it.g % kMeta, mph = (it.g / kMeta) & 1;
+      if (gi == 0) DTRACE(3, it.g, 0);
       mbar_wait(&bars->mfull[m], mph);
+      if (gi == 0) DTRACE(3, it.g, 1);
       uint32_t cols[kRowsPerGatherer];
 #pragma unroll
       for (int r = 0; r < kRowsPerGatherer; ++r)
@@ -422,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->mempty[m]);
       mbar_wait(&bars->sempty[q], qph ^ 1);
+      if (gi == 0) DTRACE(3, it.g, 2);
       const uint32_t f0 = it.fb * kDenseFeat + 4 * lane;      // this lane's 4 features
       const uint32_t dst = saddr(xslot) + q * kXBytes + 16 * lane;
       const bool full = f0 + 4 <= p.d && (p.ldx & 3) == 0 &&
@@ -446,12 +477,23 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
           }
         }
       }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
-                       saddr(&bars->sfull[q]))
-                   : "memory");
+      // one arrive per warp and slot (see the metadata loader): chunk
+      // g - kGatherAhead is signalled once at most kGatherAhead newer groups pend
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      ++issued;
+      if (issued > kGatherAhead) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kGatherAhead) : "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->sfull[(issued - 1 - kGatherAhead) % kXSlots]);
+      }
+      if (gi == 0) DTRACE(3, it.g, 3);
       it.next(p, 0, 1);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    if (lane == 0)
+      for (uint32_t k = issued > kGatherAhead ? issued - kGatherAhead : 0; k < issued; ++k)
+        mbar_arrive(&bars->sfull[k % kXSlots]);
   } else if (warp >= kProd0 && warp < kEpi0) {
     // ------------------------------------------------------------ X' converters
     // set j owns chunks g = j mod kSets: staged slice -> (scale) -> hi/lo split
@@ -463,11 +505,16 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       const uint32_t s = it.g % kStages, ph = (it.g / kStages) & 1;
       const uint32_t m = it.g % kMeta, mph = (it.g / kMeta) & 1;
       const uint32_t q = it.g % kXSlots, qph = (it.g / kXSlots) & 1;
+      const bool tr = set == 0 && quarter == 0;
+      if (tr) DTRACE(4, it.g, 0);
       mbar_wait(&bars->mfull[m], mph);
+      if (tr) DTRACE(4, it.g, 1);
       const float* sc = reinterpret_cast<const float*>(meta_ring + m * kDenseMetaWords + kDenseK);
       mbar_wait(&bars->sfull[q], qph);
+      if (tr) DTRACE(4, it.g, 2);
       const float* xs = reinterpret_cast<const float*>(xslot + q * kXBytes) + quarter * 32 + lane;
       mbar_wait(&bars->xempty[s], ph ^ 1);
+      if (tr) DTRACE(4, it.g, 3);
       tc_fence_after();
       const uint32_t taddr = tb + ((quarter * 32) << 16) + kStageCol + 64 * s;
 #pragma unroll
@@ -484,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
         tmem_st8(taddr + 32 + 8 * part, lo);
       }
       __syncwarp();
+      if (tr) DTRACE(4, it.g, 4);
       if (lane == 0) {
         mbar_arrive(&bars->sempty[q]);
         mbar_arrive(&bars->mempty[m]);
@@ -492,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->xfull[s]);
+      if (tr) DTRACE(4, it.g, 5);
       it.next(p, set, kSets);
     }
   } else if (warp >= kEpi0) {
@@ -510,7 +559,9 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
         continue;
       }
       const uint32_t a = nacc & 1;
+      if (quarter == 0) DTRACE(5, nacc, 0);
       mbar_wait(&bars->accfull[a], (nacc >> 1) & 1);
+      if (quarter == 0) DTRACE(5, nacc, 1);
       tc_fence_after();
 #pragma unroll 1
       for (uint32_t c0 = 0; c0 < kDenseRows; c0 += 32) {
@@ -527,6 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
             if (c0 + j < t.y) __stcs(ybase + (long long)(c0 + j) * p.ldy, __uint_as_float(r[j]));
         }
       }
+      if (quarter == 0) DTRACE(5, nacc, 2);
       ++nacc;
     }
   }
@@ -662,8 +714,8 @@ void dense_launch(DeviceMatrix* h, const uint32_t* tiles, const uint32_t* meta, 
   p.trace = nullptr;
   const char* trace_path = std::getenv("CBM_B200_DENSE_TRACE");
   if (trace_path) {
-    ck(cudaMalloc(&p.trace, 3 * 4096 * 8), "trace");
-    ck(cudaMemsetAsync(p.trace, 0, 3 * 4096 * 8, s), "trace");
+    ck(cudaMalloc(&p.trace, 6 * kTraceChunks * 8 * 8), "trace");
+    ck(cudaMemsetAsync(p.trace, 0, 6 * kTraceChunks * 8 * 8, s), "trace");
   }
   const uint64_t units = uint64_t(n_tiles) * p.n_fb;
   if (units >= 0xFFFFFFFFull) throw invalid_argument("spmm: too many dense-block units");
@@ -682,15 +734,20 @@ void dense_launch(DeviceMatrix* h, const uint32_t* tiles, const uint32_t* meta, 
     dense_kernel<false><<<grid, kThreads, smem, s>>>(p);
   }
   ck(cudaGetLastError(), "dense_kernel launch");
-  if (trace_path) {  // dev tool: per chunk of CTA 0: before xfull, after xfull, after bfull
-    std::vector<unsigned long long> t(3 * 4096);
+  if (trace_path) {  // dev tool: CTA 0's stamps, one line per (role, chunk)
+    std::vector<unsigned long long> t(6 * kTraceChunks * 8);
     ck(cudaStreamSynchronize(s), "trace");
     ck(cudaMemcpy(t.data(), p.trace, t.size() * 8, cudaMemcpyDeviceToHost), "trace");
     cudaFree(p.trace);
     if (FILE* f = std::fopen(trace_path, "a")) {
       std::fprintf(f, "call\n");
-      for (int g = 0; g < 4096 && t[3 * g]; ++g)
-        std::fprintf(f, "%d %llu %llu %llu\n", g, t[3 * g], t[3 * g + 1], t[3 * g + 2]);
+      for (uint32_t role = 0; role < 6; ++role)
+        for (uint32_t g = 0; g < kTraceChunks; ++g) {
+          const unsigned long long* q = &t[(size_t(role) * kTraceChunks + g) * 8];
+          if (!q[0]) continue;
+          std::fprintf(f, "%u %u %llu %llu %llu %llu %llu %llu\n", role, g, q[0], q[1], q[2], q[3],
+                       q[4], q[5]);
+        }
       std::fclose(f);
     }
   }

@@ -307,9 +307,10 @@ void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, 
   }
   const uint64_t bytes = (uint64_t(L.n_cols) + L.n_rows) * d * sizeof(float);
   // Column chunks (16-byte aligned): the first chunk's H2D and the last
-  // chunk's D2H cannot overlap anything, so those two are narrow (d/8) and
-  // the middle is cut in three (tools/probe_e2e.py: uniform x4 1109 us,
-  // x8 1151 us on cfg[1]; rows narrower than 64 floats slow the 2D copies).
+  // chunk's D2H cannot overlap anything, so for d >= 512 those two are narrow
+  // (d/8) and the middle is cut in three (tools/probe_e2e.py: uniform x4
+  // 1109 us, x8 1151 us on cfg[1]); rows narrower than 64 floats slow the 2D
+  // copies, so narrower operands take uniform 64-column chunks.
   std::vector<std::pair<uint32_t, uint32_t>> parts;  // (first column, width)
   auto r4 = [](uint32_t v) { return (v + 3) & ~3u; };
   uint32_t chunks = 1;
@@ -327,7 +328,7 @@ void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, 
     }
     if (c0 < d) parts.emplace_back(c0, d - c0);
     if (parts.size() > kHostChunks) throw invalid_argument("CBM_B200_HOST_WIDTHS: too many chunks");
-  } else if (chunks == 5 && !std::getenv("CBM_B200_HOST_CHUNKS")) {  // d >= 256
+  } else if (chunks == 5 && !std::getenv("CBM_B200_HOST_CHUNKS") && d >= 512) {
     const uint32_t edge = r4(d / 8), rest = d - 2 * edge, mid = r4((rest + 2) / 3);
     uint32_t c0 = 0;
     const uint32_t m3 = (rest - 2 * mid) & ~3u;  // every chunk starts 16-byte aligned
@@ -336,6 +337,11 @@ void device_spmm_host(DeviceMatrix* h, const float* x, int64_t ldx, uint32_t d, 
       c0 += w;
     }
   } else {
+    // 256 <= d < 512: uniform chunks of 64 columns. Strided 2-D copies of rows
+    // narrower than 64 floats run well below the link rate (cfg[4], 2.5 GB each
+    // way: 32/64/64/64/32 81.8 ms, 4 x 64 64.7 ms, 8 x 32 90.2 ms; the floor
+    // for fully overlapped copies is 53.5 ms: profiles/r02l_e2e_sweep.txt)
+    if (chunks == 5 && !std::getenv("CBM_B200_HOST_CHUNKS")) chunks = std::min(kHostChunks, (d + 63) / 64);
     const uint32_t cw = r4((d + chunks - 1) / chunks);
     for (uint32_t c0 = 0; c0 < d; c0 += cw) parts.emplace_back(c0, std::min(cw, d - c0));
   }

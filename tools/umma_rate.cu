@@ -21,6 +21,7 @@ __global__ void rate(unsigned long long* out, int iters) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* b = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t dummy;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < N * 32; i += blockDim.x) reinterpret_cast<uint32_t*>(b)[i] = 0;
@@ -30,6 +31,7 @@ __global__ void rate(unsigned long long* out, int iters) {
   }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&dummy)), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -67,6 +69,12 @@ __global__ void rate(unsigned long long* out, int iters) {
     const uint32_t acol = N == 256 ? 256 : 384;   // A columns after the accumulator
     unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      if (CONT >= 10 && (i & 1) == 0 && i) {   // CONT - 10 commits per 8 MMAs (dummy barrier)
+#pragma unroll
+        for (int c = 0; c < CONT - 10; ++c)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&dummy)));
+      }
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
         const uint32_t acc = (i | ks) != 0;
@@ -122,5 +130,7 @@ int main() {
   run<1, 256>("bf16 M128 N256 K16", 148);
   run<0, 128, 1>("tf32 N128 + smem traffic (12 warps)", 1, 512);
   run<0, 128, 2>("tf32 N128 + tmem st traffic (12 warps)", 1, 512);
+  run<0, 128, 11>("tf32 N128, 1 commit per 8 MMAs", 1);
+  run<0, 128, 13>("tf32 N128, 3 commits per 8 MMAs", 1);
   return 0;
 }
