@@ -24,7 +24,8 @@ __global__ void rate(unsigned long long* out, int iters) {
   __shared__ __align__(8) uint64_t dummy;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < N * 32; i += blockDim.x) reinterpret_cast<uint32_t*>(b)[i] = 0;
+  for (int i = threadIdx.x; i < N * 32; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(b)[i] = CONT == 20 ? (((i * 2654435761u) >> 13) & 1 ? 0x3F800000u : 0u) : 0u;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -39,6 +40,21 @@ __global__ void rate(unsigned long long* out, int iters) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tb = tbase;
+  if (CONT == 20 && warp < 4) {   // A: pseudo-random tf32 values in every operand column
+    for (int c = 256; c < 512; c += 8) {
+      uint32_t r[8];
+      for (int k = 0; k < 8; ++k)
+        r[k] = (0x3F000000u + ((threadIdx.x * 40503u + (c + k) * 2654435761u) & 0x00FFE000u)) ^ ((c + k) & 1 ? 0x80000000u : 0u);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
+                       tb + ((32 * warp) << 16) + c),
+                   "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
   __shared__ __align__(16) float junk[4][32 * 64];
   __shared__ volatile int stop;
   if (threadIdx.x == 0) stop = 0;
@@ -130,6 +146,9 @@ int main() {
   run<1, 256>("bf16 M128 N256 K16", 148);
   run<0, 128, 1>("tf32 N128 + smem traffic (12 warps)", 1, 512);
   run<0, 128, 2>("tf32 N128 + tmem st traffic (12 warps)", 1, 512);
+  run<0, 128, 20>("tf32 N128, random A / 0-1 B data, 1 CTA", 1);
+  run<0, 128, 20>("tf32 N128, random A / 0-1 B data, 148 CTAs", 148);
+  run<1, 128, 20>("bf16 N128, random A / 0-1 B data, 148 CTAs", 148);
   run<0, 128, 11>("tf32 N128, 1 commit per 8 MMAs", 1);
   run<0, 128, 13>("tf32 N128, 3 commits per 8 MMAs", 1);
   return 0;
