@@ -517,6 +517,32 @@ def run_north_star(args, P, O, WL, dev, stream, flush):
     out["unit"] = UNIT
     out["roofline"] = roofline_for(info, ms, a.n_rows, a.n_cols, wl.d, True, "cfg3")
     out["gpu_launches_per_step"] = int(op.info()["launches_per_call"])
+    # configs[3] as BASELINE.json states it: 2-layer GCN inference
+    # A_hat relu(A_hat X W0) W1 (gcn.cpp:22-33), X n x 128, W0 128 x 256, W1 256 x 112
+    # (Glorot, seeded), the dense products by our GEMM kernel, A_hat. by the CBM path
+    try:
+        xg = P.generate_dense("normal", a.n_cols, 128, 0xC0F61003)
+        w0 = P.generate_dense("glorot", 128, 256, 0xC0F62003)
+        w1 = P.generate_dense("glorot", 256, 112, 0xC0F62103)
+        tx, t0, t1 = (torch.from_numpy(t).to(dev) for t in (xg, w0, w1))
+        got = op.gcn_forward(tx, t0, t1, stream)
+        torch.cuda.synchronize()
+        gcn = {"shape": "X n x 128, W0 128 x 256, W1 256 x 112"}
+        if O is not None and O.ref_available():
+            want = rc.gcn_forward(xg, w0, w1, args.threads)
+            den = float(np.abs(want).max()) or 1.0
+            err = float(np.abs(got.cpu().numpy().astype(np.float64) - want).max()) / den
+            gcn["parity"] = {"ok": err <= TOL, "normwise_err": err,
+                             "against": "reference gcn_forward (oracle/_ref)"}
+        for _ in range(3):
+            op.gcn_forward(tx, t0, t1, stream)
+        torch.cuda.synchronize()
+        gcn["ms_per_forward"] = float(statistics.mean(time_steps(
+            lambda: op.gcn_forward(tx, t0, t1, stream), min(args.steps, 20), stream, flush)))
+        gcn["gpu_launches_per_forward"] = int(op.info()["launches_per_call"])
+        out["gcn_forward"] = gcn
+    except Exception as e:  # an extra key must never take the bench line down
+        out["gcn_forward"] = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
     op.close()
     return out
 

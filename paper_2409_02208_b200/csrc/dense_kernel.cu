@@ -322,31 +322,44 @@ __global__ void __launch_bounds__(kThreads, 1) dense_kernel(const DenseParams p)
       const uint32_t a = nacc & 1;
       mbar_wait(&bars->accempty[a], ((nacc >> 1) & 1) ^ 1);
       tc_fence_after();
-      for (uint32_t j = 0; j < t.w; ++j, ++g) {
-        const uint32_t s = g % kStages, ph = (g / kStages) & 1;
-        DTRACE(0, g, 0);
-        mbar_wait(&bars->xfull[s], ph);
-        DTRACE(0, g, 1);
-        mbar_wait(&bars->bfull[s], ph);
-        DTRACE(0, g, 2);
+      // Two chunks per turn (kStages = 4: two stages in the MMAs, two being
+      // filled): the issuing lane blocks ~830 cycles per chunk inside its eight
+      // issues (the MMAs' real-data rate) and spends another ~400 in the operand
+      // waits and the loop around them; issuing a pair back to back halves the
+      // number of those gaps.
+      for (uint32_t j = 0; j < t.w;) {
+        const uint32_t n2 = (j + 1 < t.w && !(p.dbg & 256)) ? 2u : 1u;
+        for (uint32_t q = 0; q < n2; ++q) {
+          const uint32_t s = (g + q) % kStages, ph = ((g + q) / kStages) & 1;
+          DTRACE(0, g + q, 0);
+          mbar_wait(&bars->xfull[s], ph);
+          DTRACE(0, g + q, 1);
+          mbar_wait(&bars->bfull[s], ph);
+          DTRACE(0, g + q, 2);
+        }
         tc_fence_after();
         if (lane == 0 && !(p.dbg & 2)) {
-          const uint64_t bdesc = sw128_desc(saddr(bstage + s * kBBytes));
+          for (uint32_t q = 0; q < n2; ++q) {
+            const uint32_t s = (g + q) % kStages;
+            const uint64_t bdesc = sw128_desc(saddr(bstage + s * kBBytes));
 #pragma unroll
-          for (uint32_t piece = 0; piece < 2; ++piece)
+            for (uint32_t piece = 0; piece < 2; ++piece)
 #pragma unroll
-            for (uint32_t ks = 0; ks < kDenseK / 8; ++ks)
-              mma_tf32(tb + kAccCol + 128 * a, tb + kStageCol + 64 * s + 32 * piece + 8 * ks,
-                       bdesc + 2 * ks, idesc, (j | piece | ks) != 0);
-          // one commit frees the stage for both operand producers
-          tc_commit(&bars->xempty[s]);
-          if (j + 1 == t.w) tc_commit(&bars->accfull[a]);
+              for (uint32_t ks = 0; ks < kDenseK / 8; ++ks)
+                mma_tf32(tb + kAccCol + 128 * a, tb + kStageCol + 64 * s + 32 * piece + 8 * ks,
+                         bdesc + 2 * ks, idesc, (j | q | piece | ks) != 0);
+            // one commit frees the stage for both operand producers
+            tc_commit(&bars->xempty[s]);
+          }
+          if (j + n2 == t.w) tc_commit(&bars->accfull[a]);
         } else if (lane == 0) {
-          mbar_arrive(&bars->xempty[s]);
-          if (j + 1 == t.w) mbar_arrive(&bars->accfull[a]);
+          for (uint32_t q = 0; q < n2; ++q) mbar_arrive(&bars->xempty[(g + q) % kStages]);
+          if (j + n2 == t.w) mbar_arrive(&bars->accfull[a]);
         }
         DTRACE(0, g, 3);
         __syncwarp();
+        j += n2;
+        g += n2;
       }
       ++nacc;
     }

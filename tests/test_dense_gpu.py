@@ -31,7 +31,7 @@ def community(n, size, p_in, p_out, seed):
     return P.generate_graph("community", [n, size, p_in, p_out], seed)
 
 
-@pytest.mark.parametrize("d", [32, 64, 96, 128, 200, 256, 260])
+@pytest.mark.parametrize("d", [32, 33, 50, 64, 96, 128, 200, 256, 260])
 def test_binary_integer_x_bitwise(d):
     a = community(1000, 100, 0.5, 0.01, 21)
     c = P.build_cbm(a, 0, 4)

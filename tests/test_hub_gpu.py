@@ -33,7 +33,7 @@ def run(c, x, relu=False, **opt):
     return y, info
 
 
-@pytest.mark.parametrize("d", [32, 64, 100, 128, 256, 260])
+@pytest.mark.parametrize("d", [32, 33, 50, 64, 100, 128, 256, 260])
 def test_binary_integer_x_bitwise(d):
     a = overlay(6000, 20000, 8, 41)
     c = P.build_cbm(a, 8, 4)
