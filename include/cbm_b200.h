@@ -126,7 +126,7 @@ typedef struct cbm_b200_options {
                                 in a fixed tree order (bit-exact on integer X,
                                 ~1 ulp-level on Gaussian X) */
   uint32_t split_threshold;  /* deltas per row before splitting (0 = auto: a
-                                power of two in [32, 256], ~1/8 of a resident
+                                power of two in [32, 1024], ~1/8 of a resident
                                 warp's share of the deltas) */
   uint32_t chunk;            /* deltas per chunk (0 = auto: max(32, split/4)) */
   int32_t prescale;          /* normalized only: -1 auto, 0 off, 1 pre-scale X

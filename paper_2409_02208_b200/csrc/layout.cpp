@@ -311,14 +311,17 @@ Layout plan_layout(const cbm_b200_cbm_view& v, bool order_faithful, uint32_t spl
 
   // split plan for long rows (default mode only)
   // auto: split rows longer than ~1/8 of a warp's share of the deltas (a
-  // power of two in [32, 256]): small matrices need short pieces to spread
+  // power of two in [32, 1024]): small matrices need short pieces to spread
   // over the grid, large ones lose more to the partial-sum hand-offs than
   // they gain in balance (tools/probe_split.py: cfg[1] best at 32, cfg[2] and
   // cfg[3] at 256 / 64)
   if (split_threshold == 0) {
     const uint64_t share = L.nnz_effective / std::max<uint32_t>(1, warps_hint) / 8;
+    // (up to 1024 on very large matrices: cfg[4] with the hub rows on the tensor
+    // cores measures 1-2% better at 1024 / 256-entry pieces than at 256 / 64,
+    // profiles/r02t_cfg4_split_chunk_sweep.jsonl; cfg[2]'s share keeps it at 256)
     split_threshold = 32;
-    while (split_threshold < 256 && uint64_t(split_threshold) * 2 <= share) split_threshold *= 2;
+    while (split_threshold < 1024 && uint64_t(split_threshold) * 2 <= share) split_threshold *= 2;
   }
   if (chunk == 0) chunk = std::max<uint32_t>(32, split_threshold / 4);
   if (chunk > split_threshold) chunk = split_threshold;
