@@ -29,6 +29,13 @@ cpu_baseline : the reference's spmm_into AND csr_spmm_into (oracle/_ref) on
            this host, pinned like pin_to_cores (cbm_main.cpp:92-104), at
            T = all host threads and T = 1; runtime_reduction_pct as
            cbm_main.cpp:276-283.
+comparators : gpu_csr_comparator (the uncompressed matrix through the same
+           kernels: the paper's runtime reduction on this GPU) and
+           cusparse_comparator (cuSPARSE CSR SpMM fp32, the vendor bar);
+           reported only, never on the product path.
+north_star_cfg3 : configs[3] in the same run: A_hat.X at d=256 (value, roofline,
+           parity) and its 2-layer GCN forward (gcn.cpp:22-33) timed and
+           checked against the reference's gcn_forward.
 """
 from __future__ import annotations
 
